@@ -1,0 +1,196 @@
+/*
+ * dbsa_b200.h -- C ABI of libdbsa_sm100a.so, the B200 (sm_100a) hot path of
+ * Dynamic Block-Sparse Attention (arXiv 2503.08640).
+ *
+ * The reference package (/root/reference/pkg/src/dbsa) has no FFI: its only
+ * numeric seam is `kernels.masked_attention` (kernels.py:73-100), called once
+ * per (layer, kv-head) from `model._forward` (model.py:338-351), and its
+ * data-movement / selection steps are plain numpy (kvstore.py:70-106,
+ * kvstore.py:188-221, retrieval.py:352-388).  Each entry point below replaces
+ * one of those sites; the Python package `paper_2503_08640_b200` binds them
+ * with ctypes behind the reference's own Python API.
+ *
+ * Conventions
+ *   - extern "C", plain pointers and int64_t sizes; no torch types.
+ *   - every device buffer is allocated and owned by the caller; the library
+ *     never allocates persistent device memory.
+ *   - every call takes an explicit cudaStream_t (passed as void*) and is
+ *     asynchronous on it; the library keeps no global mutable state, so calls
+ *     are reentrant across host threads (reference threading contract:
+ *     bench.py:147-150, pipeline.py:322-327).
+ *   - return 0 on success; a non-zero DBSA_ERR_* code maps 1:1 onto the
+ *     reference exception hierarchy (errors.py:4-29); dbsa_last_error()
+ *     returns the thread-local message of the last failure.
+ *
+ * KV page pool layout (component K2, replaces SegmentedKVCache storage,
+ * kvstore.py:36-106).  One pool per cache, bf16:
+ *   K   [L][Hkv][rows][HDP]   keys ROTATED at their original positions
+ *   V^T [L][Hkv][HDP][rows]   values, transposed (token dim contiguous)
+ * rows = n_pages * 64; a group (block) owns a contiguous run of whole pages,
+ * pages never span groups; HDP = head_dim padded to {16,32,64,128}, padding
+ * columns are zero.  Selecting groups is pointer indirection into this pool
+ * (segment tables below), never a copy (replaces assemble, kvstore.py:188-221).
+ */
+#ifndef DBSA_B200_H
+#define DBSA_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DBSA_ABI_VERSION 1
+#define DBSA_PAGE_TOKENS 64
+
+/* Error codes -> reference exceptions (errors.py:4-29). */
+#define DBSA_OK 0
+#define DBSA_ERR_SHAPE 1       /* ShapeError       errors.py:8  */
+#define DBSA_ERR_MASK 2        /* MaskError        errors.py:12 */
+#define DBSA_ERR_CONFIG 3      /* ConfigError      errors.py:16 */
+#define DBSA_ERR_VALIDATION 4  /* ValidationError  errors.py:20 */
+#define DBSA_ERR_COMPAT 5      /* CompatibilityError errors.py:24 */
+#define DBSA_ERR_CUDA 6        /* RuntimeError (driver / launch failure) */
+
+/* Segment kinds. */
+#define DBSA_SEG_FULL 0 /* context chunk: every key visible to every row */
+#define DBSA_SEG_SELF 1 /* the rows' own tokens: causal, optionally a tree */
+
+/* One unit of attention work = one CTA: up to 128*num_m query rows of one kv
+ * head (token-major GQA packing: row r = token (r / gs), head (r % gs)),
+ * attending to the segment list [seg_begin, seg_end). */
+typedef struct DbsaAttnWork {
+  int32_t q_tok0;    /* first token of the slab (index into q / tok_* arrays) */
+  int32_t n_tok;     /* tokens in the slab; rows = n_tok * gs */
+  int32_t self_tok0; /* token index whose local self index is 0 */
+  int32_t kv_head;
+  int32_t seg_begin;
+  int32_t seg_end;
+  int32_t prefix;   /* SELF keys with local index < prefix are visible to all rows */
+  int32_t out_mode; /* 0: normalized bf16 into out; 1: fp32 partial + lse */
+  int64_t part_row0; /* partial row base (out_mode 1) */
+} DbsaAttnWork;
+
+/* A run of consecutive KV rows of one plane. */
+typedef struct DbsaAttnSeg {
+  int32_t src;   /* 0 = pool planes, 1 = aux planes */
+  int32_t layer; /* layer coordinate inside the planes */
+  int32_t row0;  /* first row */
+  int32_t n_tok; /* > 0 */
+  int32_t kind;  /* DBSA_SEG_FULL / DBSA_SEG_SELF */
+  int32_t rot;   /* row of rot_table applied to the queries, -1 = none */
+  int32_t pad0, pad1;
+} DbsaAttnSeg;
+
+/* Components K1 (stage-1 block-sparse prefill) and K3 (stage-2 split-KV
+ * query attention) -- one tcgen05/TMEM/TMA kernel.  Replaces
+ * kernels.masked_attention (kernels.py:73-100) as called from
+ * model._forward (model.py:327-351) including the rotary application of
+ * model.py:327-328: queries are read UNROTATED from `q` and rotated in the
+ * prologue at tok_pos[t] (rope_table), composed with the per-segment shift
+ * rot_table[seg.rot] (the stage-2 re-positioning of kvstore.py:201-218 moved
+ * to the query side: R(p_q - delta) q . R(p_orig) k == R(p_q) q . R(p_new) k).
+ */
+typedef struct DbsaAttnArgs {
+  const void *q;        /* bf16, element (t, head, d) at q[t*q_tok_stride + head*head_dim + d] */
+  int64_t q_tok_stride; /* elements */
+  const int32_t *tok_pos; /* [tokens] rotary position of each query token */
+  const int32_t *tok_lo;  /* [tokens] tree mask: lowest visible non-prefix SELF key (local); NULL = 0 */
+  const float *rope_table; /* float2 [rope_rows][head_dim/2]: cos, sin of pos*theta^(-2i/hd) */
+  int64_t rope_rows;
+  const float *rot_table;  /* float2 [n_rot][head_dim/2]: cos, sin of (-delta)*theta^(-2i/hd) */
+  const void *k_pool, *v_pool; /* bf16 planes, see layout above */
+  int64_t pool_rows;
+  int32_t pool_layers;
+  const void *k_aux, *v_aux; /* second plane set (stage-2 new tokens); may alias pool */
+  int64_t aux_rows;
+  int32_t aux_layers;
+  int32_t n_heads, n_kv_heads, head_dim, hd_pad;
+  float scale; /* softmax scale, 1/sqrt(head_dim) (model.py:315) */
+  int32_t num_m; /* 1 or 2 M-tiles of 128 rows per work */
+  const DbsaAttnWork *works; /* device */
+  int32_t n_works;
+  const DbsaAttnSeg *segs; /* device */
+  void *out; /* bf16, element (t, head, d) at out[t*out_tok_stride + head*head_dim + d] */
+  int64_t out_tok_stride;
+  float *part_o;   /* fp32 [rows][head_dim] (out_mode 1) */
+  float *part_lse; /* fp32 [rows], natural-log LSE (out_mode 1) */
+} DbsaAttnArgs;
+int dbsa_attention(const DbsaAttnArgs *args, void *stream);
+
+/* Component K3m: combine split partials, lse = log sum exp(lse_s),
+ * O = sum exp(lse_s - lse) O_s -- reproduces the single softmax over the
+ * concatenated key set of kernels.py:52-56. */
+typedef struct DbsaMergeGroup {
+  int64_t part_row0; /* partial row of split 0, row 0 */
+  int32_t rows;      /* rows per split */
+  int32_t n_splits;
+  int32_t q_tok0; /* output token of row 0 */
+  int32_t kv_head;
+} DbsaMergeGroup;
+typedef struct DbsaMergeArgs {
+  const float *part_o, *part_lse;
+  const DbsaMergeGroup *groups; /* device */
+  int32_t n_groups;
+  int32_t max_rows;
+  int32_t n_heads, n_kv_heads, head_dim;
+  void *out; /* bf16 */
+  int64_t out_tok_stride;
+} DbsaMergeArgs;
+int dbsa_lse_merge(const DbsaMergeArgs *args, void *stream);
+
+/* Component K2w: page write of one layer's K (rotated at tok_pos) and V
+ * (transposed) for a set of 64-token pages.  Replaces the per-block copy of
+ * SegmentedKVCache.append_block (kvstore.py:103-105) and the rotary
+ * transform of model.rope_rotate_heads (model.py:222-239) for keys. */
+typedef struct DbsaPage {
+  int32_t tok0;  /* first token of the page in the qkv buffer */
+  int32_t n_tok; /* 1..64 valid tokens; the rest of the page is zeroed */
+  int32_t row0;  /* destination row (multiple of 64) */
+  int32_t pad;
+} DbsaPage;
+typedef struct DbsaKvWriteArgs {
+  const void *k_src, *v_src; /* bf16, (t, kvh, d) at src[t*src_tok_stride + kvh*head_dim + d] */
+  int64_t src_tok_stride;
+  const int32_t *tok_pos;
+  const float *rope_table;
+  int64_t rope_rows;
+  const DbsaPage *pages; /* device */
+  int32_t n_pages;
+  void *k_dst, *v_dst; /* planes */
+  int64_t dst_rows;
+  int32_t dst_layers, layer;
+  int32_t n_kv_heads, head_dim, hd_pad;
+} DbsaKvWriteArgs;
+int dbsa_kv_write(const DbsaKvWriteArgs *args, void *stream);
+
+/* Rotary table: table[p][i] = (cos, sin)(p * inv_freq[i]) with the angle
+ * formed in float64 exactly as model.rope_angles (model.py:205-209). */
+int dbsa_rope_table(float *table, int64_t rows, const double *inv_freq, int32_t half,
+                    int64_t pos0, void *stream);
+
+/* Component K4: per query, [0] + top-(budget-1) of units 1..n-1 under the
+ * total order (score desc, id asc), then re-ordered by `ordering`
+ * (0 in-order, 1 low-to-high, 2 reverse) -- bit-exact replacement of
+ * retrieval.select + retrieval.order (retrieval.py:352-388). */
+int dbsa_topk_select(const double *scores, int64_t n_queries, int64_t n_units, int64_t budget,
+                     int32_t ordering, int32_t *out_ids, void *stream);
+
+/* Dense-path helpers fused for the pre-norm block (model.py:321,355,358;
+ * kernels.py:103-123): RMSNorm fp32 -> bf16, and silu(gate) * up. */
+int dbsa_rmsnorm(const float *x, const float *weight, void *out, int64_t rows, int64_t dim,
+                 float eps, void *stream);
+int dbsa_silu_mul(const void *gate_up, void *out, int64_t rows, int64_t ffn, void *stream);
+
+/* Label scoring gather (model.py:414-417,441-443): for each scored row r,
+ * logprob[r] = logits[r, target[r]] - logsumexp(logits[r, :]) in fp32. */
+int dbsa_label_logprob(const float *logits, int64_t rows, int64_t vocab, const int32_t *target,
+                       float *out, void *stream);
+
+int dbsa_abi_version(void);
+const char *dbsa_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DBSA_B200_H */

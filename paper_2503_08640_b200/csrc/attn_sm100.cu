@@ -1,0 +1,517 @@
+// attn_sm100.cu -- K1 (stage-1 block-sparse prefill) and K3 (stage-2 split-KV
+// query attention) of DBSA as ONE warp-specialised tcgen05/TMEM/TMA kernel.
+//
+// Reference semantics: kernels.masked_attention (kernels.py:73-100) called per
+// (layer, kv head) from model._forward (model.py:327-351): q rotated at its own
+// position and scaled by 1/sqrt(hd), softmax over the allowed keys only
+// (masked entries exactly 0), then P.V.  Here a CTA owns up to 128*NUM_M query
+// rows of one kv head (GQA heads packed token-major, the stacking of
+// model.py:338-342) and streams the keys of a SEGMENT LIST through an online
+// softmax, so the block-sparse mask of masks.block_mask_rows (masks.py:164-177)
+// is never materialised:
+//   stage 1: segments = [sink, prev-j groups] (FULL) + the group itself (SELF,
+//            causal)                       -- pipeline.encode_blocks (pipeline.py:203-229)
+//   stage 2: segments = selected chunks (FULL, each with its query-side RoPE
+//            shift) + the query/label tokens (SELF, causal tree)
+//                                          -- Runner.infer / score_label (pipeline.py:410-421, model.py:420-443)
+//
+// Roles (warp-specialised, one CTA per work item):
+//   warp 0      TMA producer: K tile [64 x HDP] + V^T tile [HDP x 64] per stage
+//   warp 1      MMA issuer (one thread): S = Q K^T and O += P V on tcgen05
+//   warp 2      TMEM allocator
+//   warps 4..   softmax warpgroups, one per 128-row M tile, one row per thread:
+//               Q prologue (load + RoPE + swizzled st.shared), S from TMEM,
+//               online softmax with lazy O rescale, P -> smem, epilogue.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+
+#include "../../include/dbsa_b200.h"
+#include "dbsa_internal.h"
+#include "sm100_ptx.cuh"
+
+namespace dbsa {
+
+constexpr int kBN = 64;  // keys per tile
+
+template <int HDP, int NUM_M>
+struct AttnCfg {
+  static constexpr int QSW = HDP >= 64 ? 128 : HDP * 2;   // swizzle width of Q / K rows (bytes)
+  static constexpr int KATOM = HDP >= 64 ? 64 : HDP;      // K-dim elements per atom column
+  static constexpr int NATOM = HDP / KATOM;               // atom columns along head_dim
+  static constexpr int Q_BYTES = 128 * HDP * 2;
+  static constexpr int P_BYTES = 128 * kBN * 2;
+  static constexpr int K_BYTES = kBN * HDP * 2;
+  static constexpr int V_BYTES = HDP * kBN * 2;
+  static constexpr int STAGE_BYTES = K_BYTES + V_BYTES;
+  static constexpr int FIXED = NUM_M * (Q_BYTES + P_BYTES);
+  static constexpr int BAR_BYTES = 1024;
+  static constexpr int SMEM_LIMIT = 232448 - 1024 /*align slack*/;
+  static constexpr int STAGES_FIT = (SMEM_LIMIT - FIXED - BAR_BYTES) / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_FIT > 6 ? 6 : STAGES_FIT;
+  static constexpr int SMEM = FIXED + STAGES * STAGE_BYTES + BAR_BYTES + 1024;
+  static constexpr int THREADS = 128 + 128 * NUM_M;
+  static constexpr int TMEM_NEED = NUM_M * (HDP + kBN);
+  static constexpr int TMEM_COLS =
+      TMEM_NEED <= 32 ? 32 : TMEM_NEED <= 64 ? 64 : TMEM_NEED <= 128 ? 128 : TMEM_NEED <= 256 ? 256 : 512;
+  static_assert(STAGES >= 2, "not enough shared memory for a 2-stage pipeline");
+};
+
+struct AttnParams {
+  const __nv_bfloat16 *q;
+  int64_t q_tok_stride;
+  const int32_t *tok_pos;
+  const int32_t *tok_lo;
+  const float2 *rope;
+  int64_t rope_rows;
+  const float2 *rot;
+  int32_t n_heads, n_kv_heads, head_dim, gs;
+  float scale_log2;
+  const DbsaAttnWork *works;
+  const DbsaAttnSeg *segs;
+  __nv_bfloat16 *out;
+  int64_t out_tok_stride;
+  float *part_o;
+  float *part_lse;
+};
+
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Rotate this thread's query row (token t, head) at rope position `pos`,
+// composed with the optional per-segment shift, and write it zero-padded to
+// HDP into the swizzled K-major Q tile.  (model.rope_rotate_heads,
+// model.py:222-239: pair (x_i, x_{i+hd/2}).)
+template <int HDP>
+__device__ __forceinline__ void load_q_row(const AttnParams &p, uint8_t *q_tile, int row, bool valid,
+                                           int t, int head, int rot) {
+  constexpr int QSW = AttnCfg<HDP, 1>::QSW;
+  const int hd = p.head_dim, half = hd >> 1;
+  uint16_t *dst16 = nullptr;
+  (void)dst16;
+  if (!valid) {
+#pragma unroll
+    for (int c = 0; c < HDP / 8; ++c) {
+      const int atom = c / (QSW / 16), cc = c % (QSW / 16);
+      uint4 *d = reinterpret_cast<uint4 *>(q_tile + atom * 128 * QSW + swz_offset(row, cc, QSW));
+      *d = make_uint4(0, 0, 0, 0);
+    }
+    return;
+  }
+  const __nv_bfloat16 *src = p.q + (int64_t)t * p.q_tok_stride + (int64_t)head * hd;
+  const float2 *rp = p.rope + (int64_t)p.tok_pos[t] * half;
+  const float2 *rr = rot >= 0 ? p.rot + (int64_t)rot * half : nullptr;
+  // Build the rotated row chunk by chunk (8 output elements per 16-byte chunk).
+#pragma unroll 1
+  for (int c = 0; c < HDP / 8; ++c) {
+    float o[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int e = c * 8 + j;
+      float val = 0.f;
+      if (e < hd) {
+        const int i = e < half ? e : e - half;
+        const float lo = __bfloat162float(src[i]);
+        const float hi = __bfloat162float(src[i + half]);
+        float2 cs = rp[i];
+        if (rr) {
+          const float2 d = rr[i];
+          cs = make_float2(cs.x * d.x - cs.y * d.y, cs.y * d.x + cs.x * d.y);
+        }
+        val = e < half ? (lo * cs.x - hi * cs.y) : (lo * cs.y + hi * cs.x);
+      }
+      o[j] = val;
+    }
+    const int atom = c / (QSW / 16), cc = c % (QSW / 16);
+    uint4 *d = reinterpret_cast<uint4 *>(q_tile + atom * 128 * QSW + swz_offset(row, cc, QSW));
+    *d = make_uint4(pack_bf16(o[0], o[1]), pack_bf16(o[2], o[3]), pack_bf16(o[4], o[5]),
+                    pack_bf16(o[6], o[7]));
+  }
+}
+
+template <int HDP, int NUM_M>
+__global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
+    dbsa_attn_kernel(const __grid_constant__ CUtensorMap tm_k0, const __grid_constant__ CUtensorMap tm_v0,
+                     const __grid_constant__ CUtensorMap tm_k1, const __grid_constant__ CUtensorMap tm_v1,
+                     const AttnParams p) {
+  using C = AttnCfg<HDP, NUM_M>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *sQ = smem;                             // NUM_M x Q_BYTES
+  uint8_t *sP = sQ + NUM_M * C::Q_BYTES;          // NUM_M x P_BYTES
+  uint8_t *sK = sP + NUM_M * C::P_BYTES;          // STAGES x K_BYTES
+  uint8_t *sV = sK + C::STAGES * C::K_BYTES;      // STAGES x V_BYTES
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sV + C::STAGES * C::V_BYTES);
+  uint64_t *kv_full = bars;                       // [STAGES]
+  uint64_t *kv_empty = kv_full + C::STAGES;       // [STAGES]
+  uint64_t *q_full = kv_empty + C::STAGES;        // [NUM_M]
+  uint64_t *s_full = q_full + NUM_M;              // [NUM_M]
+  uint64_t *p_full = s_full + NUM_M;              // [NUM_M]
+  uint64_t *o_full = p_full + NUM_M;              // [NUM_M]
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(o_full + NUM_M);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const DbsaAttnWork w = p.works[blockIdx.x];
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+    }
+    for (int m = 0; m < NUM_M; ++m) {
+      mbar_init(&q_full[m], 128);
+      mbar_init(&s_full[m], 1);
+      mbar_init(&p_full[m], 128);
+      mbar_init(&o_full[m], 1);
+    }
+    fence_mbar_init();
+    tma_prefetch(&tm_k0);
+    tma_prefetch(&tm_v0);
+    tma_prefetch(&tm_k1);
+    tma_prefetch(&tm_v1);
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int j = 0;
+      for (int si = w.seg_begin; si < w.seg_end; ++si) {
+        const DbsaAttnSeg sg = p.segs[si];
+        const CUtensorMap *tk = sg.src ? &tm_k1 : &tm_k0;
+        const CUtensorMap *tv = sg.src ? &tm_v1 : &tm_v0;
+        const int nt = (sg.n_tok + kBN - 1) / kBN;
+        for (int tt = 0; tt < nt; ++tt, ++j) {
+          const int st = j % C::STAGES;
+          if (j >= C::STAGES) mbar_wait(&kv_empty[st], ((j / C::STAGES) & 1) ^ 1);
+          mbar_arrive_expect_tx(&kv_full[st], C::STAGE_BYTES);
+          const int row = sg.row0 + tt * kBN;
+#pragma unroll
+          for (int a = 0; a < C::NATOM; ++a)
+            tma_load_4d(sK + st * C::K_BYTES + a * kBN * C::QSW, tk, &kv_full[st], a * C::KATOM, row,
+                        w.kv_head, sg.layer);
+          tma_load_4d(sV + st * C::V_BYTES, tv, &kv_full[st], row, 0, w.kv_head, sg.layer);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = umma_idesc_bf16(128, kBN);
+      constexpr uint32_t idesc_o = umma_idesc_bf16(128, HDP);
+      const uint32_t sQa = smem_u32(sQ), sPa = smem_u32(sP), sKa = smem_u32(sK), sVa = smem_u32(sV);
+      int n_tiles = 0;
+      for (int si = w.seg_begin; si < w.seg_end; ++si) n_tiles += (p.segs[si].n_tok + kBN - 1) / kBN;
+
+      auto issue_qk = [&](int m, int j) {
+        const int st = j % C::STAGES;
+        const uint32_t d = tbase + NUM_M * HDP + m * kBN;
+#pragma unroll
+        for (int kk = 0; kk < HDP / 16; ++kk) {
+          const int a = (kk * 16) / C::KATOM;
+          const int off = ((kk * 16) % C::KATOM) * 2;
+          const uint64_t ad = umma_desc_kmajor(sQa + m * C::Q_BYTES + a * 128 * C::QSW + off, C::QSW);
+          const uint64_t bd = umma_desc_kmajor(sKa + st * C::K_BYTES + a * kBN * C::QSW + off, C::QSW);
+          umma_bf16_ss(d, ad, bd, idesc_s, kk > 0 ? 1u : 0u);
+        }
+        umma_commit(&s_full[m]);
+      };
+      auto issue_pv = [&](int m, int j) {
+        const int st = j % C::STAGES;
+        const uint32_t d = tbase + m * HDP;
+#pragma unroll
+        for (int kk = 0; kk < kBN / 16; ++kk) {
+          const uint64_t ad = umma_desc_kmajor(sPa + m * C::P_BYTES + kk * 32, 128);
+          const uint64_t bd = umma_desc_kmajor(sVa + st * C::V_BYTES + kk * 32, 128);
+          umma_bf16_ss(d, ad, bd, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+        }
+      };
+
+      if (n_tiles > 0) {
+        mbar_wait(&kv_full[0], 0);
+        tc_fence_after();
+        for (int m = 0; m < NUM_M; ++m) {
+          mbar_wait(&q_full[m], 0);
+          tc_fence_after();
+          issue_qk(m, 0);
+        }
+        for (int j = 0; j < n_tiles; ++j) {
+          for (int m = 0; m < NUM_M; ++m) {
+            mbar_wait(&p_full[m], j & 1);
+            tc_fence_after();
+            issue_pv(m, j);
+            if (m == NUM_M - 1) umma_commit(&kv_empty[j % C::STAGES]);
+            if (j + 1 < n_tiles) {
+              if (m == 0) {
+                mbar_wait(&kv_full[(j + 1) % C::STAGES], ((j + 1) / C::STAGES) & 1);
+                tc_fence_after();
+              }
+              issue_qk(m, j + 1);
+            }
+          }
+        }
+      }
+      for (int m = 0; m < NUM_M; ++m) umma_commit(&o_full[m]);
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ softmax warpgroups
+    const int m = (warp - 4) >> 2;
+    const int q4 = warp & 3;
+    const int trow = q4 * 32 + lane;  // row inside the M tile == TMEM lane
+    const int r = m * 128 + trow;     // row inside the work
+    const int rows = w.n_tok * p.gs;
+    const bool valid = r < rows;
+    const int t = w.q_tok0 + (valid ? r / p.gs : 0);
+    const int head = w.kv_head * p.gs + (valid ? r % p.gs : 0);
+    const int rl = t - w.self_tok0;
+    const int lo = (p.tok_lo && valid) ? p.tok_lo[t] : 0;
+    uint8_t *q_tile = sQ + m * C::Q_BYTES;
+    uint8_t *p_tile = sP + m * C::P_BYTES;
+    const uint32_t lane_base = tbase + ((uint32_t)(q4 * 32) << 16);
+    const uint32_t t_s = lane_base + NUM_M * HDP + m * kBN;
+    const uint32_t t_o = lane_base + m * HDP;
+
+    int cur_rot = w.seg_end > w.seg_begin ? p.segs[w.seg_begin].rot : -1;
+    load_q_row<HDP>(p, q_tile, trow, valid, t, head, cur_rot);
+    fence_proxy_async_smem();
+    mbar_arrive(&q_full[m]);
+
+    float m_used = -INFINITY, l_sum = 0.f;
+    int j = 0;
+    for (int si = w.seg_begin; si < w.seg_end; ++si) {
+      const DbsaAttnSeg sg = p.segs[si];
+      const int nt = (sg.n_tok + kBN - 1) / kBN;
+      const bool is_self = sg.kind == DBSA_SEG_SELF;
+      for (int tt = 0; tt < nt; ++tt, ++j) {
+        mbar_wait(&s_full[m], j & 1);
+        tc_fence_after();
+        float x[kBN];
+        {
+          float a[32], b[32];
+          tmem_ld32(t_s, a);
+          tmem_ld32(t_s + 32, b);
+          tmem_wait_ld();
+#pragma unroll
+          for (int c = 0; c < 32; ++c) {
+            x[c] = a[c];
+            x[c + 32] = b[c];
+          }
+        }
+        const int k0 = tt * kBN;
+        float tmax = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < kBN; ++c) {
+          const int kl = k0 + c;
+          bool ok = valid && kl < sg.n_tok;
+          if (is_self) ok = ok && kl <= rl && (kl < w.prefix || kl >= lo);
+          x[c] = ok ? x[c] * p.scale_log2 : -INFINITY;
+          tmax = fmaxf(tmax, x[c]);
+        }
+        const float m_new = fmaxf(m_used, tmax);
+        // Lazy rescale (threshold 2^8): O and l keep a stale max until it
+        // grows by more than 8 in log2 units.  tcgen05.ld/st are warp-wide, so
+        // the decision is warp-uniform.
+        const bool need = (j > 0) && (m_used != -INFINITY) && (m_new > m_used + 8.f);
+        float alpha = 1.f;
+        if (__any_sync(0xffffffffu, need)) {
+          if (m_used != -INFINITY) alpha = fast_exp2(m_used - m_new);
+          m_used = m_new;
+#pragma unroll 1
+          for (int c0 = 0; c0 < HDP; c0 += 16) {
+            float o[16];
+            tmem_ld16(t_o + c0, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) o[i] *= alpha;
+            tmem_st16(t_o + c0, o);
+          }
+          tmem_wait_st();
+        } else if (m_used == -INFINITY) {
+          m_used = m_new;  // first finite max: O row holds only zeros (or nothing yet)
+        }
+        l_sum *= alpha;
+        const float msub = m_used == -INFINITY ? 0.f : m_used;
+        float psum = 0.f;
+#pragma unroll
+        for (int c = 0; c < kBN; c += 8) {
+          float e[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            e[i] = fast_exp2(x[c + i] - msub);
+            psum += e[i];
+          }
+          uint4 *d = reinterpret_cast<uint4 *>(p_tile + swz_offset(trow, c / 8, 128));
+          *d = make_uint4(pack_bf16(e[0], e[1]), pack_bf16(e[2], e[3]), pack_bf16(e[4], e[5]),
+                          pack_bf16(e[6], e[7]));
+        }
+        l_sum += psum;
+        // Segment boundary: re-stage Q with the next segment's RoPE shift.  QK of
+        // this tile is complete (s_full), so the Q tile is free.
+        if (tt == nt - 1 && si + 1 < w.seg_end) {
+          const int nrot = p.segs[si + 1].rot;
+          if (nrot != cur_rot) {
+            cur_rot = nrot;
+            load_q_row<HDP>(p, q_tile, trow, valid, t, head, cur_rot);
+          }
+        }
+        fence_proxy_async_smem();
+        tc_fence_before();
+        mbar_arrive(&p_full[m]);
+      }
+    }
+
+    // ------------------------------------------------------------ epilogue
+    mbar_wait(&o_full[m], 0);
+    tc_fence_after();
+    const float inv_l = l_sum > 0.f ? 1.f / l_sum : 0.f;
+    const int hd = p.head_dim;
+#pragma unroll 1
+    for (int c0 = 0; c0 < HDP; c0 += 16) {
+      float o[16];
+      tmem_ld16(t_o + c0, o);
+      tmem_wait_ld();
+      if (valid && c0 < hd) {
+        if (w.out_mode == 0) {
+          __nv_bfloat16 *dst = p.out + (int64_t)t * p.out_tok_stride + (int64_t)head * hd + c0;
+          if (hd % 16 == 0) {
+            uint4 *d4 = reinterpret_cast<uint4 *>(dst);
+            d4[0] = make_uint4(pack_bf16(o[0] * inv_l, o[1] * inv_l), pack_bf16(o[2] * inv_l, o[3] * inv_l),
+                               pack_bf16(o[4] * inv_l, o[5] * inv_l), pack_bf16(o[6] * inv_l, o[7] * inv_l));
+            d4[1] = make_uint4(pack_bf16(o[8] * inv_l, o[9] * inv_l), pack_bf16(o[10] * inv_l, o[11] * inv_l),
+                               pack_bf16(o[12] * inv_l, o[13] * inv_l), pack_bf16(o[14] * inv_l, o[15] * inv_l));
+          } else {
+            for (int i = 0; i < 16 && c0 + i < hd; ++i) dst[i] = __float2bfloat16(o[i] * inv_l);
+          }
+        } else {
+          float *dst = p.part_o + (w.part_row0 + r) * (int64_t)hd + c0;
+          for (int i = 0; i < 16 && c0 + i < hd; ++i) dst[i] = o[i] * inv_l;
+        }
+      }
+    }
+    if (valid && w.out_mode == 1) {
+      // natural-log LSE of the scaled scores: (m + log2 l) * ln 2
+      p.part_lse[w.part_row0 + r] = l_sum > 0.f ? (m_used + log2f(l_sum)) * 0.69314718055994531f : -INFINITY;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc(tbase, C::TMEM_COLS);
+}
+
+// ---------------------------------------------------------------- host side
+
+static bool encode_plane_maps(const DbsaAttnArgs &a, const void *k, const void *v, int64_t rows, int layers,
+                              CUtensorMap *tk, CUtensorMap *tv) {
+  const int HDP = a.hd_pad;
+  const int qsw = HDP >= 64 ? 128 : HDP * 2;
+  const int katom = HDP >= 64 ? 64 : HDP;
+  CUtensorMapSwizzle ksw = qsw == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                           : qsw == 64  ? CU_TENSOR_MAP_SWIZZLE_64B
+                                        : CU_TENSOR_MAP_SWIZZLE_32B;
+  {
+    cuuint64_t dims[4] = {(cuuint64_t)HDP, (cuuint64_t)rows, (cuuint64_t)a.n_kv_heads, (cuuint64_t)layers};
+    cuuint64_t strides[3] = {(cuuint64_t)HDP * 2, (cuuint64_t)rows * HDP * 2,
+                             (cuuint64_t)a.n_kv_heads * rows * HDP * 2};
+    cuuint32_t box[4] = {(cuuint32_t)katom, (cuuint32_t)kBN, 1, 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    if (!encode_tiled_bf16(tk, k, 4, dims, strides, box, estr, ksw)) return false;
+  }
+  {
+    cuuint64_t dims[4] = {(cuuint64_t)rows, (cuuint64_t)HDP, (cuuint64_t)a.n_kv_heads, (cuuint64_t)layers};
+    cuuint64_t strides[3] = {(cuuint64_t)rows * 2, (cuuint64_t)HDP * rows * 2,
+                             (cuuint64_t)a.n_kv_heads * HDP * rows * 2};
+    cuuint32_t box[4] = {(cuuint32_t)kBN, (cuuint32_t)HDP, 1, 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    if (!encode_tiled_bf16(tv, v, 4, dims, strides, box, estr, CU_TENSOR_MAP_SWIZZLE_128B)) return false;
+  }
+  return true;
+}
+
+template <int HDP, int NUM_M>
+static int launch_attn(const DbsaAttnArgs &a, const AttnParams &p, const CUtensorMap *maps, cudaStream_t s) {
+  using C = AttnCfg<HDP, NUM_M>;
+  auto kern = dbsa_attn_kernel<HDP, NUM_M>;
+  static thread_local bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return set_error(DBSA_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+    attr_set = true;
+  }
+  kern<<<a.n_works, C::THREADS, C::SMEM, s>>>(maps[0], maps[1], maps[2], maps[3], p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(DBSA_ERR_CUDA, "attention launch: %s", cudaGetErrorString(e));
+  return DBSA_OK;
+}
+
+}  // namespace dbsa
+
+extern "C" int dbsa_attention(const DbsaAttnArgs *args, void *stream) {
+  using namespace dbsa;
+  if (!args) return set_error(DBSA_ERR_VALIDATION, "dbsa_attention: null args");
+  const DbsaAttnArgs &a = *args;
+  if (a.n_works < 0) return set_error(DBSA_ERR_VALIDATION, "n_works < 0");
+  if (a.n_works == 0) return DBSA_OK;
+  if (a.head_dim <= 0 || a.head_dim % 2 || a.head_dim > a.hd_pad)
+    return set_error(DBSA_ERR_CONFIG, "head_dim %d invalid for hd_pad %d", a.head_dim, a.hd_pad);
+  if (!(a.hd_pad == 16 || a.hd_pad == 32 || a.hd_pad == 64 || a.hd_pad == 128))
+    return set_error(DBSA_ERR_CONFIG, "hd_pad must be 16/32/64/128, got %d", a.hd_pad);
+  if (a.n_kv_heads <= 0 || a.n_heads % a.n_kv_heads)
+    return set_error(DBSA_ERR_CONFIG, "n_heads %d not a multiple of n_kv_heads %d", a.n_heads, a.n_kv_heads);
+  if (a.num_m != 1 && a.num_m != 2) return set_error(DBSA_ERR_CONFIG, "num_m must be 1 or 2");
+  if (a.pool_rows % 64 || a.aux_rows % 64) return set_error(DBSA_ERR_SHAPE, "plane rows must be multiples of 64");
+  if (!a.q || !a.tok_pos || !a.rope_table || !a.k_pool || !a.v_pool || !a.works || !a.segs)
+    return set_error(DBSA_ERR_VALIDATION, "dbsa_attention: null pointer argument");
+
+  CUtensorMap maps[4];
+  if (!encode_plane_maps(a, a.k_pool, a.v_pool, a.pool_rows, a.pool_layers, &maps[0], &maps[1]))
+    return DBSA_ERR_CUDA;
+  const void *ka = a.k_aux ? a.k_aux : a.k_pool;
+  const void *va = a.v_aux ? a.v_aux : a.v_pool;
+  const int64_t ar = a.k_aux ? a.aux_rows : a.pool_rows;
+  const int al = a.k_aux ? a.aux_layers : a.pool_layers;
+  if (!encode_plane_maps(a, ka, va, ar, al, &maps[2], &maps[3])) return DBSA_ERR_CUDA;
+
+  AttnParams p;
+  p.q = reinterpret_cast<const __nv_bfloat16 *>(a.q);
+  p.q_tok_stride = a.q_tok_stride;
+  p.tok_pos = a.tok_pos;
+  p.tok_lo = a.tok_lo;
+  p.rope = reinterpret_cast<const float2 *>(a.rope_table);
+  p.rope_rows = a.rope_rows;
+  p.rot = reinterpret_cast<const float2 *>(a.rot_table);
+  p.n_heads = a.n_heads;
+  p.n_kv_heads = a.n_kv_heads;
+  p.head_dim = a.head_dim;
+  p.gs = a.n_heads / a.n_kv_heads;
+  p.scale_log2 = a.scale * 1.4426950408889634f;
+  p.works = a.works;
+  p.segs = a.segs;
+  p.out = reinterpret_cast<__nv_bfloat16 *>(a.out);
+  p.out_tok_stride = a.out_tok_stride;
+  p.part_o = a.part_o;
+  p.part_lse = a.part_lse;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  switch (a.hd_pad * 10 + a.num_m) {
+    case 161: return launch_attn<16, 1>(a, p, maps, s);
+    case 162: return launch_attn<16, 2>(a, p, maps, s);
+    case 321: return launch_attn<32, 1>(a, p, maps, s);
+    case 322: return launch_attn<32, 2>(a, p, maps, s);
+    case 641: return launch_attn<64, 1>(a, p, maps, s);
+    case 642: return launch_attn<64, 2>(a, p, maps, s);
+    case 1281: return launch_attn<128, 1>(a, p, maps, s);
+    case 1282: return launch_attn<128, 2>(a, p, maps, s);
+  }
+  return set_error(DBSA_ERR_CONFIG, "unsupported attention variant");
+}

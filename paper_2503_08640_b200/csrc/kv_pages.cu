@@ -1,0 +1,115 @@
+// kv_pages.cu -- K2w page write (rotated K rows + transposed V) and the
+// float64-derived rotary table.
+//
+// Reference: SegmentedKVCache.append_block stores per-block pre-rotation K/V
+// (kvstore.py:70-106); stage 1 re-rotates context blocks at their ORIGINAL
+// positions before every use (pipeline.py:191-200).  The pool stores K already
+// rotated at the original positions (so stage 1 reads it as-is) and stage 2
+// moves the re-positioning to the query side (attn_sm100.cu).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "../../include/dbsa_b200.h"
+#include "dbsa_internal.h"
+#include "sm100_ptx.cuh"
+
+namespace dbsa {
+
+// grid (n_pages, n_kv_heads), 128 threads.  K: [L][Hkv][rows][HDP]; V^T: [L][Hkv][HDP][rows].
+__global__ void kv_write_kernel(DbsaKvWriteArgs a) {
+  const DbsaPage pg = a.pages[blockIdx.x];
+  const int head = blockIdx.y;
+  const int hd = a.head_dim, half = hd >> 1, HDP = a.hd_pad;
+  const __nv_bfloat16 *ks = reinterpret_cast<const __nv_bfloat16 *>(a.k_src);
+  const __nv_bfloat16 *vs = reinterpret_cast<const __nv_bfloat16 *>(a.v_src);
+  const float2 *rope = reinterpret_cast<const float2 *>(a.rope_table);
+  const int64_t plane = (int64_t)a.layer * a.n_kv_heads + head;
+  __nv_bfloat16 *kd = reinterpret_cast<__nv_bfloat16 *>(a.k_dst) + plane * a.dst_rows * HDP;
+  __nv_bfloat16 *vd = reinterpret_cast<__nv_bfloat16 *>(a.v_dst) + plane * a.dst_rows * HDP;
+
+  // K rows: item = (row i, 8-element chunk c), rotated at tok_pos (model.py:222-239).
+  const int kchunks = HDP / 8;
+  for (int it = threadIdx.x; it < DBSA_PAGE_TOKENS * kchunks; it += blockDim.x) {
+    const int i = it / kchunks, c = it % kchunks;
+    float o[8];
+    if (i < pg.n_tok) {
+      const int t = pg.tok0 + i;
+      const __nv_bfloat16 *src = ks + (int64_t)t * a.src_tok_stride + (int64_t)head * hd;
+      const float2 *rp = rope + (int64_t)a.tok_pos[t] * half;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int e = c * 8 + j;
+        float val = 0.f;
+        if (e < hd) {
+          const int pi = e < half ? e : e - half;
+          const float lo = __bfloat162float(src[pi]), hi = __bfloat162float(src[pi + half]);
+          const float2 cs = rp[pi];
+          val = e < half ? lo * cs.x - hi * cs.y : lo * cs.y + hi * cs.x;
+        }
+        o[j] = val;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[j] = 0.f;
+    }
+    *reinterpret_cast<uint4 *>(kd + (int64_t)(pg.row0 + i) * HDP + c * 8) =
+        make_uint4(pack_bf16(o[0], o[1]), pack_bf16(o[2], o[3]), pack_bf16(o[4], o[5]), pack_bf16(o[6], o[7]));
+  }
+  // V^T columns: item = (dim d, 8-token chunk ic), 16-byte coalesced stores along the token axis.
+  for (int it = threadIdx.x; it < HDP * (DBSA_PAGE_TOKENS / 8); it += blockDim.x) {
+    const int d = it / (DBSA_PAGE_TOKENS / 8), ic = it % (DBSA_PAGE_TOKENS / 8);
+    float o[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int i = ic * 8 + j;
+      o[j] = (i < pg.n_tok && d < hd)
+                 ? __bfloat162float(vs[(int64_t)(pg.tok0 + i) * a.src_tok_stride + (int64_t)head * hd + d])
+                 : 0.f;
+    }
+    *reinterpret_cast<uint4 *>(vd + (int64_t)d * a.dst_rows + pg.row0 + ic * 8) =
+        make_uint4(pack_bf16(o[0], o[1]), pack_bf16(o[2], o[3]), pack_bf16(o[4], o[5]), pack_bf16(o[6], o[7]));
+  }
+}
+
+// table[p][i] = (cos, sin)((pos0 + p) * inv_freq[i]), angle formed in float64
+// (model.rope_angles, model.py:205-209), rounded once to float32.
+__global__ void rope_table_kernel(float2 *table, int64_t rows, const double *inv_freq, int half, int64_t pos0) {
+  const int64_t n = rows * half;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = idx / half;
+    const int i = (int)(idx % half);
+    const double ang = (double)(pos0 + p) * inv_freq[i];
+    double s, c;
+    sincos(ang, &s, &c);
+    table[idx] = make_float2((float)c, (float)s);
+  }
+}
+
+}  // namespace dbsa
+
+extern "C" int dbsa_kv_write(const DbsaKvWriteArgs *args, void *stream) {
+  using namespace dbsa;
+  if (!args) return set_error(DBSA_ERR_VALIDATION, "dbsa_kv_write: null args");
+  const DbsaKvWriteArgs &a = *args;
+  if (a.n_pages < 0) return set_error(DBSA_ERR_VALIDATION, "n_pages < 0");
+  if (a.n_pages == 0) return DBSA_OK;
+  if (!(a.hd_pad == 16 || a.hd_pad == 32 || a.hd_pad == 64 || a.hd_pad == 128) || a.head_dim > a.hd_pad ||
+      a.head_dim % 2)
+    return set_error(DBSA_ERR_CONFIG, "bad head_dim %d / hd_pad %d", a.head_dim, a.hd_pad);
+  if (a.dst_rows % DBSA_PAGE_TOKENS) return set_error(DBSA_ERR_SHAPE, "dst_rows must be a multiple of 64");
+  if (a.layer < 0 || a.layer >= a.dst_layers) return set_error(DBSA_ERR_VALIDATION, "layer out of range");
+  dim3 grid(a.n_pages, a.n_kv_heads);
+  kv_write_kernel<<<grid, 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(a);
+  return check_launch("kv_write");
+}
+
+extern "C" int dbsa_rope_table(float *table, int64_t rows, const double *inv_freq, int32_t half, int64_t pos0,
+                               void *stream) {
+  using namespace dbsa;
+  if (rows <= 0 || half <= 0) return set_error(DBSA_ERR_VALIDATION, "rope table: empty");
+  const int64_t n = rows * half;
+  const int blocks = (int)((n + 255) / 256 < 148 * 16 ? (n + 255) / 256 : 148 * 16);
+  rope_table_kernel<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(reinterpret_cast<float2 *>(table),
+                                                                                  rows, inv_freq, half, pos0);
+  return check_launch("rope_table");
+}

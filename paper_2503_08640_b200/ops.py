@@ -1,0 +1,155 @@
+"""Device-op wrappers over the C ABI (torch tensors in, launches on the current
+stream out).  Torch is used only for device memory and streams here; every
+computation is one of the hand-written sm_100a kernels in csrc/.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import numpy as np
+
+from . import _native as nat
+from .errors import ConfigError, ShapeError
+
+PAGE = nat.PAGE_TOKENS
+
+WORK_DTYPE = np.dtype(
+    [("q_tok0", "<i4"), ("n_tok", "<i4"), ("self_tok0", "<i4"), ("kv_head", "<i4"),
+     ("seg_begin", "<i4"), ("seg_end", "<i4"), ("prefix", "<i4"), ("out_mode", "<i4"),
+     ("part_row0", "<i8")], align=True)
+SEG_DTYPE = np.dtype(
+    [("src", "<i4"), ("layer", "<i4"), ("row0", "<i4"), ("n_tok", "<i4"),
+     ("kind", "<i4"), ("rot", "<i4"), ("pad0", "<i4"), ("pad1", "<i4")], align=True)
+PAGE_DTYPE = np.dtype([("tok0", "<i4"), ("n_tok", "<i4"), ("row0", "<i4"), ("pad", "<i4")], align=True)
+MERGE_DTYPE = np.dtype(
+    [("part_row0", "<i8"), ("rows", "<i4"), ("n_splits", "<i4"), ("q_tok0", "<i4"), ("kv_head", "<i4")],
+    align=True)
+
+assert WORK_DTYPE.itemsize == ctypes.sizeof(nat.AttnWork)
+assert SEG_DTYPE.itemsize == ctypes.sizeof(nat.AttnSeg)
+assert PAGE_DTYPE.itemsize == ctypes.sizeof(nat.Page)
+assert MERGE_DTYPE.itemsize == ctypes.sizeof(nat.MergeGroup)
+
+ORDERING_CODES = {"in-order": 0, "low-to-high": 1, "reverse": 2}
+
+
+def hd_pad(head_dim: int) -> int:
+    """Head dim padded to a tcgen05-friendly width (zero columns)."""
+    for p in (16, 32, 64, 128):
+        if head_dim <= p:
+            return p
+    raise ConfigError(f"head_dim {head_dim} > 128 is not supported by the sm_100a kernels")
+
+
+def inv_freq(head_dim: int, theta: float) -> np.ndarray:
+    """theta ** (-arange(0, hd, 2) / hd) in float64 (model.rope_angles, model.py:207)."""
+    return theta ** (-np.arange(0, head_dim, 2, dtype=np.float64) / head_dim)
+
+
+def to_device(arr: np.ndarray, device):
+    import torch
+
+    t = torch.from_numpy(np.ascontiguousarray(arr).view(np.uint8))
+    if t.numel() == 0:
+        return torch.empty(0, dtype=torch.uint8, device=device)
+    return t.pin_memory().to(device, non_blocking=True)
+
+
+def rope_table(rows: int, head_dim: int, theta: float, device, pos0: int = 0):
+    """float32 [rows, hd/2, 2] table of (cos, sin)(pos * inv_freq) built on device in float64."""
+    import torch
+
+    half = head_dim // 2
+    freq = torch.from_numpy(inv_freq(head_dim, theta)).to(device)
+    table = torch.empty((rows, half, 2), dtype=torch.float32, device=device)
+    nat.check(nat.load_library().dbsa_rope_table(table.data_ptr(), rows, freq.data_ptr(), half, pos0,
+                                                 nat.stream_handle()))
+    table._keepalive = freq  # freq must outlive the async launch
+    return table
+
+
+def shift_table(deltas, head_dim: int, theta: float) -> np.ndarray:
+    """Host float64 (cos, sin) of (-delta) * inv_freq for each delta -> float32 [n, hd/2, 2]."""
+    f = inv_freq(head_dim, theta)
+    ang = -np.asarray(deltas, dtype=np.float64)[:, None] * f[None, :]
+    return np.stack([np.cos(ang), np.sin(ang)], axis=-1).astype(np.float32)
+
+
+def kv_write(k_src, v_src, src_tok_stride, tok_pos, rope, pages_dev, n_pages, k_dst, v_dst, dst_rows,
+             dst_layers, layer, n_kv_heads, head_dim):
+    a = nat.KvWriteArgs(
+        k_src=k_src.data_ptr(), v_src=v_src.data_ptr(), src_tok_stride=src_tok_stride,
+        tok_pos=tok_pos.data_ptr(), rope_table=rope.data_ptr(), rope_rows=rope.shape[0],
+        pages=pages_dev.data_ptr(), n_pages=n_pages, k_dst=k_dst.data_ptr(), v_dst=v_dst.data_ptr(),
+        dst_rows=dst_rows, dst_layers=dst_layers, layer=layer, n_kv_heads=n_kv_heads,
+        head_dim=head_dim, hd_pad=hd_pad(head_dim))
+    nat.check(nat.load_library().dbsa_kv_write(ctypes.byref(a), nat.stream_handle()))
+
+
+def attention(*, q, q_tok_stride, tok_pos, tok_lo, rope, rot, pool, aux, n_heads, n_kv_heads, head_dim,
+              works_dev, n_works, segs_dev, num_m, out, out_tok_stride, part_o=None, part_lse=None):
+    """Launch K1/K3.  `pool` / `aux` are (k_planes, v_planes, rows, layers)."""
+    kp, vp, prow, pl = pool
+    ka, va, arow, al = aux if aux is not None else (None, None, 0, 0)
+    a = nat.AttnArgs(
+        q=q.data_ptr(), q_tok_stride=q_tok_stride, tok_pos=tok_pos.data_ptr(),
+        tok_lo=nat.ptr(tok_lo), rope_table=rope.data_ptr(), rope_rows=rope.shape[0],
+        rot_table=nat.ptr(rot), k_pool=kp.data_ptr(), v_pool=vp.data_ptr(), pool_rows=prow,
+        pool_layers=pl, k_aux=nat.ptr(ka), v_aux=nat.ptr(va), aux_rows=arow, aux_layers=al,
+        n_heads=n_heads, n_kv_heads=n_kv_heads, head_dim=head_dim, hd_pad=hd_pad(head_dim),
+        scale=float(1.0 / math.sqrt(head_dim)), num_m=num_m, works=works_dev.data_ptr(),
+        n_works=n_works, segs=segs_dev.data_ptr(), out=out.data_ptr(), out_tok_stride=out_tok_stride,
+        part_o=nat.ptr(part_o), part_lse=nat.ptr(part_lse))
+    nat.check(nat.load_library().dbsa_attention(ctypes.byref(a), nat.stream_handle()))
+
+
+def lse_merge(part_o, part_lse, groups_dev, n_groups, max_rows, n_heads, n_kv_heads, head_dim, out,
+              out_tok_stride):
+    a = nat.MergeArgs(part_o=part_o.data_ptr(), part_lse=part_lse.data_ptr(), groups=groups_dev.data_ptr(),
+                      n_groups=n_groups, max_rows=max_rows, n_heads=n_heads, n_kv_heads=n_kv_heads,
+                      head_dim=head_dim, out=out.data_ptr(), out_tok_stride=out_tok_stride)
+    nat.check(nat.load_library().dbsa_lse_merge(ctypes.byref(a), nat.stream_handle()))
+
+
+def topk_select(scores, budget: int, ordering: str):
+    """scores: float64 [n_queries, n_units] (device) -> int32 [n_queries, budget] unit ids."""
+    import torch
+
+    if scores.dtype != torch.float64 or scores.dim() != 2:
+        raise ShapeError("topk_select expects a 2-D float64 score matrix")
+    scores = scores.contiguous()
+    out = torch.empty((scores.shape[0], budget), dtype=torch.int32, device=scores.device)
+    nat.check(nat.load_library().dbsa_topk_select(
+        scores.data_ptr(), scores.shape[0], scores.shape[1], budget, ORDERING_CODES[ordering],
+        out.data_ptr(), nat.stream_handle()))
+    return out
+
+
+def rmsnorm(x, weight, eps: float, out=None):
+    import torch
+
+    out = out if out is not None else torch.empty(x.shape, dtype=torch.bfloat16, device=x.device)
+    nat.check(nat.load_library().dbsa_rmsnorm(x.data_ptr(), weight.data_ptr(), out.data_ptr(), x.shape[0],
+                                              x.shape[1], float(eps), nat.stream_handle()))
+    return out
+
+
+def silu_mul(gate_up, ffn: int, out=None):
+    import torch
+
+    out = out if out is not None else torch.empty((gate_up.shape[0], ffn), dtype=torch.bfloat16,
+                                                  device=gate_up.device)
+    nat.check(nat.load_library().dbsa_silu_mul(gate_up.data_ptr(), out.data_ptr(), gate_up.shape[0], ffn,
+                                               nat.stream_handle()))
+    return out
+
+
+def label_logprob(logits, targets):
+    import torch
+
+    out = torch.empty(logits.shape[0], dtype=torch.float32, device=logits.device)
+    nat.check(nat.load_library().dbsa_label_logprob(logits.data_ptr(), logits.shape[0], logits.shape[1],
+                                                     targets.data_ptr(), out.data_ptr(), nat.stream_handle()))
+    return out

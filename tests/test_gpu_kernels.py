@@ -1,0 +1,294 @@
+"""Kernel-level parity of the sm_100a kernels against float64 restatements of
+the reference math (kernels.masked_attention kernels.py:73-100, rope
+model.py:205-239, select/order retrieval.py:352-388).  Inputs are rounded to
+bf16 first so the comparison isolates the kernel's own arithmetic.
+
+Tolerances: attention outputs max-abs 2e-2 (bf16 P and output rounding, O(1)
+magnitudes); top-k ids bit-exact.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+from paper_2503_08640_b200 import ops  # noqa: E402
+
+
+def _rope64(x, pos, theta):
+    # x [T, H, hd] float64; paired halves (model.py:222-239)
+    hd = x.shape[-1]
+    f = ops.inv_freq(hd, theta)
+    ang = np.asarray(pos, dtype=np.float64)[:, None] * f[None, :]
+    c, s = np.cos(ang)[:, None, :], np.sin(ang)[:, None, :]
+    lo, hi = x[..., : hd // 2], x[..., hd // 2:]
+    return np.concatenate([lo * c - hi * s, lo * s + hi * c], axis=-1)
+
+
+def _attend64(q, k, v, mask, scale):
+    s = (q @ k.T) * scale
+    s = np.where(mask, s, -np.inf)
+    m = s.max(axis=1, keepdims=True)
+    e = np.where(mask, np.exp(s - m), 0.0)
+    return (e / e.sum(axis=1, keepdims=True)) @ v
+
+
+class Pool:
+    """Minimal page pool for kernel tests: groups of tokens written with K2w."""
+
+    def __init__(self, n_kv, hd, lengths, layers=1, seed=0, theta=10000.0, dev="cuda"):
+        g = torch.Generator().manual_seed(seed)
+        self.n_kv, self.hd, self.hdp, self.theta = n_kv, hd, ops.hd_pad(hd), theta
+        self.lengths = list(lengths)
+        self.pos_start = np.concatenate([[0], np.cumsum(self.lengths)[:-1]]).astype(np.int64)
+        self.page0 = []
+        p = 0
+        for n in self.lengths:
+            self.page0.append(p)
+            p += -(-n // ops.PAGE)
+        self.rows = p * ops.PAGE
+        T = sum(self.lengths)
+        self.k_pre = torch.randn(layers, T, n_kv, hd, generator=g).to(torch.bfloat16)
+        self.v = torch.randn(layers, T, n_kv, hd, generator=g).to(torch.bfloat16)
+        self.kp = torch.zeros(layers, n_kv, self.rows, self.hdp, dtype=torch.bfloat16, device=dev)
+        self.vp = torch.zeros(layers, n_kv, self.hdp, self.rows, dtype=torch.bfloat16, device=dev)
+        self.rope = ops.rope_table(T + 4096, hd, theta, dev)
+        pages = []
+        for b, n in enumerate(self.lengths):
+            for i in range(0, n, ops.PAGE):
+                pages.append((int(self.pos_start[b]) + i, min(ops.PAGE, n - i), (self.page0[b] * ops.PAGE) + i, 0))
+        pages = np.array(pages, dtype=np.int32).view(ops.PAGE_DTYPE).reshape(-1)
+        pd = ops.to_device(pages, dev)
+        pos = torch.arange(T, dtype=torch.int32, device=dev)
+        for layer in range(layers):
+            ks = self.k_pre[layer].to(dev).reshape(T, n_kv * hd)
+            vs = self.v[layer].to(dev).reshape(T, n_kv * hd)
+            ops.kv_write(ks, vs, n_kv * hd, pos, self.rope, pd, len(pages), self.kp, self.vp, self.rows,
+                         layers, layer, n_kv, hd)
+        torch.cuda.synchronize()
+
+    def row0(self, b, start=0):
+        return self.page0[b] * ops.PAGE + start
+
+    def k_rot64(self, layer, b):
+        s, n = int(self.pos_start[b]), self.lengths[b]
+        k = self.k_pre[layer, s:s + n].double().numpy()
+        return _rope64(k, np.arange(s, s + n), self.theta)
+
+    def v64(self, layer, b):
+        s, n = int(self.pos_start[b]), self.lengths[b]
+        return self.v[layer, s:s + n].double().numpy()
+
+
+@pytest.mark.parametrize("hd,H,Hkv", [(128, 8, 2), (64, 4, 4), (16, 4, 2), (32, 2, 1), (8, 4, 2)])
+def test_kv_write_pages(hd, H, Hkv):
+    pool = Pool(Hkv, hd, [70, 64, 5, 130], layers=2, seed=1)
+    for layer in range(2):
+        for b in range(4):
+            n, r0 = pool.lengths[b], pool.row0(b)
+            got_k = pool.kp[layer, :, r0:r0 + n, :hd].float().cpu().numpy().transpose(1, 0, 2)
+            want_k = pool.k_rot64(layer, b)
+            assert np.abs(got_k - want_k).max() < 3e-2 * max(1.0, np.abs(want_k).max())
+            got_v = pool.vp[layer, :, :hd, r0:r0 + n].float().cpu().numpy().transpose(2, 0, 1)
+            np.testing.assert_array_equal(got_v, pool.v64(layer, b).astype(np.float32))
+            # page tail and head-dim padding are zero
+            tail = -(-n // ops.PAGE) * ops.PAGE
+            assert pool.kp[layer, :, r0 + n:r0 + tail].abs().sum().item() == 0
+            assert pool.kp[layer, :, r0:r0 + n, hd:].abs().sum().item() == 0
+
+
+def _stage1_case(hd, H, Hkv, lengths, j=2, layer=0, layers=1):
+    """Encode every group against sink + prev-j + self (masks.py:80-99) in one launch."""
+    dev = "cuda"
+    gs = H // Hkv
+    pool = Pool(Hkv, hd, lengths, layers=layers, seed=7)
+    T = sum(lengths)
+    g = torch.Generator().manual_seed(3)
+    q = torch.randn(T, H, hd, generator=g).to(torch.bfloat16)
+    num_m = 2 if gs * 16 > 128 else 1
+    slab_tok = (128 * num_m) // gs
+    works, segs = [], []
+    for b, n in enumerate(lengths):
+        ctx = sorted({0} | set(range(max(0, b - j), b)) - {b}) if b > 0 else []
+        for kv in range(Hkv):
+            for t0 in range(0, n, slab_tok):
+                nt = min(slab_tok, n - t0)
+                sb = len(segs)
+                for c in ctx:
+                    segs.append((0, layer, pool.row0(c), lengths[c], ops.nat.SEG_FULL, -1, 0, 0))
+                segs.append((0, layer, pool.row0(b), t0 + nt, ops.nat.SEG_SELF, -1, 0, 0))
+                works.append((int(pool.pos_start[b]) + t0, nt, int(pool.pos_start[b]), kv, sb, len(segs), 0, 0, 0))
+    W = np.array([w[:8] for w in works], dtype=np.int32)
+    wa = np.zeros(len(works), dtype=ops.WORK_DTYPE)
+    for i, name in enumerate(ops.WORK_DTYPE.names[:8]):
+        wa[name] = W[:, i]
+    sa = np.array(segs, dtype=np.int32).view(ops.SEG_DTYPE).reshape(-1)
+    out = torch.zeros(T, H, hd, dtype=torch.bfloat16, device=dev)
+    qd = q.to(dev)
+    pos = torch.arange(T, dtype=torch.int32, device=dev)
+    ops.attention(q=qd, q_tok_stride=H * hd, tok_pos=pos, tok_lo=None, rope=pool.rope, rot=None,
+                  pool=(pool.kp, pool.vp, pool.rows, layers), aux=None, n_heads=H, n_kv_heads=Hkv, head_dim=hd,
+                  works_dev=ops.to_device(wa, dev), n_works=len(wa), segs_dev=ops.to_device(sa, dev), num_m=num_m,
+                  out=out, out_tok_stride=H * hd)
+    torch.cuda.synchronize()
+    got = out.float().cpu().numpy()
+    q64 = _rope64(q.double().numpy(), np.arange(T), pool.theta)
+    scale = 1.0 / math.sqrt(hd)
+    worst = 0.0
+    for b, n in enumerate(lengths):
+        ctx = sorted({0} | set(range(max(0, b - j), b)) - {b}) if b > 0 else []
+        s = int(pool.pos_start[b])
+        for kv in range(Hkv):
+            ks = [pool.k_rot64(layer, c)[:, kv] for c in ctx] + [pool.k_rot64(layer, b)[:, kv]]
+            vs = [pool.v64(layer, c)[:, kv] for c in ctx] + [pool.v64(layer, b)[:, kv]]
+            K, V = np.concatenate(ks), np.concatenate(vs)
+            nctx = K.shape[0] - n
+            mask = np.zeros((n, K.shape[0]), dtype=bool)
+            mask[:, :nctx] = True
+            mask[:, nctx:] = np.tril(np.ones((n, n), dtype=bool))
+            for h in range(gs):
+                head = kv * gs + h
+                want = _attend64(q64[s:s + n, head], K, V, mask, scale)
+                worst = max(worst, float(np.abs(got[s:s + n, head] - want).max()))
+    return worst
+
+
+@pytest.mark.parametrize("hd,H,Hkv", [(128, 8, 2), (128, 4, 4), (64, 8, 2), (16, 4, 2), (32, 6, 3), (8, 4, 2)])
+def test_stage1_block_sparse_attention(hd, H, Hkv):
+    worst = _stage1_case(hd, H, Hkv, [150, 64, 97, 200, 33])
+    assert worst < 2e-2, worst
+
+
+def test_stage1_attention_second_layer():
+    assert _stage1_case(128, 8, 2, [65, 130, 64], layer=1, layers=2) < 2e-2
+
+
+def _stage2_case(hd, H, Hkv, lengths, sel, n_q, labels, splits, theta=10000.0):
+    """One query + label tree against selected (re-positioned) groups, with
+    split-KV partials merged by K3m."""
+    dev = "cuda"
+    gs = H // Hkv
+    pool = Pool(Hkv, hd, lengths, seed=11, theta=theta)
+    Tp = sum(lengths[b] for b in sel)
+    # new tokens: query (n_q) then each label (tree), positions Tp + index-in-branch
+    n_new = n_q + sum(labels)
+    pos = list(range(Tp, Tp + n_q))
+    lo = [0] * n_q
+    for L in labels:
+        start = len(pos)
+        pos += list(range(Tp + n_q, Tp + n_q + L))
+        lo += [start] * L
+    g = torch.Generator().manual_seed(5)
+    qn = torch.randn(n_new, H, hd, generator=g).to(torch.bfloat16)
+    kn = torch.randn(n_new, Hkv, hd, generator=g).to(torch.bfloat16)
+    vn = torch.randn(n_new, Hkv, hd, generator=g).to(torch.bfloat16)
+    aux_rows = -(-n_new // ops.PAGE) * ops.PAGE
+    ka = torch.zeros(1, Hkv, aux_rows, pool.hdp, dtype=torch.bfloat16, device=dev)
+    va = torch.zeros(1, Hkv, pool.hdp, aux_rows, dtype=torch.bfloat16, device=dev)
+    posd = torch.tensor(pos, dtype=torch.int32, device=dev)
+    pages = np.array([(i, min(ops.PAGE, n_new - i), i, 0) for i in range(0, n_new, ops.PAGE)],
+                     dtype=np.int32).view(ops.PAGE_DTYPE).reshape(-1)
+    ops.kv_write(kn.to(dev).reshape(n_new, -1), vn.to(dev).reshape(n_new, -1), Hkv * hd, posd, pool.rope,
+                 ops.to_device(pages, dev), len(pages), ka, va, aux_rows, 1, 0, Hkv, hd)
+    # chunks: selected groups at new positions, delta = new_start - orig_start
+    deltas, chunk_segs, new_start = [], [], 0
+    for b in sel:
+        deltas.append(new_start - int(pool.pos_start[b]))
+        chunk_segs.append((0, 0, pool.row0(b), lengths[b], ops.nat.SEG_FULL, len(deltas) - 1, 0, 0))
+        new_start += lengths[b]
+    rot = torch.from_numpy(ops.shift_table(deltas, hd, theta)).to(dev)
+    per = -(-len(chunk_segs) // splits)
+    groups_segs = [chunk_segs[i:i + per] for i in range(0, len(chunk_segs), per)]
+    groups_segs[-1] = groups_segs[-1] + [(1, 0, 0, n_new, ops.nat.SEG_SELF, -1, 0, 0)]
+    S = len(groups_segs)
+    num_m = 2 if n_new * gs > 128 else 1
+    assert n_new * gs <= 128 * num_m
+    rows = n_new * gs
+    works, segs = [], []
+    mgroups = []
+    for kv in range(Hkv):
+        base = kv * S * rows
+        for s, gseg in enumerate(groups_segs):
+            sb = len(segs)
+            segs += gseg
+            works.append((0, n_new, 0, kv, sb, len(segs), n_q, 1 if S > 1 else 0, base + s * rows))
+        mgroups.append((base, rows, S, 0, kv))
+    wa = np.zeros(len(works), dtype=ops.WORK_DTYPE)
+    for i, name in enumerate(ops.WORK_DTYPE.names):
+        wa[name] = [w[i] for w in works]
+    sa = np.array(segs, dtype=np.int32).view(ops.SEG_DTYPE).reshape(-1)
+    out = torch.zeros(n_new, H, hd, dtype=torch.bfloat16, device=dev)
+    part_o = torch.zeros(Hkv * S * rows, hd, dtype=torch.float32, device=dev)
+    part_l = torch.zeros(Hkv * S * rows, dtype=torch.float32, device=dev)
+    ops.attention(q=qn.to(dev), q_tok_stride=H * hd, tok_pos=posd, tok_lo=torch.tensor(lo, dtype=torch.int32,
+                  device=dev), rope=pool.rope, rot=rot, pool=(pool.kp, pool.vp, pool.rows, 1), aux=(ka, va, aux_rows, 1),
+                  n_heads=H, n_kv_heads=Hkv, head_dim=hd, works_dev=ops.to_device(wa, dev), n_works=len(wa),
+                  segs_dev=ops.to_device(sa, dev), num_m=num_m, out=out, out_tok_stride=H * hd, part_o=part_o,
+                  part_lse=part_l)
+    if S > 1:
+        ma = np.zeros(len(mgroups), dtype=ops.MERGE_DTYPE)
+        for i, name in enumerate(ops.MERGE_DTYPE.names):
+            ma[name] = [m[i] for m in mgroups]
+        ops.lse_merge(part_o, part_l, ops.to_device(ma, dev), len(ma), rows, H, Hkv, hd, out, H * hd)
+    torch.cuda.synchronize()
+    got = out.float().cpu().numpy()
+    # reference: assemble (rotate K at new positions 0..Tp-1), query at own positions, tree mask
+    Kc = np.concatenate([pool.k_pre[0, int(pool.pos_start[b]):int(pool.pos_start[b]) + lengths[b]].double().numpy()
+                         for b in sel])
+    Kc = _rope64(Kc, np.arange(Tp), theta)
+    Vc = np.concatenate([pool.v64(0, b) for b in sel])
+    Kn = _rope64(kn.double().numpy(), pos, theta)
+    q64 = _rope64(qn.double().numpy(), pos, theta)
+    K = np.concatenate([Kc, Kn])
+    V = np.concatenate([Vc, vn.double().numpy()])
+    mask = np.zeros((n_new, Tp + n_new), dtype=bool)
+    mask[:, :Tp] = True
+    for r in range(n_new):
+        for k in range(n_new):
+            mask[r, Tp + k] = k <= r and (k < n_q or k >= lo[r])
+    worst = 0.0
+    for kv in range(Hkv):
+        for h in range(gs):
+            head = kv * gs + h
+            want = _attend64(q64[:, head], K[:, kv], V[:, kv], mask, 1.0 / math.sqrt(hd))
+            worst = max(worst, float(np.abs(got[:, head] - want).max()))
+    return worst
+
+
+@pytest.mark.parametrize("splits", [1, 2, 3])
+@pytest.mark.parametrize("hd,H,Hkv,theta", [(128, 8, 2, 500000.0), (16, 4, 2, 10000.0), (64, 4, 4, 10000.0)])
+def test_stage2_split_kv_attention(hd, H, Hkv, theta, splits):
+    worst = _stage2_case(hd, H, Hkv, [100, 64, 300, 77, 150, 90], sel=[0, 2, 3, 5], n_q=20, labels=[4, 6, 3, 5],
+                         splits=splits, theta=theta)
+    assert worst < 2e-2, worst
+
+
+def _py_select(scores, budget, ordering):
+    n = len(scores)
+    cand = sorted(range(1, n), key=lambda u: (-scores[u], u))[: budget - 1]
+    if ordering == "in-order":
+        cand.sort()
+    elif ordering == "low-to-high":
+        cand.sort(key=lambda u: (scores[u], u))
+    else:
+        cand.sort(key=lambda u: -u)
+    return [0] + cand
+
+
+@pytest.mark.parametrize("n_units", [1, 2, 16, 60, 997])
+@pytest.mark.parametrize("ordering", ["in-order", "low-to-high", "reverse"])
+def test_topk_bit_exact(n_units, ordering):
+    rng = np.random.default_rng(n_units)
+    scores = rng.random((33, n_units))
+    scores[:, ::3] = np.round(scores[:, ::3], 1)  # ties
+    scores[0] = 0.0                               # all tied
+    dev_scores = torch.from_numpy(scores).cuda()
+    for ratio in (0.1, 0.3, 0.5, 1.0):
+        budget = math.ceil(ratio * n_units)
+        got = ops.topk_select(dev_scores, budget, ordering).cpu().numpy()
+        for q in range(scores.shape[0]):
+            assert list(got[q]) == _py_select(list(scores[q]), budget, ordering)
