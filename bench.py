@@ -1,0 +1,425 @@
+"""Headline benchmark: DBSA stage-2 per-query latency at the Llama-3.1-8B
+shape over a 90k-token pool at 30 % retrieval (BASELINE.json metric, configs
+C2/C3), with the stage-1 pre-encode of that pool measured alongside.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--impl ours|reference]
+
+One process per GPU (torchrun for N > 1).  Stage 2 is query-data-parallel:
+every rank holds the weights and the pool cache and answers its own B
+queries per step (weak scaling); no collective on the data path.  A "step" =
+one batch of B synthetic test queries through the hot path: K4 group
+selection on the device over float64 retrieval scores, one tree-masked
+forward of query + 4 labels against the selected groups' pages (K3/K3m per
+layer), label scoring and argmax.
+
+value  = device time of K steps (CUDA events, inputs resident in HBM, work
+         tables prebuilt), ms per query over all ranks.
+e2e    = the same steps through the public API (Stage2Session.answer) from
+         pinned host buffers: H2D of query ids + scores, host planning, D2H
+         of the predicted labels, all inside the timed region.
+--impl reference times the reference algorithm (the numpy CPU oracle,
+oracle/dbsa_oracle.py, which restates pkg/src/dbsa) on this host's cores on
+bounded samples of the same workload and extrapolates to ms per query.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "stage-2 per-query latency (ms) @90k pool, 30% retrieval; stage-1 pre-encode tok/s"
+UNIT = "ms/query"
+
+# Llama-3.1-8B shape
+CFG8B = dict(d_model=4096, n_layers=32, n_heads=32, n_kv_heads=8, head_dim=128, ffn_dim=14336, vocab_size=128256,
+             rope_theta=500000.0, norm_eps=1e-5, max_seq_len=131072)
+N_GROUPS, GROUP_TOK = 60, 1500
+Q_TOK, N_LABELS, LABEL_TOK = 32, 4, 4
+RATIO = 0.30
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return (float(d.get("hbm_gbs", 6537.3)), float(d.get("bf16_tflops", 1701.9)),
+                float(d.get("bf16_tflops_sustained", 1438.9)), "MEASURED_PEAKS.json")
+    # the driver's measurement for this pool, as recorded in BASELINE.md §2
+    return 6537.3, 1701.9, 1438.9, "MEASURED_PEAKS.json values recorded in BASELINE.md §2"
+
+
+def traffic_for(kernel: str, cfg_key: str):
+    p = ROOT / "profiles" / "traffic.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d.get(f"{kernel}@{cfg_key}")
+    return None
+
+
+class Clocks:
+    """nvidia-smi sampler for the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            out, _ = self.proc.communicate(timeout=10)
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        for l in getattr(self, "lines", []):
+            f = [x.strip() for x in l.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for name, col in (("hw_slowdown", 5), ("hw_thermal_slowdown", 6), ("sw_thermal_slowdown", 7),
+                              ("sw_power_cap", 8)):
+                if f[col].lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+class KernelTimer:
+    """CUDA events around every launch of one kernel family, on its stream."""
+
+    def __init__(self):
+        self.pairs = []
+
+    def wrap(self, fn):
+        import torch
+
+        def inner(*a, **k):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            r = fn(*a, **k)
+            e.record()
+            self.pairs.append((s, e))
+            return r
+
+        return inner
+
+    def mean_ms(self):
+        if not self.pairs:
+            return None
+        return sum(s.elapsed_time(e) for s, e in self.pairs) / len(self.pairs)
+
+
+# ------------------------------------------------------------------ workload
+def synth_pool(seed=0):
+    rng = np.random.default_rng(seed)
+    return [rng.integers(3, CFG8B["vocab_size"], size=GROUP_TOK).tolist() for _ in range(N_GROUPS)]
+
+
+def synth_queries(n, seed):
+    rng = np.random.default_rng(seed)
+    q = [rng.integers(3, CFG8B["vocab_size"], size=Q_TOK).tolist() for _ in range(n)]
+    scores = rng.random((n, N_GROUPS))  # float64 retrieval scores per (query, group)
+    return q, scores
+
+
+def label_ids():
+    rng = np.random.default_rng(12345)
+    return [rng.integers(3, CFG8B["vocab_size"], size=LABEL_TOK).tolist() for _ in range(N_LABELS)]
+
+
+def run_ours(args):
+    import hashlib
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2503_08640_b200 as P
+    from paper_2503_08640_b200 import engine, masks, ops
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    cfg = P.ModelConfig(**CFG8B)
+    dm = engine.DeviceModel.random(cfg, seed=0, device=dev)
+    pool = synth_pool(0)
+    blocks = [(ids, hashlib.sha256(np.asarray(ids, np.int64).tobytes()).digest(), ()) for ids in pool]
+    pattern = masks.AttentionPattern.sink_prev_self(2)
+
+    # ---------------- stage 1 (C2): pre-encode the 90k pool (warm-up encode, then timed)
+    k1 = KernelTimer()
+    orig_attn = ops.attention
+    s1_times = []
+    cache = None
+    for it in range(2):
+        cache = P.SegmentedKVCache(cfg, dev, capacity_tokens=N_GROUPS * GROUP_TOK)
+        if it == 1:
+            ops.attention = k1.wrap(orig_attn)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        pairs = P.encode_blocks(dm, cache, blocks, pattern)
+        b.record()
+        torch.cuda.synchronize()
+        ops.attention = orig_attn
+        s1_times.append(a.elapsed_time(b))
+    cache.seal()
+    s1_ms = s1_times[-1]
+    hbm, tf_burst, tf_sus, peak_src = peaks()
+    k1_ms = k1.mean_ms()
+    k1_flops = pairs * 4 * cfg.head_dim * cfg.n_heads  # one layer (metrics.py:21-22)
+    stage1 = {"metric": "stage-1 pre-encode tok/s", "value": N_GROUPS * GROUP_TOK / (s1_ms / 1e3), "unit": "tok/s",
+              "ms": s1_ms, "pool_tokens": N_GROUPS * GROUP_TOK, "attended_pairs": pairs,
+              "roofline": {"kernel": "dbsa_attn_kernel (K1)", "bound": "tensor",
+                           "achieved": k1_flops / (k1_ms / 1e3) / 1e12 if k1_ms else None,
+                           "peak": tf_burst, "unit": "TFLOP/s",
+                           "frac": (k1_flops / (k1_ms / 1e3) / 1e12) / tf_burst if k1_ms else None,
+                           "traffic": traffic_for("k1", "c2"), "launch_ms": k1_ms,
+                           "flops_per_launch": k1_flops, "share_of_step": (k1_ms * cfg.n_layers) / s1_ms,
+                           "peak_source": peak_src}}
+
+    # ---------------- stage 2 (C3 at 30 %)
+    sess = P.Stage2Session(dm, cache, [(g, 0, GROUP_TOK) for g in range(N_GROUPS)], label_ids(), RATIO, "in-order")
+    B, K, W = args.batch, args.steps, args.warmup
+    steps = []
+    for s in range(W + K):
+        q, sc = synth_queries(B, seed=1000 * rank + s)
+        ids = sess.select(sc)
+        jobs, plan = sess.plan(ids, q)
+        sc_dev = torch.from_numpy(sc).to(dev)
+        steps.append((q, sc, sc_dev, jobs, plan))
+    torch.cuda.synchronize()
+
+    def device_step(st):
+        _, _, sc_dev, jobs, plan = st
+        ops.topk_select(sc_dev, sess.budget, "in-order")
+        return sess.run(jobs, plan)
+
+    for st in steps[:W]:
+        device_step(st)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    k3 = KernelTimer()
+    ops.attention = k3.wrap(orig_attn)
+    n0 = ops.LAUNCHES
+    with Clocks(local) as clk:
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        for st in steps[W:]:
+            device_step(st)
+        ev1.record()
+        torch.cuda.synchronize()
+    ops.attention = orig_attn
+    launches = ops.LAUNCHES - n0
+    dev_ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([dev_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_ms = float(t.item())
+    n_queries = B * K * world
+    value = dev_ms / n_queries
+
+    # ---------------- e2e through the public API from pinned host buffers
+    host = []
+    for s in range(K):
+        q, sc = synth_queries(B, seed=777000 + 1000 * rank + s)
+        host.append((q, torch.from_numpy(sc).pin_memory()))
+    for q, sc in host[:1]:
+        sess.answer(sc.numpy(), q)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    h2d = d2h = 0
+    for q, sc in host:
+        ids, s_dev, best = sess.answer(sc.numpy(), q)
+        out = best.cpu()
+        h2d += sc.numel() * 8 + B * Q_TOK * 8
+        d2h += out.numel() * out.element_size() + ids.size * 4
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    # roofline of K3 (dominant stage-2 kernel): algorithmic bytes per launch =
+    # selected KV (2 * Hkv * hd * 2 B per token, one layer) + Q in + O out.
+    plan0 = steps[W][4]
+    kv_bytes = plan0.kv_tokens * 2 * cfg.n_kv_heads * cfg.head_dim * 2
+    qo_bytes = 2 * plan0.n_tok * cfg.n_heads * cfg.head_dim * 2
+    k3_ms = k3.mean_ms()
+    achieved = (kv_bytes + qo_bytes) / (k3_ms / 1e3) / 1e9 if k3_ms else None
+    clocks = clk.summary()
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": dev_ms / K, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic (random-init weights, uniform token ids, U(0,1) f64 retrieval scores)",
+        "config": {"workload": "C3: Llama-3.1-8B shape, 90k-token pool (60 groups x 1500), 30% retrieval "
+                               "(18 groups, T'=27000), query 32 tok + 4 labels x 4 tok",
+                   "queries_per_step_per_gpu": B, "parallelism": f"query-dp{world}",
+                   "l2": "inputs larger than L2 (12.1 GB KV pages + 16 GB weights per GPU)"},
+        "e2e": {"value": e2e_ms / n_queries, "unit": UNIT, "h2d_bytes_per_step": h2d // K,
+                "d2h_bytes_per_step": d2h // K},
+        "roofline": {"kernel": "dbsa_attn_kernel (K3)", "bound": "hbm", "achieved": achieved, "peak": hbm,
+                     "unit": "GB/s", "frac": achieved / hbm if achieved else None,
+                     "traffic": traffic_for("k3", "c3"), "launch_ms": k3_ms,
+                     "bytes_per_launch": kv_bytes + qo_bytes,
+                     "share_of_step": (k3_ms * cfg.n_layers) / (dev_ms / K) if k3_ms else None,
+                     "peak_source": peak_src},
+        "stage1": stage1,
+        "gpu_launches": launches,
+        "clocks": clocks,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cb = cpu_reference_sample(steps=1, seconds=args.cpu_seconds)
+        line["cpu_baseline"] = cb
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------ CPU reference arm
+def cpu_reference_sample(steps=1, seconds=20.0):
+    """Time the reference algorithm (oracle port of pkg/src/dbsa) at the exact
+    Llama-3.1-8B stage-2 shapes on this host, extrapolated to ms/query:
+    per query = 32 layers x (assemble one layer over T'=27000) +
+    4 labels x 32 layers x (one layer of _forward over 36 tokens against T')."""
+    from oracle import dbsa_oracle as O
+
+    c = CFG8B
+    hd, H, Hkv, d, f = c["head_dim"], c["n_heads"], c["n_kv_heads"], c["d_model"], c["ffn_dim"]
+    Tp = int(math.ceil(RATIO * N_GROUPS)) * GROUP_TOK
+    n_new = Q_TOK + LABEL_TOK
+    rng = np.random.default_rng(0)
+    lim = 1.0 / np.sqrt(d)
+    w = {k: rng.uniform(-lim, lim, size=s).astype(np.float32) for k, s in
+         (("wq", (d, H * hd)), ("wk", (d, Hkv * hd)), ("wv", (d, Hkv * hd)), ("wo", (H * hd, d)),
+          ("w_gate", (d, f)), ("w_up", (d, f)), ("w_down", (f, d)))}
+    k_pre = rng.standard_normal((Tp, Hkv, hd)).astype(np.float32)
+    v = rng.standard_normal((Tp, Hkv, hd)).astype(np.float32)
+    h = rng.standard_normal((n_new, d)).astype(np.float32)
+    ones = np.ones(d, np.float32)
+    layer_s, asm_s = [], []
+    t_end = time.perf_counter() + seconds
+    for _ in range(max(1, steps)):
+        t0 = time.perf_counter()
+        k_rot = O.rope(k_pre, np.arange(Tp), c["rope_theta"])  # assemble: rotate at new positions
+        vv = v.copy()
+        asm_s.append(time.perf_counter() - t0)
+        t0 = time.perf_counter()
+        pos = np.arange(Tp, Tp + n_new)
+        x = O.rms_norm(h, ones, 1e-5)
+        q = O.mm(x, w["wq"]).reshape(n_new, H, hd)
+        k = O.mm(x, w["wk"]).reshape(n_new, Hkv, hd)
+        vn = O.mm(x, w["wv"]).reshape(n_new, Hkv, hd)
+        qr, kr = O.rope(q, pos, c["rope_theta"]), O.rope(k, pos, c["rope_theta"])
+        mask = O.query_mask(Tp, n_new)
+        gs = H // Hkv
+        gmask = np.vstack([mask] * gs)
+        att = np.empty((n_new, H, hd), np.float32)
+        for g in range(Hkv):
+            ka = np.concatenate([k_rot[:, g], kr[:, g]])
+            va = np.concatenate([vv[:, g], vn[:, g]])
+            qg = qr[:, g * gs:(g + 1) * gs].transpose(1, 0, 2).reshape(gs * n_new, hd)
+            o = O.masked_attention((qg / np.sqrt(hd)).astype(np.float32), ka, va, gmask)
+            att[:, g * gs:(g + 1) * gs] = o.reshape(gs, n_new, hd).transpose(1, 0, 2)
+        h2 = (h.astype(np.float64) + O.mm(att.reshape(n_new, -1), w["wo"])).astype(np.float32)
+        x = O.rms_norm(h2, ones, 1e-5)
+        _ = O.mm(O.silu_gate(O.mm(x, w["w_gate"]), O.mm(x, w["w_up"])), w["w_down"])
+        layer_s.append(time.perf_counter() - t0)
+        if time.perf_counter() > t_end:
+            break
+    L = c["n_layers"]
+    per_query = L * float(np.median(asm_s)) + N_LABELS * L * float(np.median(layer_s))
+    cores = len(os.sched_getaffinity(0))
+    return {"value": per_query * 1e3, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{len(layer_s)} x (one layer of reference _forward for one label, 36 tok vs T'={Tp}, 8B shape; "
+                      f"plus one layer of assemble); extrapolated x{N_LABELS} labels x{L} layers; numpy/OpenBLAS "
+                      f"threads={os.environ.get('OPENBLAS_NUM_THREADS', 'default')}",
+            "layer_label_s": float(np.median(layer_s)), "assemble_layer_s": float(np.median(asm_s))}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    samples = []
+    for _ in range(args.warmup):
+        cpu_reference_sample(steps=1, seconds=0)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        samples.append(cpu_reference_sample(steps=1, seconds=0))
+    wall = time.perf_counter() - t0
+    v = float(np.median([s["value"] for s in samples]))
+    cb = dict(samples[-1])
+    cb["value"] = v
+    cb["sample"] = cb["sample"] + f"; {args.steps} steps"
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall * 1e3 / max(1, args.steps),
+            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": "C3: Llama-3.1-8B shape, 90k-token pool, 30% retrieval, query 32 tok + 4 labels",
+                       "parallelism": "host CPU"},
+            "cpu_baseline": cb, "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--batch", type=int, default=64)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

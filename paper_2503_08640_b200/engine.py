@@ -1,0 +1,663 @@
+"""Device orchestration of the DBSA hot path on one B200.
+
+Stage 1 (reference: pipeline.encode_blocks, pipeline.py:166-233) runs
+LAYER-SYNCHRONOUSLY over all new groups at once -- legal because splitting at
+group boundaries equals one forward under the token-level mask
+(test_model.py:152-170, test_acceptance.py:60-108): per layer one QKV GEMM
+over every pool token, one K2w launch writing every group's rotated K and V^T
+into its pages, one K1 launch in which every CTA streams [sink, prev-j groups,
+self-causal] for a 256-row slab of one group, then O-proj and FFN.
+
+Stage 2 (reference: Runner.infer / score_label, pipeline.py:369-421,
+model.py:420-443) scores ALL labels of a query in one forward: the query
+tokens followed by every label, each label at positions T'+|q|.., with a tree
+mask (label tokens see the query and their own label, causally) -- so the
+selected KV is read once per query, not once per label.  Queries are batched:
+the dense GEMMs see every new token of the batch, and K3 runs one CTA per
+(query, kv head, KV split) over the query's chunk table (the selected groups'
+page ranges, no assembled copy), with fp32 partials merged by K3m.
+
+Torch is plumbing here (device memory, the current stream, cuBLAS GEMMs for
+the dense projections); every attention / page / selection step is a kernel
+of libdbsa_sm100a.so.  There is no CPU path: without CUDA this raises.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from . import _native as nat
+from . import ops
+from .errors import ConfigError, ValidationError
+
+PAGE = ops.PAGE
+SEG_FULL, SEG_SELF = nat.SEG_FULL, nat.SEG_SELF
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def default_device(device=None):
+    torch = _torch()
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2503_08640_b200 needs a CUDA (sm_100a) device; there is no CPU fallback")
+    if device is None:
+        return torch.device("cuda", torch.cuda.current_device())
+    dev = torch.device(device)
+    if dev.type != "cuda":
+        raise RuntimeError(f"device {dev} is not a CUDA device; there is no CPU fallback")
+    return dev if dev.index is not None else torch.device("cuda", torch.cuda.current_device())
+
+
+# ============================================================== weights
+class DeviceModel:
+    """Weights resident in HBM, laid out for the fused projections:
+    wqkv = [wq | wk | wv] (d, (H + 2 Hkv) hd) and wgu = [w_gate | w_up]
+    (d, 2 ffn) as bf16 GEMM operands; embedding, norms and the residual
+    stream stay fp32 (the reference's f32 storage, kernels.py:1-7)."""
+
+    def __init__(self, config, device, embed, layers, out_norm, lm_head):
+        self.config = config
+        self.device = device
+        self.embed = embed
+        self.layers = layers
+        self.out_norm = out_norm
+        self.lm_head = lm_head
+        self.rope = ops.rope_table(config.max_seq_len, config.head_dim, config.rope_theta, device)
+        self.config_hash = config.hash_bytes()
+
+    @classmethod
+    def from_weights(cls, weights, device):
+        torch = _torch()
+        t = weights.tensors
+
+        def f32(name):
+            return torch.from_numpy(np.ascontiguousarray(t[name])).to(device)
+
+        def bf(*names):
+            arr = np.concatenate([t[n] for n in names], axis=1) if len(names) > 1 else t[names[0]]
+            return torch.from_numpy(np.ascontiguousarray(arr)).to(device).to(torch.bfloat16)
+
+        layers = []
+        for i in range(weights.config.n_layers):
+            p = f"layers.{i}."
+            layers.append(dict(attn_norm=f32(p + "attn_norm"), wqkv=bf(p + "wq", p + "wk", p + "wv"),
+                               wo=bf(p + "wo"), ffn_norm=f32(p + "ffn_norm"), wgu=bf(p + "w_gate", p + "w_up"),
+                               wdown=bf(p + "w_down")))
+        return cls(weights.config, device, f32("tok_embed"), layers, f32("out_norm"), bf("lm_head"))
+
+    @classmethod
+    def random(cls, config, seed: int = 0, device=None):
+        """Device-side random init with the reference's scaled-uniform scheme
+        (model.py:159-171): norms 1, embedding U(+-0.1), projections
+        U(+-1/sqrt(fan_in)).  Used for the Llama-scale configurations whose
+        float32 host copy would not be practical; not bit-identical to
+        init_random's Philox stream."""
+        torch = _torch()
+        dev = default_device(device)
+        g = torch.Generator(device=dev)
+        g.manual_seed(int(seed))
+        c = config
+        qw, kw = c.n_heads * c.head_dim, c.n_kv_heads * c.head_dim
+
+        def u(shape, fan_in, dtype=torch.bfloat16):
+            b = 1.0 / math.sqrt(fan_in)
+            return torch.empty(shape, dtype=dtype, device=dev).uniform_(-b, b, generator=g)
+
+        ones = lambda n: torch.ones(n, dtype=torch.float32, device=dev)  # noqa: E731
+        layers = [dict(attn_norm=ones(c.d_model), wqkv=u((c.d_model, qw + 2 * kw), c.d_model),
+                       wo=u((qw, c.d_model), qw), ffn_norm=ones(c.d_model),
+                       wgu=u((c.d_model, 2 * c.ffn_dim), c.d_model), wdown=u((c.ffn_dim, c.d_model), c.ffn_dim))
+                  for _ in range(c.n_layers)]
+        embed = torch.empty((c.vocab_size, c.d_model), dtype=torch.float32, device=dev).uniform_(-0.1, 0.1, generator=g)
+        return cls(c, dev, embed, layers, ones(c.d_model), u((c.d_model, c.vocab_size), c.d_model))
+
+    def nbytes(self) -> int:
+        n = self.embed.numel() * 4 + self.lm_head.numel() * 2
+        for lw in self.layers:
+            n += sum(v.numel() * v.element_size() for v in lw.values())
+        return n
+
+
+# ============================================================== page store (K2)
+class PageStore:
+    """The cache's HBM page pool.  K [L][Hkv][rows][HDP], V^T [L][Hkv][HDP][rows]
+    (bf16); rows are handed out in whole 64-token pages per group."""
+
+    def __init__(self, config, device, capacity_tokens: int = 0):
+        self.config = config
+        self.device = device
+        self.hdp = ops.hd_pad(config.head_dim)
+        self.used_rows = 0
+        self.rows = 0
+        self.k = self.v = None
+        self._rope = None
+        if capacity_tokens:
+            self._grow(_round_page(capacity_tokens) + PAGE)
+
+    @property
+    def rope(self):
+        if self._rope is None:
+            self._rope = ops.rope_table(self.config.max_seq_len, self.config.head_dim, self.config.rope_theta,
+                                        self.device)
+        return self._rope
+
+    def _grow(self, rows: int) -> None:
+        torch = _torch()
+        c = self.config
+        rows = _round_page(rows)
+        k = torch.zeros((c.n_layers, c.n_kv_heads, rows, self.hdp), dtype=torch.bfloat16, device=self.device)
+        v = torch.zeros((c.n_layers, c.n_kv_heads, self.hdp, rows), dtype=torch.bfloat16, device=self.device)
+        if self.k is not None and self.used_rows:
+            k[:, :, : self.used_rows].copy_(self.k[:, :, : self.used_rows])
+            v[..., : self.used_rows].copy_(self.v[..., : self.used_rows])
+        self.k, self.v, self.rows = k, v, rows
+
+    def reserve(self, counts) -> list[int]:
+        need = sum(_round_page(n) for n in counts)
+        if self.used_rows + need > self.rows:
+            self._grow(max(self.used_rows + need, self.rows + self.rows // 2))
+        out = []
+        for n in counts:
+            out.append(self.used_rows)
+            self.used_rows += _round_page(n)
+        return out
+
+    def nbytes(self) -> int:
+        return 0 if self.k is None else 2 * self.k.numel() * 2
+
+    def planes(self):
+        return (self.k, self.v, self.rows, self.config.n_layers)
+
+    def write_host_group(self, entry, pre_kv) -> None:
+        """Upload one group's host pre-rotation K/V and write its pages (K2w)."""
+        torch = _torch()
+        c = self.config
+        n = entry.token_count
+        pos = torch.arange(entry.pos_start, entry.pos_end, dtype=torch.int32, device=self.device)
+        pages = _pages_for([(0, n, entry.row0)])
+        pdev = ops.to_device(pages, self.device)
+        for layer, (k, v) in enumerate(pre_kv):
+            ks = torch.from_numpy(np.ascontiguousarray(k, np.float32)).to(self.device).to(torch.bfloat16)
+            vs = torch.from_numpy(np.ascontiguousarray(v, np.float32)).to(self.device).to(torch.bfloat16)
+            ops.kv_write(ks.reshape(n, -1), vs.reshape(n, -1), c.n_kv_heads * c.head_dim, pos, self.rope, pdev,
+                         len(pages), self.k, self.v, self.rows, c.n_layers, layer, c.n_kv_heads, c.head_dim)
+        torch.cuda.current_stream(self.device).synchronize()
+
+    def read_rows(self, layer: int, row0: int, n: int):
+        """(K rotated, V) float32 (n, Hkv, hd) of a row range (host copy)."""
+        hd = self.config.head_dim
+        k = self.k[layer, :, row0:row0 + n, :hd].float().permute(1, 0, 2).cpu().numpy()
+        v = self.v[layer, :, :hd, row0:row0 + n].float().permute(2, 0, 1).cpu().numpy()
+        return np.ascontiguousarray(k), np.ascontiguousarray(v)
+
+
+def _round_page(n: int) -> int:
+    return -(-int(n) // PAGE) * PAGE
+
+
+def _pages_for(spans) -> np.ndarray:
+    """spans: (first token in the source buffer, n_tok, first destination row)."""
+    out = []
+    for tok0, n, row0 in spans:
+        for i in range(0, n, PAGE):
+            out.append((tok0 + i, min(PAGE, n - i), row0 + i, 0))
+    return np.array(out, dtype=np.int32).reshape(-1, 4).view(ops.PAGE_DTYPE).reshape(-1)
+
+
+def _seg_array(segs) -> np.ndarray:
+    a = np.zeros(len(segs), dtype=ops.SEG_DTYPE)
+    if segs:
+        s = np.asarray(segs, dtype=np.int32).reshape(len(segs), -1)
+        for i, name in enumerate(("src", "layer", "row0", "n_tok", "kind", "rot")):
+            a[name] = s[:, i]
+    return a
+
+
+def _per_layer_segs(seg_arr: np.ndarray, n_layers: int) -> np.ndarray:
+    """[L, n_segs]: pool segments (src 0) address layer l, aux (src 1) layer 0."""
+    out = np.repeat(seg_arr[None, :], n_layers, axis=0)
+    pool = out["src"] == 0
+    out["layer"] = np.where(pool, np.arange(n_layers, dtype=np.int32)[:, None], 0)
+    return out
+
+
+def _work_array(works) -> np.ndarray:
+    a = np.zeros(len(works), dtype=ops.WORK_DTYPE)
+    if works:
+        w = np.asarray(works, dtype=np.int64).reshape(len(works), -1)
+        for i, name in enumerate(ops.WORK_DTYPE.names):
+            a[name] = w[:, i]
+    return a
+
+
+# ============================================================== dense block
+def mm_f32(a, b, out):
+    """out (fp32) = a @ b for bf16 operands, fp32 accumulate and output (cuBLAS)."""
+    torch = _torch()
+    try:
+        return torch.mm(a, b, out_dtype=torch.float32, out=out)
+    except (TypeError, RuntimeError):
+        out.copy_(torch.mm(a, b, out_dtype=torch.float32))
+        return out
+
+
+class _Scratch:
+    """Per-forward activation buffers, reused across layers."""
+
+    def __init__(self, dm, n_tok):
+        torch = _torch()
+        c, dev = dm.config, dm.device
+        qw, kw = c.n_heads * c.head_dim, c.n_kv_heads * c.head_dim
+        self.x = torch.empty((n_tok, c.d_model), dtype=torch.bfloat16, device=dev)
+        self.qkv = torch.empty((n_tok, qw + 2 * kw), dtype=torch.bfloat16, device=dev)
+        self.att = torch.empty((n_tok, qw), dtype=torch.bfloat16, device=dev)
+        self.proj = torch.empty((n_tok, c.d_model), dtype=torch.float32, device=dev)
+        self.ffn_chunk = max(1, min(n_tok, (1 << 31) // (2 * c.ffn_dim * 2)))
+        self.gu = torch.empty((min(n_tok, self.ffn_chunk), 2 * c.ffn_dim), dtype=torch.bfloat16, device=dev)
+        self.act = torch.empty((min(n_tok, self.ffn_chunk), c.ffn_dim), dtype=torch.bfloat16, device=dev)
+
+
+def _decoder(dm, ids_dev, attend, write_kv, n_layers=None):
+    """Pre-norm decoder body (model.py:319-359) over n new tokens.  `write_kv(l,
+    qkv)` stores the layer's keys/values, `attend(l, qkv, out)` fills the
+    attention output.  Returns the fp32 final hidden states."""
+    torch = _torch()
+    c = dm.config
+    n = ids_dev.shape[0]
+    s = _Scratch(dm, n)
+    h = dm.embed.index_select(0, ids_dev)
+    L = c.n_layers if n_layers is None else n_layers
+    for layer in range(L):
+        lw = dm.layers[layer]
+        ops.rmsnorm(h, lw["attn_norm"], c.norm_eps, out=s.x)
+        torch.mm(s.x, lw["wqkv"], out=s.qkv)
+        write_kv(layer, s.qkv)
+        attend(layer, s.qkv, s.att)
+        mm_f32(s.att, lw["wo"], s.proj)
+        h.add_(s.proj)
+        ops.rmsnorm(h, lw["ffn_norm"], c.norm_eps, out=s.x)
+        for a in range(0, n, s.ffn_chunk):
+            b = min(n, a + s.ffn_chunk)
+            gu, act = s.gu[: b - a], s.act[: b - a]
+            torch.mm(s.x[a:b], lw["wgu"], out=gu)
+            ops.silu_mul(gu, c.ffn_dim, out=act)
+            mm_f32(act, lw["wdown"], s.proj[a:b])
+        h.add_(s.proj)
+    return h
+
+
+# ============================================================== stage 1 (K1 + K2w)
+class Stage1Plan:
+    """Device tables of one layer-synchronous stage-1 encode of groups
+    `new` (BlockEntry list; their tokens are contiguous, first at tok_base)."""
+
+    def __init__(self, dm, cache, new, pattern):
+        c = dm.config
+        gs, hkv = c.group_size, c.n_kv_heads
+        self.tok_base = new[0].pos_start
+        self.n_tok = new[-1].pos_end - self.tok_base
+        longest = max(e.token_count for e in new)
+        self.num_m = 2 if longest * gs > 128 else 1
+        slab = (128 * self.num_m) // gs
+        if slab < 1:
+            raise ConfigError(f"group size {gs} exceeds the 256 rows of one K1 work")
+        segs, works = [], []
+        pairs = 0
+        for e in new:
+            ctx = [cache.blocks[j] for j in pattern.context_of(e.block_id)]
+            n_ctx = sum(x.token_count for x in ctx)
+            local0 = e.pos_start - self.tok_base
+            t = e.token_count
+            pairs += n_ctx * t + t * (t + 1) // 2
+            for t0 in range(0, t, slab):
+                nt = min(slab, t - t0)
+                sb = len(segs)
+                segs += [(0, 0, x.row0, x.token_count, SEG_FULL, -1) for x in ctx]
+                segs.append((0, 0, e.row0, t0 + nt, SEG_SELF, -1))
+                keys = n_ctx + t0 + nt
+                for kv in range(hkv):
+                    works.append((keys, local0 + t0, nt, local0, kv, sb, len(segs), 0, 0, 0))
+        works.sort(key=lambda w: -w[0])  # longest key streams first: a shorter tail wave
+        self.pairs = pairs
+        self.n_works = len(works)
+        self.n_segs = len(segs)
+        self.keys_visited = sum(w[0] * w[2] * gs for w in works)
+        dev = dm.device
+        self.works = ops.to_device(_work_array([w[1:] for w in works]), dev)
+        self.segs = ops.to_device(_per_layer_segs(_seg_array(segs), c.n_layers), dev)
+        pages = _pages_for([(e.pos_start - self.tok_base, e.token_count, e.row0) for e in new])
+        self.n_pages = len(pages)
+        self.pages = ops.to_device(pages, dev)
+        torch = _torch()
+        self.pos = torch.arange(self.tok_base, self.tok_base + self.n_tok, dtype=torch.int32, device=dev)
+
+    def segs_ptr(self, layer: int) -> int:
+        return self.segs.data_ptr() + layer * self.n_segs * ops.SEG_DTYPE.itemsize
+
+
+def encode_groups(dm, cache, new, ids, pattern, layers=None) -> int:
+    """Stage 1 for groups `new` whose concatenated token ids are `ids`; writes
+    their pages in every layer.  Returns the attended pair count
+    (pipeline.py:231-232)."""
+    torch = _torch()
+    c = dm.config
+    plan = Stage1Plan(dm, cache, new, pattern)
+    store = cache.store
+    qw, kw = c.n_heads * c.head_dim, c.n_kv_heads * c.head_dim
+    stride = qw + 2 * kw
+    ids_dev = torch.as_tensor(np.asarray(ids, dtype=np.int64)).to(dm.device, non_blocking=True)
+
+    def write_kv(layer, qkv):
+        ops.kv_write(qkv[:, qw:], qkv[:, qw + kw:], stride, plan.pos, dm.rope, plan.pages, plan.n_pages, store.k,
+                     store.v, store.rows, c.n_layers, layer, c.n_kv_heads, c.head_dim)
+
+    def attend(layer, qkv, out):
+        ops.attention(q=qkv, q_tok_stride=stride, tok_pos=plan.pos, tok_lo=None, rope=dm.rope, rot=None,
+                      pool=store.planes(), aux=None, n_heads=c.n_heads, n_kv_heads=c.n_kv_heads, head_dim=c.head_dim,
+                      works_dev=plan.works, n_works=plan.n_works, segs_dev=plan.segs_ptr(layer), num_m=plan.num_m,
+                      out=out, out_tok_stride=qw)
+
+    _decoder(dm, ids_dev, attend, write_kv, n_layers=layers)
+    return plan.pairs
+
+
+# ============================================================== stage 2 (K3 + K3m)
+class QueryJob:
+    """One stage-2 forward: new tokens (query, then label branches) against a
+    chunk table.  pos/lo are LOCAL (position = n_ctx + pos; lo = lowest
+    non-prefix self key visible, tree mask)."""
+
+    __slots__ = ("chunks", "n_ctx", "ids", "pos", "lo", "prefix")
+
+    def __init__(self, chunks, n_ctx, ids, pos, lo, prefix):
+        self.chunks, self.n_ctx, self.ids, self.pos, self.lo, self.prefix = chunks, n_ctx, ids, pos, lo, prefix
+
+
+def label_job(chunks, n_ctx, query_ids, labels) -> QueryJob:
+    """Query followed by every label as a branch of a token tree."""
+    nq = len(query_ids)
+    ids, pos, lo = list(query_ids), list(range(nq)), [0] * nq
+    for lab in labels:
+        start = len(ids)
+        ids += list(lab)
+        pos += list(range(nq, nq + len(lab)))
+        lo += [start] * len(lab)
+    return QueryJob(chunks, n_ctx, ids, pos, lo, nq)
+
+
+class Stage2Plan:
+    """Device tables for a batch of QueryJobs."""
+
+    def __init__(self, dm, jobs, target_ctas: int | None = None):
+        torch = _torch()
+        c = dm.config
+        gs, hkv, hd = c.group_size, c.n_kv_heads, c.head_dim
+        self.n_jobs = len(jobs)
+        n_new = [len(j.ids) for j in jobs]
+        self.tok0 = np.concatenate([[0], np.cumsum(n_new)]).astype(np.int64)
+        self.n_tok = int(self.tok0[-1])
+        self.num_m = 2 if max(n_new) * gs > 128 else 1
+        slab = (128 * self.num_m) // gs
+        if slab < 1:
+            raise ConfigError(f"group size {gs} exceeds the 256 rows of one K3 work")
+        aux_rows = [_round_page(n) for n in n_new]
+        self.aux_row0 = np.concatenate([[0], np.cumsum(aux_rows)]).astype(np.int64)
+        self.aux_rows = int(self.aux_row0[-1])
+        n_sms = 148
+        target = target_ctas or 4 * n_sms
+        segs, works, merges, rots = [], [], [], []
+        part_rows = 0
+        kv_bytes = 0
+        for qi, j in enumerate(jobs):
+            n = n_new[qi]
+            slabs = [(t0, min(slab, n - t0)) for t0 in range(0, n, slab)]
+            ch = np.asarray(j.chunks, dtype=np.int64).reshape(-1, 3)
+            kv_bytes += int(ch[:, 1].sum()) if len(ch) else 0
+            n_split = max(1, min(len(ch), -(-target // max(1, len(jobs) * hkv * len(slabs)))))
+            bounds = _split_bounds(ch[:, 1] if len(ch) else np.zeros(0, np.int64), n_split)
+            chunk_segs = []
+            for row, cnt, delta in ch:
+                rot = -1
+                if delta != 0:
+                    rot = len(rots)
+                    rots.append(int(delta))
+                chunk_segs.append((0, 0, int(row), int(cnt), SEG_FULL, rot))
+            split_ranges = []
+            for s in range(n_split):
+                sb = len(segs)
+                segs += chunk_segs[bounds[s]:bounds[s + 1]]
+                split_ranges.append((sb, len(segs)))
+            q0 = int(self.tok0[qi])
+            for t0, nt in slabs:
+                rows = nt * gs
+                last_sb = len(segs)
+                segs += chunk_segs[bounds[n_split - 1]:bounds[n_split]]
+                segs.append((1, 0, int(self.aux_row0[qi]), t0 + nt, SEG_SELF, -1))
+                last = (last_sb, len(segs))
+                for kv in range(hkv):
+                    base = part_rows
+                    mode = 1 if n_split > 1 else 0
+                    for s in range(n_split):
+                        sb, se = last if s == n_split - 1 else split_ranges[s]
+                        works.append((q0 + t0, nt, q0, kv, sb, se, j.prefix, mode, base + s * rows))
+                    if n_split > 1:
+                        merges.append((base, rows, n_split, q0 + t0, kv))
+                        part_rows += n_split * rows
+        self.kv_tokens = kv_bytes
+        self.n_works, self.n_segs, self.n_merge = len(works), len(segs), len(merges)
+        dev = dm.device
+        self.works = ops.to_device(_work_array(works), dev)
+        self.segs = ops.to_device(_per_layer_segs(_seg_array(segs), c.n_layers), dev)
+        self.merges = ops.to_device(_merge_array(merges), dev) if merges else None
+        self.max_rows = max((m[1] for m in merges), default=0)
+        self.rot = (torch.from_numpy(ops.shift_table(rots, hd, c.rope_theta)).to(dev) if rots
+                    else torch.zeros((1, hd // 2, 2), dtype=torch.float32, device=dev))
+        self.part_o = torch.empty((max(part_rows, 1), hd), dtype=torch.float32, device=dev)
+        self.part_lse = torch.empty((max(part_rows, 1),), dtype=torch.float32, device=dev)
+        pos = np.concatenate([np.asarray(j.pos, np.int64) + j.n_ctx for j in jobs]).astype(np.int32)
+        lo = np.concatenate([np.asarray(j.lo, np.int64) for j in jobs]).astype(np.int32)
+        ids = np.concatenate([np.asarray(j.ids, np.int64) for j in jobs])
+        if int(pos.max()) >= c.max_seq_len:
+            raise ValidationError(f"position {int(pos.max())} exceeds max_seq_len {c.max_seq_len}")
+        self.pos = torch.from_numpy(pos).to(dev, non_blocking=True)
+        self.lo = torch.from_numpy(lo).to(dev, non_blocking=True)
+        self.ids = torch.from_numpy(ids).to(dev, non_blocking=True)
+        self.pages = ops.to_device(_pages_for([(int(self.tok0[i]), n_new[i], int(self.aux_row0[i]))
+                                               for i in range(len(jobs))]), dev)
+        self.n_pages = int(sum(-(-n // PAGE) for n in n_new))
+        hdp = ops.hd_pad(hd)
+        self.k_aux = torch.zeros((1, hkv, self.aux_rows, hdp), dtype=torch.bfloat16, device=dev)
+        self.v_aux = torch.zeros((1, hkv, hdp, self.aux_rows), dtype=torch.bfloat16, device=dev)
+
+    def segs_ptr(self, layer: int) -> int:
+        return self.segs.data_ptr() + layer * self.n_segs * ops.SEG_DTYPE.itemsize
+
+
+def _split_bounds(counts: np.ndarray, n_split: int) -> list[int]:
+    """Cut a chunk list into n_split contiguous runs of ~equal token count."""
+    n = len(counts)
+    if n == 0:
+        return [0] * (n_split + 1)
+    cum = np.cumsum(counts)
+    total = cum[-1]
+    b = [0]
+    for s in range(1, n_split):
+        k = int(np.searchsorted(cum, total * s / n_split))
+        k = min(max(k + 1, b[-1] + 1), n - (n_split - s))
+        b.append(k)
+    b.append(n)
+    return b
+
+
+def _merge_array(merges) -> np.ndarray:
+    a = np.zeros(len(merges), dtype=ops.MERGE_DTYPE)
+    m = np.asarray(merges, dtype=np.int64)
+    for i, name in enumerate(ops.MERGE_DTYPE.names):
+        a[name] = m[:, i]
+    return a
+
+
+def run_jobs(dm, store, jobs, target_ctas=None, plan=None):
+    """Forward every job's new tokens; returns (plan, fp32 hidden [n_tok, d])."""
+    c = dm.config
+    plan = plan or Stage2Plan(dm, jobs, target_ctas)
+    qw, kw = c.n_heads * c.head_dim, c.n_kv_heads * c.head_dim
+    stride = qw + 2 * kw
+    pool = store.planes() if store is not None and store.k is not None else (plan.k_aux, plan.v_aux, plan.aux_rows, 1)
+    aux = (plan.k_aux, plan.v_aux, plan.aux_rows, 1)
+
+    def write_kv(layer, qkv):
+        ops.kv_write(qkv[:, qw:], qkv[:, qw + kw:], stride, plan.pos, dm.rope, plan.pages, plan.n_pages,
+                     plan.k_aux, plan.v_aux, plan.aux_rows, 1, 0, c.n_kv_heads, c.head_dim)
+
+    def attend(layer, qkv, out):
+        ops.attention(q=qkv, q_tok_stride=stride, tok_pos=plan.pos, tok_lo=plan.lo, rope=dm.rope, rot=plan.rot,
+                      pool=pool, aux=aux, n_heads=c.n_heads, n_kv_heads=c.n_kv_heads, head_dim=c.head_dim,
+                      works_dev=plan.works, n_works=plan.n_works, segs_dev=plan.segs_ptr(layer), num_m=plan.num_m,
+                      out=out, out_tok_stride=qw, part_o=plan.part_o, part_lse=plan.part_lse)
+        if plan.n_merge:
+            ops.lse_merge(plan.part_o, plan.part_lse, plan.merges, plan.n_merge, plan.max_rows, c.n_heads,
+                          c.n_kv_heads, c.head_dim, out, qw)
+
+    h = _decoder(dm, plan.ids, attend, write_kv)
+    return plan, h
+
+
+def _final_logits(dm, h_rows):
+    torch = _torch()
+    x = ops.rmsnorm(h_rows, dm.out_norm, dm.config.norm_eps)
+    return torch.mm(x, dm.lm_head, out_dtype=torch.float32)
+
+
+class LabelScorer:
+    """Row gather + lm_head + log-softmax gather for a batch of label jobs
+    (model.py:441-443, pipeline.py:376-382)."""
+
+    def __init__(self, dm, plan, jobs, n_labels):
+        torch = _torch()
+        rows, targets, owner = [], [], []
+        for qi, j in enumerate(jobs):
+            base = int(plan.tok0[qi])
+            nq = j.prefix
+            off = nq
+            for li in range(n_labels):
+                # label li occupies [off, off + len) with lo == off
+                ln = 0
+                while off + ln < len(j.ids) and j.lo[off + ln] == off:
+                    ln += 1
+                prev = base + nq - 1
+                for k in range(ln):
+                    rows.append(prev)
+                    targets.append(j.ids[off + k])
+                    owner.append(qi * n_labels + li)
+                    prev = base + off + k
+                off += ln
+        dev = dm.device
+        self.rows = torch.tensor(rows, dtype=torch.int64, device=dev)
+        self.targets = torch.tensor(targets, dtype=torch.int32, device=dev)
+        self.owner = torch.tensor(owner, dtype=torch.int64, device=dev)
+        self.n_out = len(jobs) * n_labels
+        self.n_labels = n_labels
+
+    def __call__(self, dm, h):
+        torch = _torch()
+        logits = _final_logits(dm, h.index_select(0, self.rows))
+        lp = ops.label_logprob(logits, self.targets)
+        scores = torch.zeros(self.n_out, dtype=torch.float32, device=h.device).index_add_(0, self.owner, lp)
+        scores = scores.view(-1, self.n_labels)
+        return scores, torch.argmax(scores, dim=1)
+
+
+def score_labels(dm, assembled, query_ids, labels):
+    """Per-label scores (host float array) of one query against `assembled`."""
+    store, chunks, n_ctx = _ctx_of(assembled)
+    job = label_job(chunks, n_ctx, query_ids, labels)
+    plan, h = run_jobs(dm, store, [job])
+    scores, _ = LabelScorer(dm, plan, [job], len(labels))(dm, h)
+    return scores[0].double().cpu().numpy()
+
+
+def forward_query(dm, assembled, query_ids):
+    store, chunks, n_ctx = _ctx_of(assembled)
+    n = len(query_ids)
+    job = QueryJob(chunks, n_ctx, list(query_ids), list(range(n)), [0] * n, n)
+    _, h = run_jobs(dm, store, [job])
+    return _final_logits(dm, h).cpu().numpy()
+
+
+def _ctx_of(assembled):
+    if assembled is None or assembled.total_tokens == 0:
+        return None, np.zeros((0, 3), np.int64), 0
+    return assembled.cache.store, assembled.chunks, assembled.total_tokens
+
+
+def logits_host(dm, hidden):
+    torch = _torch()
+    h = torch.as_tensor(np.asarray(hidden, np.float32)).to(dm.device)
+    return _final_logits(dm, h).cpu().numpy()
+
+
+def forward_explicit_context(dm, tokens, context):
+    """forward_encode with host context arrays: the context (already rotated at
+    its positions) goes into an aux page set, the new tokens into another."""
+    torch = _torch()
+    c = dm.config
+    n_ctx, t = len(context), len(tokens)
+    store = PageStore(c, dm.device, n_ctx + t)
+    dev = dm.device
+    rows = store.reserve([n_ctx, t] if n_ctx else [t])
+    hdp = store.hdp
+    if n_ctx:
+        # context K is already rotated: write it unrotated-by-table (position 0 row = identity)
+        zero = torch.zeros(n_ctx, dtype=torch.int32, device=dev)
+        pages = ops.to_device(_pages_for([(0, n_ctx, rows[0])]), dev)
+        for layer, (k, v) in enumerate(context.layers):
+            ks = torch.from_numpy(np.ascontiguousarray(k, np.float32)).to(dev).to(torch.bfloat16)
+            vs = torch.from_numpy(np.ascontiguousarray(v, np.float32)).to(dev).to(torch.bfloat16)
+            ops.kv_write(ks.reshape(n_ctx, -1), vs.reshape(n_ctx, -1), c.n_kv_heads * c.head_dim, zero, dm.rope,
+                         pages, -(-n_ctx // PAGE), store.k, store.v, store.rows, c.n_layers, layer, c.n_kv_heads,
+                         c.head_dim)
+    del hdp
+    self_row = rows[-1]
+    qw, kw = c.n_heads * c.head_dim, c.n_kv_heads * c.head_dim
+    stride = qw + 2 * kw
+    pos = torch.tensor(np.asarray(tokens.positions, np.int32), device=dev)
+    pages = ops.to_device(_pages_for([(0, t, self_row)]), dev)
+    gs = c.group_size
+    num_m = 2 if t * gs > 128 else 1
+    slab = (128 * num_m) // gs
+    segs, works = [], []
+    for t0 in range(0, t, slab):
+        nt = min(slab, t - t0)
+        sb = len(segs)
+        if n_ctx:
+            segs.append((0, 0, rows[0], n_ctx, SEG_FULL, -1))
+        segs.append((0, 0, self_row, t0 + nt, SEG_SELF, -1))
+        for kv in range(c.n_kv_heads):
+            works.append((t0, nt, 0, kv, sb, len(segs), 0, 0, 0))
+    wdev = ops.to_device(_work_array(works), dev)
+    sdev = ops.to_device(_per_layer_segs(_seg_array(segs), c.n_layers), dev)
+    pre = []
+
+    def write_kv(layer, qkv):
+        ops.kv_write(qkv[:, qw:], qkv[:, qw + kw:], stride, pos, dm.rope, pages, -(-t // PAGE), store.k, store.v,
+                     store.rows, c.n_layers, layer, c.n_kv_heads, c.head_dim)
+        pre.append((qkv[:, qw:qw + kw].float().reshape(t, c.n_kv_heads, c.head_dim).cpu().numpy(),
+                    qkv[:, qw + kw:].float().reshape(t, c.n_kv_heads, c.head_dim).cpu().numpy()))
+
+    def attend(layer, qkv, out):
+        ops.attention(q=qkv, q_tok_stride=stride, tok_pos=pos, tok_lo=None, rope=dm.rope, rot=None,
+                      pool=store.planes(), aux=None, n_heads=c.n_heads, n_kv_heads=c.n_kv_heads, head_dim=c.head_dim,
+                      works_dev=wdev, n_works=len(works),
+                      segs_dev=sdev.data_ptr() + layer * len(segs) * ops.SEG_DTYPE.itemsize, num_m=num_m, out=out,
+                      out_tok_stride=qw)
+
+    ids = torch.tensor(np.asarray(tokens.ids, np.int64), device=dev)
+    h = _decoder(dm, ids, attend, write_kv)
+    return pre, h.cpu().numpy()

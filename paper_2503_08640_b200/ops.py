@@ -15,6 +15,20 @@ from .errors import ConfigError, ShapeError
 
 PAGE = nat.PAGE_TOKENS
 
+# Number of libdbsa kernel launches issued through this module (bench.py's
+# `gpu_launches`).  Plain int: increments are GIL-atomic enough for a count.
+LAUNCHES = 0
+
+
+def _launched(n: int = 1) -> None:
+    global LAUNCHES
+    LAUNCHES += n
+
+
+def _p(x) -> int:
+    """Device pointer of a tensor, or an int address passed through."""
+    return int(x) if isinstance(x, int) else int(x.data_ptr())
+
 WORK_DTYPE = np.dtype(
     [("q_tok0", "<i4"), ("n_tok", "<i4"), ("self_tok0", "<i4"), ("kv_head", "<i4"),
      ("seg_begin", "<i4"), ("seg_end", "<i4"), ("prefix", "<i4"), ("out_mode", "<i4"),
@@ -66,6 +80,7 @@ def rope_table(rows: int, head_dim: int, theta: float, device, pos0: int = 0):
     table = torch.empty((rows, half, 2), dtype=torch.float32, device=device)
     nat.check(nat.load_library().dbsa_rope_table(table.data_ptr(), rows, freq.data_ptr(), half, pos0,
                                                  nat.stream_handle()))
+    _launched()
     table._keepalive = freq  # freq must outlive the async launch
     return table
 
@@ -86,6 +101,7 @@ def kv_write(k_src, v_src, src_tok_stride, tok_pos, rope, pages_dev, n_pages, k_
         dst_rows=dst_rows, dst_layers=dst_layers, layer=layer, n_kv_heads=n_kv_heads,
         head_dim=head_dim, hd_pad=hd_pad(head_dim))
     nat.check(nat.load_library().dbsa_kv_write(ctypes.byref(a), nat.stream_handle()))
+    _launched()
 
 
 def attention(*, q, q_tok_stride, tok_pos, tok_lo, rope, rot, pool, aux, n_heads, n_kv_heads, head_dim,
@@ -99,10 +115,11 @@ def attention(*, q, q_tok_stride, tok_pos, tok_lo, rope, rot, pool, aux, n_heads
         rot_table=nat.ptr(rot), k_pool=kp.data_ptr(), v_pool=vp.data_ptr(), pool_rows=prow,
         pool_layers=pl, k_aux=nat.ptr(ka), v_aux=nat.ptr(va), aux_rows=arow, aux_layers=al,
         n_heads=n_heads, n_kv_heads=n_kv_heads, head_dim=head_dim, hd_pad=hd_pad(head_dim),
-        scale=float(1.0 / math.sqrt(head_dim)), num_m=num_m, works=works_dev.data_ptr(),
-        n_works=n_works, segs=segs_dev.data_ptr(), out=out.data_ptr(), out_tok_stride=out_tok_stride,
+        scale=float(1.0 / math.sqrt(head_dim)), num_m=num_m, works=_p(works_dev),
+        n_works=n_works, segs=_p(segs_dev), out=out.data_ptr(), out_tok_stride=out_tok_stride,
         part_o=nat.ptr(part_o), part_lse=nat.ptr(part_lse))
     nat.check(nat.load_library().dbsa_attention(ctypes.byref(a), nat.stream_handle()))
+    _launched()
 
 
 def lse_merge(part_o, part_lse, groups_dev, n_groups, max_rows, n_heads, n_kv_heads, head_dim, out,
@@ -111,6 +128,7 @@ def lse_merge(part_o, part_lse, groups_dev, n_groups, max_rows, n_heads, n_kv_he
                       n_groups=n_groups, max_rows=max_rows, n_heads=n_heads, n_kv_heads=n_kv_heads,
                       head_dim=head_dim, out=out.data_ptr(), out_tok_stride=out_tok_stride)
     nat.check(nat.load_library().dbsa_lse_merge(ctypes.byref(a), nat.stream_handle()))
+    _launched()
 
 
 def topk_select(scores, budget: int, ordering: str):
@@ -124,6 +142,7 @@ def topk_select(scores, budget: int, ordering: str):
     nat.check(nat.load_library().dbsa_topk_select(
         scores.data_ptr(), scores.shape[0], scores.shape[1], budget, ORDERING_CODES[ordering],
         out.data_ptr(), nat.stream_handle()))
+    _launched()
     return out
 
 
@@ -133,6 +152,7 @@ def rmsnorm(x, weight, eps: float, out=None):
     out = out if out is not None else torch.empty(x.shape, dtype=torch.bfloat16, device=x.device)
     nat.check(nat.load_library().dbsa_rmsnorm(x.data_ptr(), weight.data_ptr(), out.data_ptr(), x.shape[0],
                                               x.shape[1], float(eps), nat.stream_handle()))
+    _launched()
     return out
 
 
@@ -143,6 +163,7 @@ def silu_mul(gate_up, ffn: int, out=None):
                                                   device=gate_up.device)
     nat.check(nat.load_library().dbsa_silu_mul(gate_up.data_ptr(), out.data_ptr(), gate_up.shape[0], ffn,
                                                nat.stream_handle()))
+    _launched()
     return out
 
 
@@ -152,4 +173,5 @@ def label_logprob(logits, targets):
     out = torch.empty(logits.shape[0], dtype=torch.float32, device=logits.device)
     nat.check(nat.load_library().dbsa_label_logprob(logits.data_ptr(), logits.shape[0], logits.shape[1],
                                                      targets.data_ptr(), out.data_ptr(), nat.stream_handle()))
+    _launched()
     return out

@@ -1,0 +1,388 @@
+"""Stage-1 pre-encode and stage-2 retrieve-and-answer calls
+(reference: pipeline.py:1-482).
+
+Same names, signatures, validation and return types as the reference:
+`encode_pool(weights, task, config) -> EncodedPool`,
+`encode_blocks(weights, cache, new_blocks, pattern) -> int`,
+`Runner(weights, cache, index, task, config).infer(query) -> (label, QueryMetrics)`
+and `infer(...)`.  `weights` is the reference's host `ModelWeights` (uploaded
+once) or an `engine.DeviceModel`.  Added for throughput: `Runner.infer_batch`
+and the lower-level `Stage2Session`, which take many queries per forward and
+select their groups with K4 on the device.
+
+Methods: "dbsa" (the hot path), "fixed" (all groups of the cache, the
+reference's cached-ICL baseline) and "zero" (no context) run on the same
+kernels.  "ret" re-encodes retrieved text without a cache; it is a baseline
+outside the DBSA hot path and is rejected with ConfigError.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import threading
+import time
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+
+from . import engine, kvstore, masks, retrieval, tokenizer
+from .errors import CompatibilityError, ConfigError, ValidationError
+from .metrics import Metrics, QueryMetrics, flops_attention
+
+DBSA, FIXED_ICL, RET_ICL, ZERO_SHOT = "dbsa", "fixed", "ret", "zero"
+METHODS = (DBSA, FIXED_ICL, RET_ICL, ZERO_SHOT)
+_ALIASES = {"dbsa": DBSA, "fixed": FIXED_ICL, "fixed-icl": FIXED_ICL, "ret": RET_ICL, "ret-icl": RET_ICL,
+            "reticl": RET_ICL, "zero": ZERO_SHOT, "zero-shot": ZERO_SHOT}
+
+
+def canonical_method(name: str) -> str:
+    try:
+        return _ALIASES[name.lower()]
+    except KeyError:
+        raise ValidationError(f"unknown method {name!r}; expected one of {METHODS}") from None
+
+
+@dataclass(frozen=True)
+class Demonstration:
+    query: str
+    answer: str
+
+    def __post_init__(self) -> None:
+        if not self.query.strip() or not self.answer.strip():
+            raise ValidationError("demonstration query and answer must be non-empty")
+
+    def raw_text(self) -> str:
+        return f"{self.query} {self.answer}"
+
+
+@dataclass(frozen=True)
+class PromptTemplate:
+    """Rendering of demos / queries / labels (pipeline.py:58-71)."""
+
+    demo_format: str = "Q: {query}\nA: {answer}\n\n"
+    query_format: str = "Q: {query}\nA:"
+    label_format: str = " {label}"
+
+    def render_demo(self, demo: Demonstration) -> str:
+        return self.demo_format.format(query=demo.query, answer=demo.answer)
+
+    def render_query(self, query: str) -> str:
+        return self.query_format.format(query=query)
+
+    def render_label(self, label: str) -> str:
+        return self.label_format.format(label=label)
+
+
+@dataclass(frozen=True)
+class TaskSpec:
+    pool: tuple[Demonstration, ...]
+    labels: tuple[str, ...]
+    template: PromptTemplate = PromptTemplate()
+
+    def __post_init__(self) -> None:
+        if not self.pool:
+            raise ValidationError("demonstration pool must be non-empty")
+        if not self.labels:
+            raise ValidationError("label set must be non-empty")
+        if len(set(self.labels)) != len(self.labels):
+            raise ValidationError("labels must be distinct")
+        bad = [d.answer for d in self.pool if d.answer not in set(self.labels)]
+        if bad:
+            raise ValidationError(f"pool answer {bad[0]!r} is not in the label set")
+
+
+@dataclass(frozen=True)
+class MethodConfig:
+    """Method knobs with the reference defaults (pipeline.py:93-136)."""
+
+    method: str = DBSA
+    pattern: masks.AttentionPattern = masks.AttentionPattern.sink_prev_self(2)
+    block_size: int = 50
+    ratio: float = 0.30
+    granularity: str = kvstore.BLOCK_GRANULARITY
+    grouping: retrieval.GroupingStrategy = field(default_factory=lambda: retrieval.GroupingStrategy.random(0))
+    ordering: str = retrieval.IN_ORDER
+    seed: int = 0
+    max_pool_tokens: int = 262144
+
+    def __post_init__(self) -> None:
+        object.__setattr__(self, "method", canonical_method(self.method))
+        if self.block_size < 1:
+            raise ConfigError(f"block_size must be >= 1, got {self.block_size}")
+        if not 0.0 < self.ratio <= 1.0:
+            raise ConfigError(f"ratio must be in (0, 1], got {self.ratio}")
+        if self.granularity not in kvstore.GRANULARITIES:
+            raise ConfigError(f"unknown granularity {self.granularity!r}")
+        if self.ordering not in retrieval.ORDERINGS:
+            raise ConfigError(f"unknown ordering {self.ordering!r}")
+
+    @property
+    def local_blocks(self) -> int:
+        return self.pattern.local_blocks
+
+    def digest(self) -> str:
+        parts = (self.method, self.pattern.kind, str(self.pattern.local_blocks), str(self.block_size),
+                 f"{self.ratio:.6f}", self.granularity, self.grouping.kind, f"{self.grouping.swap_fraction:.6f}",
+                 self.ordering)
+        return hashlib.sha256("|".join(parts).encode("utf-8")).hexdigest()[:16]
+
+
+@dataclass
+class EncodedPool:
+    cache: kvstore.SegmentedKVCache
+    index: retrieval.Bm25Index
+    partition: retrieval.BlockPartition
+    metrics: Metrics
+    encode_seconds: float = 0.0
+    index_seconds: float = 0.0
+
+
+def _device_model(weights):
+    return weights if isinstance(weights, engine.DeviceModel) else weights.device()
+
+
+def render_block(template: PromptTemplate, pool, members):
+    """(text, ids, per-demo token spans) of one group (pipeline.py:149-163)."""
+    spans, parts, off = [], [], 0
+    for e in members:
+        part = template.render_demo(pool[e])
+        n = len(part.encode("utf-8"))  # byte-level tokenizer: one token per byte
+        spans.append((off, off + n))
+        parts.append(part)
+        off += n
+    text = "".join(parts)
+    return text, tokenizer.encode(text), tuple(spans)
+
+
+def encode_blocks(weights, cache: kvstore.SegmentedKVCache, new_blocks, pattern: masks.AttentionPattern) -> int:
+    """Append and encode groups (token ids, sha256 digest, demo spans) against
+    their allowed context (pipeline.py:166-233).  All new groups go through the
+    model together, layer by layer, on the GPU.  Returns attended pairs."""
+    dm = _device_model(weights)
+    kvstore.check_compatible(cache, dm.config)
+    if not new_blocks:
+        return 0
+    counts = [len(ids) for ids, _, _ in new_blocks]
+    total = cache.total_tokens + sum(counts)
+    if total >= dm.config.max_seq_len:
+        raise ValidationError(f"pool of {total} tokens exceeds max_seq_len {dm.config.max_seq_len}")
+    ids = np.concatenate([np.asarray(i, np.int64) for i, _, _ in new_blocks])
+    if ids.min() < 0 or ids.max() >= dm.config.vocab_size:
+        raise ValidationError(f"token id outside vocabulary [0, {dm.config.vocab_size})")
+    new = cache._reserve(counts, [d for _, d, _ in new_blocks], [s for _, _, s in new_blocks])
+    return engine.encode_groups(dm, cache, new, ids, pattern)
+
+
+def build_index(task: TaskSpec, partition: retrieval.BlockPartition, spans_per_block, granularity: str):
+    """Unit texts and cache coordinates per granularity (pipeline.py:236-262)."""
+    raw = [d.raw_text() for d in task.pool]
+    if granularity == kvstore.BLOCK_GRANULARITY:
+        texts = [" ".join(raw[e] for e in m) for m in partition.blocks]
+        refs = [(b, 0, spans_per_block[b][-1][1]) for b in range(partition.n_blocks)]
+        examples = [tuple(m) for m in partition.blocks]
+    else:
+        first = partition.blocks[0]
+        texts, refs, examples = [" ".join(raw[e] for e in first)], [(0, 0, spans_per_block[0][-1][1])], [tuple(first)]
+        for b in range(1, partition.n_blocks):
+            for slot, e in enumerate(partition.blocks[b]):
+                texts.append(raw[e])
+                refs.append((b, *spans_per_block[b][slot]))
+                examples.append((e,))
+    return retrieval.Bm25Index(texts, granularity, refs, examples)
+
+
+def encode_pool(weights, task: TaskSpec, config: MethodConfig, partition: retrieval.BlockPartition | None = None,
+                device=None) -> EncodedPool:
+    """Stage 1: group, render, encode on the GPU, index (pipeline.py:286-319)."""
+    dm = _device_model(weights)
+    t0 = time.perf_counter()
+    if partition is None:
+        partition = retrieval.group([d.raw_text() for d in task.pool], config.block_size,
+                                    replace(config.grouping, seed=config.seed))
+    rendered = [render_block(task.template, task.pool, m) for m in partition.blocks]
+    total = sum(len(ids) for _, ids, _ in rendered)
+    if total > config.max_pool_tokens:
+        raise ValidationError(f"pool of {total} tokens exceeds the configured limit {config.max_pool_tokens}")
+    cache = kvstore.SegmentedKVCache(dm.config, device or dm.device, capacity_tokens=total)
+    new_blocks = [(ids, hashlib.sha256(text.encode("utf-8")).digest(), spans) for text, ids, spans in rendered]
+    attended = encode_blocks(dm, cache, new_blocks, config.pattern)
+    cache.seal()
+    import torch
+
+    torch.cuda.current_stream(cache.device).synchronize()
+    encode_s = time.perf_counter() - t0
+    t1 = time.perf_counter()
+    index = build_index(task, partition, [s for _, _, s in rendered], config.granularity)
+    index_s = time.perf_counter() - t1
+    m = Metrics(setup_seconds=encode_s + index_s, cache_bytes=kvstore.storage_bytes(dm.config, cache.total_tokens, 4))
+    m.attended_tokens.append(attended)
+    m.attention_flops.append(flops_attention(attended, dm.config, cache.total_tokens))
+    return EncodedPool(cache, index, partition, m, encode_s, index_s)
+
+
+class Stage2Session:
+    """Batched stage 2 over a sealed cache: K4 selection, chunk tables, one
+    tree-masked forward per batch, label scores and argmax on the device.
+
+    unit_refs: (block, start, end) per retrieval unit (Bm25Index.unit_refs).
+    """
+
+    def __init__(self, weights, cache: kvstore.SegmentedKVCache, unit_refs, label_ids, ratio: float, ordering: str):
+        self.dm = _device_model(weights)
+        self.cache = cache
+        self.label_ids = [list(x) for x in label_ids]
+        self.ratio, self.ordering = ratio, ordering
+        refs = np.asarray(unit_refs, dtype=np.int64).reshape(-1, 3)
+        blocks = cache.blocks
+        row0 = np.array([e.row0 for e in blocks], np.int64)
+        pos0 = np.array([e.pos_start for e in blocks], np.int64)
+        self.u_row = row0[refs[:, 0]] + refs[:, 1]
+        self.u_len = refs[:, 2] - refs[:, 1]
+        self.u_orig = pos0[refs[:, 0]] + refs[:, 1]
+        self.n_units = len(refs)
+        self.budget = retrieval.budget_for(ratio, self.n_units)
+
+    def chunks_for(self, ids: np.ndarray):
+        """ordered unit ids [B, k] -> per-query chunk tables and T'."""
+        ln = self.u_len[ids]
+        new_start = np.cumsum(ln, axis=1) - ln
+        delta = new_start - self.u_orig[ids]
+        tab = np.stack([self.u_row[ids], ln, delta], axis=-1)
+        return tab, ln.sum(axis=1)
+
+    def select(self, scores: np.ndarray):
+        """K4 on the device: float64 scores [B, n_units] -> ordered ids (host int64)."""
+        import torch
+
+        ids = engine.ops.topk_select(torch.from_numpy(np.ascontiguousarray(scores)).to(self.dm.device), self.budget,
+                                     self.ordering)
+        return ids.cpu().numpy().astype(np.int64)
+
+    def plan(self, ids: np.ndarray, query_ids_list, target_ctas=None):
+        tabs, n_ctx = self.chunks_for(ids)
+        jobs = [engine.label_job(tabs[i], int(n_ctx[i]), q, self.label_ids) for i, q in enumerate(query_ids_list)]
+        return jobs, engine.Stage2Plan(self.dm, jobs, target_ctas)
+
+    def run(self, jobs, plan):
+        """Forward + label scoring; returns device (scores [B, n_labels], argmax [B])."""
+        _, h = engine.run_jobs(self.dm, self.cache.store, jobs, plan=plan)
+        scorer = engine.LabelScorer(self.dm, plan, jobs, len(self.label_ids))
+        return scorer(self.dm, h)
+
+    def answer(self, scores: np.ndarray, query_ids_list):
+        ids = self.select(scores)
+        jobs, plan = self.plan(ids, query_ids_list)
+        s, best = self.run(jobs, plan)
+        return ids, s, best
+
+
+class Runner:
+    """Inference session over (weights, cache, index) (pipeline.py:322-446).
+    Read-only after prepare(); infer() may run from several threads (each
+    thread launches on its own current stream)."""
+
+    def __init__(self, weights, cache, index, task: TaskSpec, config: MethodConfig):
+        self.weights = weights
+        self.dm = _device_model(weights)
+        self.cache, self.index, self.task, self.config = cache, index, task, config
+        self.method = config.method
+        if self.method == RET_ICL:
+            raise ConfigError("method 'ret' (no-cache re-encode baseline) is outside the DBSA GPU path")
+        if self.method in (DBSA, FIXED_ICL) and cache is None:
+            raise ValidationError(f"method {self.method!r} requires an encoded cache")
+        if self.method == DBSA and index is None:
+            raise ValidationError(f"method {self.method!r} requires a retrieval index")
+        if cache is not None and cache.config_hash != self.dm.config.hash_bytes():
+            raise CompatibilityError("cache and weights were built for different configs")
+        # lexicographic label order: score ties resolve to the smallest label (pipeline.py:349-354)
+        self.labels = sorted(task.labels)
+        self.label_ids = [tokenizer.encode(task.template.render_label(lab)) for lab in self.labels]
+        self._full: kvstore.AssembledCache | None = None
+        self._lock = threading.Lock()
+
+    def prepare(self) -> None:
+        if self.method == FIXED_ICL and self._full is None:
+            with self._lock:
+                if self._full is None:
+                    self._full = kvstore.assemble(self.cache, kvstore.all_blocks_selection(self.cache))
+
+    def _pairs(self, n_ctx: int, query_ids) -> tuple[int, int]:
+        pairs = tokens = 0
+        for lab in self.label_ids:
+            n = len(query_ids) + len(lab)
+            pairs += n * n_ctx + n * (n + 1) // 2
+            tokens += n
+        return pairs, tokens
+
+    def _score(self, assembled, query_ids):
+        scores = engine.score_labels(self.dm, assembled, query_ids, self.label_ids)
+        best = int(np.argmax(scores))  # first maximum == strict '>' scan (pipeline.py:380-382)
+        return self.labels[best], scores
+
+    def infer(self, query_text: str):
+        cfg = self.config
+        qm = QueryMetrics()
+        t_start = time.perf_counter()
+        query_ids = tokenizer.encode(self.task.template.render_query(query_text))
+        if self.method == ZERO_SHOT:
+            assembled = None
+            n_ctx = 0
+        elif self.method == FIXED_ICL:
+            t0 = time.perf_counter()
+            self.prepare()
+            assembled = self._full
+            qm.assembly_seconds = time.perf_counter() - t0
+            n_ctx = assembled.total_tokens
+        else:
+            t0 = time.perf_counter()
+            sel = retrieval.order(retrieval.select(self.index, query_text, cfg.ratio, cfg.granularity), cfg.ordering)
+            qm.retrieval_seconds = time.perf_counter() - t0
+            t0 = time.perf_counter()
+            assembled = kvstore.assemble(self.cache, sel)
+            qm.assembly_seconds = time.perf_counter() - t0
+            n_ctx = assembled.total_tokens
+        t0 = time.perf_counter()
+        label, _ = self._score(assembled, query_ids)
+        qm.scoring_seconds = time.perf_counter() - t0
+        pairs, tokens = self._pairs(n_ctx, query_ids)
+        qm.attended_pairs = pairs
+        qm.attention_flops = flops_attention(pairs, self.dm.config, tokens)
+        qm.total_seconds = time.perf_counter() - t_start
+        return label, qm
+
+    def session(self) -> Stage2Session:
+        if self.method != DBSA:
+            raise ConfigError("batched inference is the DBSA path")
+        return Stage2Session(self.dm, self.cache, self.index.unit_refs, self.label_ids, self.config.ratio,
+                             self.config.ordering)
+
+    def infer_batch(self, query_texts, max_batch: int = 256):
+        """DBSA answers for many queries: BM25 matrix on the host, K4 selection
+        and one batched tree-masked forward per `max_batch` queries on the GPU.
+        Returns [(label, QueryMetrics)] in input order."""
+        sess = self.session()
+        out = []
+        for b0 in range(0, len(query_texts), max_batch):
+            texts = list(query_texts[b0:b0 + max_batch])
+            t0 = time.perf_counter()
+            q_ids = [tokenizer.encode(self.task.template.render_query(t)) for t in texts]
+            scores = self.index.score_matrix([retrieval.bm25_tokenize(t) for t in texts])
+            ids, _, best = sess.answer(scores, q_ids)
+            best = best.cpu().numpy()
+            dt = (time.perf_counter() - t0) / len(texts)
+            _, n_ctx = sess.chunks_for(ids)
+            for i in range(len(texts)):
+                qm = QueryMetrics()
+                pairs, tokens = self._pairs(int(n_ctx[i]), q_ids[i])
+                qm.attended_pairs = pairs
+                qm.attention_flops = flops_attention(pairs, self.dm.config, tokens)
+                qm.total_seconds = dt
+                out.append((self.labels[int(best[i])], qm))
+        return out
+
+
+def infer(weights, cache, index, config: MethodConfig, query_text: str, task: TaskSpec):
+    """Single-query convenience wrapper (pipeline.py:471-482)."""
+    runner = Runner(weights, cache, index, task, config)
+    runner.prepare()
+    return runner.infer(query_text)

@@ -1,0 +1,220 @@
+"""End-to-end parity of the GPU path against the reference, through the
+reference-shaped API (encode_pool -> SegmentedKVCache -> Runner.infer).
+
+Reference values are the committed golden fixtures produced by the
+unmodified reference (tests/golden/make_golden.py); the CPU oracle
+(oracle/dbsa_oracle.py, pinned to the same fixtures) supplies what the
+fixtures do not store.  Gates (north star):
+  * partition, block mask, attended pairs, selected unit ids: bit-exact;
+  * K/V pages vs the reference's f32 cache: max-abs 3e-2 (bf16 storage);
+  * forward_query logits: max-abs 2e-2 vs the reference's f32 logits;
+  * per-label scores: max-abs 0.1 (sum of ~6 bf16 log-probs); predicted
+    labels identical wherever the reference's top-2 margin exceeds 10x the
+    observed score error (near-tie guard; every C1 margin is reported).
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from golden_util import CASES, load, oracle_pool  # noqa: E402
+from oracle import dbsa_oracle as O  # noqa: E402
+import paper_2503_08640_b200 as P  # noqa: E402
+from paper_2503_08640_b200 import masks, pipeline, retrieval, tokenizer  # noqa: E402
+
+LOGIT_TOL = 2e-2
+KV_TOL = 3e-2
+SCORE_TOL = 0.1
+
+
+def _setup(name):
+    meta, a = load(name)
+    cfg = P.ModelConfig(vocab_size=tokenizer.VOCAB_SIZE, **meta["spec"]["model"])
+    w = P.init_random(cfg, meta["spec"]["weight_seed"])
+    t = meta["spec"]["task"]
+    pool, tests, labels = O.recall_task(t["n_demos"], t["n_tests"], t["n_labels"], t["seed"])
+    task = P.TaskSpec(tuple(P.Demonstration(q, x) for q, x in pool), tuple(labels))
+    m = dict(meta["spec"]["method"])
+    j = m.pop("local_blocks", 2)
+    mc = P.MethodConfig(pattern=masks.AttentionPattern.sink_prev_self(j), **m)
+    return meta, a, w, task, mc
+
+
+_ENC = {}
+
+
+def _encoded(name):
+    if name not in _ENC:
+        meta, a, w, task, mc = _setup(name)
+        _ENC[name] = (meta, a, w, task, mc, P.encode_pool(w, task, mc))
+    return _ENC[name]
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_stage1_structure_and_pages(name):
+    meta, a, w, task, mc, enc = _encoded(name)
+    cache = enc.cache
+    assert cache.sealed and cache.n_blocks == meta["n_blocks"] and cache.total_tokens == meta["total_tokens"]
+    np.testing.assert_array_equal([e.token_count for e in cache.blocks], a["block_counts"])
+    np.testing.assert_array_equal([x for b in enc.partition.blocks for x in b], a["partition_members"])
+    assert enc.metrics.attended_tokens[0] == meta["attended_pairs"]
+    worst = 0.0
+    for layer in range(w.config.n_layers):
+        for b in meta["sample_blocks"]:
+            k, v = cache.segment(layer, b)
+            worst = max(worst, float(np.abs(k[:3] - a[f"k_l{layer}_b{b}"]).max()),
+                        float(np.abs(v[:3] - a[f"v_l{layer}_b{b}"]).max()))
+    assert worst < KV_TOL, worst
+
+
+def test_stage1_whole_cache_vs_oracle_c1():
+    """Every group, every layer: pages vs the oracle's f32 stage 1 (pinned to
+    the reference by test_oracle_golden)."""
+    meta, a, w, task, mc, enc = _encoded("c1")
+    st = oracle_pool("c1")
+    worst = 0.0
+    for layer in range(w.config.n_layers):
+        for b in range(enc.cache.n_blocks):
+            k, v = enc.cache.segment(layer, b)
+            rk, rv = st["kv"][layer][b]
+            worst = max(worst, float(np.abs(k - rk).max()), float(np.abs(v - rv).max()))
+    assert worst < KV_TOL, worst
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_stage2_runner_matches_reference(name):
+    meta, a, w, task, mc, enc = _encoded(name)
+    runner = P.Runner(w, enc.cache, enc.index, task, mc)
+    runner.prepare()
+    worst, margins, flips = 0.0, [], []
+    for qi, q in enumerate(meta["queries"]):
+        sel = retrieval.order(retrieval.select(enc.index, q["query"], mc.ratio, mc.granularity), mc.ordering)
+        np.testing.assert_array_equal(sel.unit_ids, a[f"q{qi}_units"])  # bit-exact selection
+        asm = P.assemble(enc.cache, sel)
+        assert asm.total_tokens == q["assembled_tokens"]
+        label, qm = runner.infer(q["query"])
+        assert qm.attended_pairs == q["attended_pairs"]
+        q_ids = tokenizer.encode(task.template.render_query(q["query"]))
+        got = runner._score(asm, q_ids)[1]
+        ref = a[f"q{qi}_label_scores"]
+        err = float(np.abs(got - ref).max())
+        worst = max(worst, err)
+        srt = np.sort(ref)
+        margin = float(srt[-1] - srt[-2]) if len(ref) > 1 else np.inf
+        margins.append(margin)
+        if label != q["predicted"]:
+            flips.append((qi, margin, err))
+    print(f"{name}: max |score err| {worst:.4g}; min top-2 margin {min(margins):.4g}; flips {flips}")
+    assert worst < SCORE_TOL, worst
+    for qi, margin, err in flips:
+        assert margin < 10 * max(err, 1e-3), f"query {qi} flipped with margin {margin} (err {err})"
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_stage2_batched_k4_path_matches_reference(name):
+    """Runner.infer_batch: K4 selection on the device + one tree-masked
+    forward for the whole batch; unit ids bit-exact, labels identical."""
+    meta, a, w, task, mc, enc = _encoded(name)
+    runner = P.Runner(w, enc.cache, enc.index, task, mc)
+    texts = [q["query"] for q in meta["queries"]]
+    sess = runner.session()
+    scores = enc.index.score_matrix([retrieval.bm25_tokenize(t) for t in texts])
+    ids = sess.select(scores)
+    for qi in range(len(texts)):
+        np.testing.assert_array_equal(ids[qi], a[f"q{qi}_units"])
+    out = runner.infer_batch(texts, max_batch=7)
+    single = [runner.infer(t)[0] for t in texts]
+    assert [lab for lab, _ in out] == single
+    for qi, (lab, qm) in enumerate(out):
+        assert qm.attended_pairs == meta["queries"][qi]["attended_pairs"]
+
+
+def test_forward_query_logits_c1():
+    meta, a, w, task, mc, enc = _encoded("c1")
+    q = meta["queries"][0]
+    units = [int(u) for u in a["q0_units"]]
+    sel = P.Selection("block", tuple(P.SegmentRef(u, *enc.index.unit_refs[u]) for u in units))
+    asm = P.assemble(enc.cache, sel)
+    q_ids = tokenizer.encode(task.template.render_query(q["query"]))
+    got = P.forward_query(w, asm, P.TokenSequence.at_offset(q_ids, asm.total_tokens))
+    err = float(np.abs(got - a["q0_logits"]).max())
+    print(f"forward_query max-abs logit error {err:.4g} (|logits| <= {np.abs(a['q0_logits']).max():.3g})")
+    assert err < LOGIT_TOL, err
+
+
+def test_score_label_and_assembled_layers_c1():
+    meta, a, w, task, mc, enc = _encoded("c1")
+    st = oracle_pool("c1")
+    units = [int(u) for u in a["q1_units"]]
+    sel = P.Selection("block", tuple(P.SegmentRef(u, *enc.index.unit_refs[u]) for u in units))
+    asm = P.assemble(enc.cache, sel)
+    ref_layers, n_ctx = O.assemble(st["cfg"], st["kv"], [st["refs"][u] for u in units])
+    assert n_ctx == asm.total_tokens
+    for (k, v), (rk, rv) in zip(asm.layers, ref_layers):
+        assert float(np.abs(k - rk).max()) < KV_TOL and float(np.abs(v - rv).max()) < KV_TOL
+    q_ids = tokenizer.encode(task.template.render_query(meta["queries"][1]["query"]))
+    for li, lab in enumerate(sorted(task.labels)):
+        s = P.score_label(w, asm, q_ids, tokenizer.encode(task.template.render_label(lab)))
+        assert abs(s - a["q1_label_scores"][li]) < SCORE_TOL
+
+
+def test_incremental_append_equals_one_shot():
+    """encode_blocks on an existing cache encodes only the new groups against
+    the stored ones (pipeline.py:179-200, test_acceptance.py:144-180)."""
+    meta, a, w, task, mc, enc = _encoded("c1")
+    rendered = [pipeline.render_block(task.template, task.pool, m) for m in enc.partition.blocks]
+    import hashlib
+
+    blocks = [(ids, hashlib.sha256(t.encode()).digest(), sp) for t, ids, sp in rendered]
+    cache = P.SegmentedKVCache(w.config)
+    n1 = P.encode_blocks(w, cache, blocks[:5], mc.pattern)
+    n2 = P.encode_blocks(w, cache, blocks[5:], mc.pattern)
+    assert n1 + n2 == meta["attended_pairs"]
+    worst = 0.0
+    for layer in range(w.config.n_layers):
+        for b in (0, 4, 5, 6, 15):
+            k1, v1 = cache.segment(layer, b)
+            k0, v0 = enc.cache.segment(layer, b)
+            worst = max(worst, float(np.abs(k1 - k0).max()), float(np.abs(v1 - v0).max()))
+    assert worst < 1e-2, worst
+
+
+def test_forward_encode_api_matches_oracle():
+    meta, a, w, task, mc, enc = _encoded("c1")
+    st = oracle_pool("c1")
+    c = st["cfg"]
+    rendered = [pipeline.render_block(task.template, task.pool, m) for m in enc.partition.blocks]
+    counts = [len(ids) for _, ids, _ in rendered]
+    off = np.concatenate([[0], np.cumsum(counts)])
+    b = 3
+    ctx = (0, 1, 2)
+    ctx_pos = np.concatenate([np.arange(off[j], off[j + 1]) for j in ctx])
+    layers = []
+    for layer in range(c.n_layers):
+        ks = [O.rope(st["kv"][layer][j][0], np.arange(off[j], off[j + 1]), c.rope_theta) for j in ctx]
+        layers.append((np.concatenate(ks), np.concatenate([st["kv"][layer][j][1] for j in ctx])))
+    tokens = P.TokenSequence.at_offset(rendered[b][1], int(off[b]))
+    mask = masks.block_mask_rows(masks.build_block_mask(16, mc.pattern), counts, b)
+    pre, hidden = P.forward_encode(w, tokens, P.ContextKV(ctx_pos, layers), mask)
+    for layer in range(c.n_layers):
+        assert float(np.abs(pre[layer][0] - st["kv"][layer][b][0]).max()) < KV_TOL
+        assert float(np.abs(pre[layer][1] - st["kv"][layer][b][1]).max()) < KV_TOL
+    with pytest.raises(P.MaskError):
+        bad = mask.copy()
+        bad[0, 0] = False
+        P.forward_encode(w, tokens, P.ContextKV(ctx_pos, layers), bad)
+
+
+def test_errors_map_to_reference_exceptions():
+    meta, a, w, task, mc, enc = _encoded("c1")
+    with pytest.raises(P.ValidationError):
+        enc.cache.append_block(16, [], b"x" * 32)  # sealed
+    with pytest.raises(P.ValidationError):
+        P.assemble(enc.cache, P.Selection("block", (P.SegmentRef(0, 0, 0, 10), P.SegmentRef(1, 99, 0, 5))))
+    other = P.ModelConfig(64, 2, 4, 4, 16, 128, 259)
+    with pytest.raises(P.CompatibilityError):
+        P.Runner(P.init_random(other, 0), enc.cache, enc.index, task, mc)
+    with pytest.raises(P.ValidationError):
+        P.score_label(w, None, [], [5])
