@@ -87,27 +87,72 @@ __device__ __forceinline__ float fast_exp2(float x) {
 // Rotate this thread's query row (token t, head) at rope position `pos`,
 // composed with the optional per-segment shift, and write it zero-padded to
 // HDP into the swizzled K-major Q tile.  (model.rope_rotate_heads,
-// model.py:222-239: pair (x_i, x_{i+hd/2}).)
+// model.py:222-239: pair (x_i, x_{i+hd/2}).)  Vector path: 16-byte loads of
+// 8 bf16 from each half plus the matching (cos, sin) pairs, all issued before
+// use so one row costs a few memory round trips, not one per element.
 template <int HDP>
 __device__ __forceinline__ void load_q_row(const AttnParams &p, uint8_t *q_tile, int row, bool valid,
                                            int t, int head, int rot) {
   constexpr int QSW = AttnCfg<HDP, 1>::QSW;
   const int hd = p.head_dim, half = hd >> 1;
-  uint16_t *dst16 = nullptr;
-  (void)dst16;
+  auto put = [&](int c, const float (&o)[8]) {
+    const int atom = c / (QSW / 16), cc = c % (QSW / 16);
+    uint4 *d = reinterpret_cast<uint4 *>(q_tile + atom * 128 * QSW + swz_offset(row, cc, QSW));
+    *d = make_uint4(pack_bf16(o[0], o[1]), pack_bf16(o[2], o[3]), pack_bf16(o[4], o[5]), pack_bf16(o[6], o[7]));
+  };
   if (!valid) {
+    const float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-    for (int c = 0; c < HDP / 8; ++c) {
-      const int atom = c / (QSW / 16), cc = c % (QSW / 16);
-      uint4 *d = reinterpret_cast<uint4 *>(q_tile + atom * 128 * QSW + swz_offset(row, cc, QSW));
-      *d = make_uint4(0, 0, 0, 0);
-    }
+    for (int c = 0; c < HDP / 8; ++c) put(c, z);
     return;
   }
   const __nv_bfloat16 *src = p.q + (int64_t)t * p.q_tok_stride + (int64_t)head * hd;
   const float2 *rp = p.rope + (int64_t)p.tok_pos[t] * half;
   const float2 *rr = rot >= 0 ? p.rot + (int64_t)rot * half : nullptr;
-  // Build the rotated row chunk by chunk (8 output elements per 16-byte chunk).
+  if (HDP >= 32 && hd == HDP && (p.q_tok_stride & 7) == 0) {
+    // fast path: full-width head, every 8-element chunk lies in one half, 16-byte aligned rows
+#pragma unroll
+    for (int c0 = 0; c0 < HDP / 16; c0 += 2) {
+      uint4 lo4[2], hi4[2];
+      float4 cs4[2][4], rr4[2][4];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int i0 = (c0 + u) * 8;  // pair index of this chunk
+        lo4[u] = *reinterpret_cast<const uint4 *>(src + i0);
+        hi4[u] = *reinterpret_cast<const uint4 *>(src + half + i0);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) cs4[u][v] = reinterpret_cast<const float4 *>(rp + i0)[v];
+        if (rr) {
+#pragma unroll
+          for (int v = 0; v < 4; ++v) rr4[u][v] = reinterpret_cast<const float4 *>(rr + i0)[v];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const __nv_bfloat16 *lo = reinterpret_cast<const __nv_bfloat16 *>(&lo4[u]);
+        const __nv_bfloat16 *hi = reinterpret_cast<const __nv_bfloat16 *>(&hi4[u]);
+        const float *cs = reinterpret_cast<const float *>(cs4[u]);
+        const float *dd = reinterpret_cast<const float *>(rr4[u]);
+        float a[8], b[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          float c = cs[2 * j], sn = cs[2 * j + 1];
+          if (rr) {
+            const float dc = dd[2 * j], ds = dd[2 * j + 1];
+            const float c2 = c * dc - sn * ds;
+            sn = sn * dc + c * ds;
+            c = c2;
+          }
+          const float x = __bfloat162float(lo[j]), y = __bfloat162float(hi[j]);
+          a[j] = x * c - y * sn;
+          b[j] = x * sn + y * c;
+        }
+        put(c0 + u, a);
+        put(HDP / 16 + c0 + u, b);
+      }
+    }
+    return;
+  }
 #pragma unroll 1
   for (int c = 0; c < HDP / 8; ++c) {
     float o[8];
@@ -128,10 +173,7 @@ __device__ __forceinline__ void load_q_row(const AttnParams &p, uint8_t *q_tile,
       }
       o[j] = val;
     }
-    const int atom = c / (QSW / 16), cc = c % (QSW / 16);
-    uint4 *d = reinterpret_cast<uint4 *>(q_tile + atom * 128 * QSW + swz_offset(row, cc, QSW));
-    *d = make_uint4(pack_bf16(o[0], o[1]), pack_bf16(o[2], o[3]), pack_bf16(o[4], o[5]),
-                    pack_bf16(o[6], o[7]));
+    put(c, o);
   }
 }
 
@@ -190,12 +232,13 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
         const DbsaAttnSeg sg = p.segs[si];
         const CUtensorMap *tk = sg.src ? &tm_k1 : &tm_k0;
         const CUtensorMap *tv = sg.src ? &tm_v1 : &tm_v0;
-        const int nt = (sg.n_tok + kBN - 1) / kBN;
+        const int off = sg.row0 & (kBN - 1);
+        const int nt = (off + sg.n_tok + kBN - 1) / kBN;
         for (int tt = 0; tt < nt; ++tt, ++j) {
           const int st = j % C::STAGES;
           if (j >= C::STAGES) mbar_wait(&kv_empty[st], ((j / C::STAGES) & 1) ^ 1);
           mbar_arrive_expect_tx(&kv_full[st], C::STAGE_BYTES);
-          const int row = sg.row0 + tt * kBN;
+          const int row = sg.row0 - off + tt * kBN;  // tiles start on 64-row page boundaries
 #pragma unroll
           for (int a = 0; a < C::NATOM; ++a)
             tma_load_4d(sK + st * C::K_BYTES + a * kBN * C::QSW, tk, &kv_full[st], a * C::KATOM, row,
@@ -211,7 +254,8 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
       constexpr uint32_t idesc_o = umma_idesc_bf16(128, HDP);
       const uint32_t sQa = smem_u32(sQ), sPa = smem_u32(sP), sKa = smem_u32(sK), sVa = smem_u32(sV);
       int n_tiles = 0;
-      for (int si = w.seg_begin; si < w.seg_end; ++si) n_tiles += (p.segs[si].n_tok + kBN - 1) / kBN;
+      for (int si = w.seg_begin; si < w.seg_end; ++si)
+        n_tiles += ((p.segs[si].row0 & (kBN - 1)) + p.segs[si].n_tok + kBN - 1) / kBN;
 
       auto issue_qk = [&](int m, int j) {
         const int st = j % C::STAGES;
@@ -286,15 +330,39 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
     fence_proxy_async_smem();
     mbar_arrive(&q_full[m]);
 
+    // Online softmax in the log2 domain.  m_used is the (scaled) running max
+    // the O accumulator and l_sum are relative to; scale is folded into the
+    // exp2 FFMA: p = 2^(x * scale_log2 - m_used).
+    const float sl2 = p.scale_log2;
+    const bool warp_dead = __all_sync(0xffffffffu, !valid);
     float m_used = -INFINITY, l_sum = 0.f;
     int j = 0;
     for (int si = w.seg_begin; si < w.seg_end; ++si) {
       const DbsaAttnSeg sg = p.segs[si];
-      const int nt = (sg.n_tok + kBN - 1) / kBN;
+      const int off = sg.row0 & (kBN - 1);
+      const int nt = (off + sg.n_tok + kBN - 1) / kBN;
       const bool is_self = sg.kind == DBSA_SEG_SELF;
+      // visible local keys of this row: [0, vis_hi) minus the band [band_lo, band_hi)
+      int vis_hi = valid ? sg.n_tok : 0;
+      int band_lo = 0, band_hi = 0;
+      if (is_self) {
+        vis_hi = min(vis_hi, rl + 1);
+        band_lo = w.prefix;
+        band_hi = lo;
+      }
       for (int tt = 0; tt < nt; ++tt, ++j) {
+        const int k0 = tt * kBN - off;  // local key index of tile column 0
+        const int c_lo = max(0, -k0), c_hi = min(kBN, vis_hi - k0);
+        const int b_lo = band_lo - k0, b_hi = band_hi - k0;
+        const bool full = c_lo == 0 && c_hi == kBN && (b_hi <= 0 || b_lo >= kBN || b_lo >= b_hi);
         mbar_wait(&s_full[m], j & 1);
         tc_fence_after();
+        if (warp_dead) {  // no valid row in this warp: its P rows only feed its own (discarded) O rows
+          if (tt == nt - 1 && si + 1 < w.seg_end) cur_rot = p.segs[si + 1].rot;
+          tc_fence_before();
+          mbar_arrive(&p_full[m]);
+          continue;
+        }
         float x[kBN];
         {
           float a[32], b[32];
@@ -307,21 +375,27 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
             x[c + 32] = b[c];
           }
         }
-        const int k0 = tt * kBN;
-        float tmax = -INFINITY;
+        if (!__all_sync(0xffffffffu, full)) {
 #pragma unroll
-        for (int c = 0; c < kBN; ++c) {
-          const int kl = k0 + c;
-          bool ok = valid && kl < sg.n_tok;
-          if (is_self) ok = ok && kl <= rl && (kl < w.prefix || kl >= lo);
-          x[c] = ok ? x[c] * p.scale_log2 : -INFINITY;
-          tmax = fmaxf(tmax, x[c]);
+          for (int c = 0; c < kBN; ++c) {
+            const bool ok = (c >= c_lo) & (c < c_hi) & ((c < b_lo) | (c >= b_hi));
+            x[c] = ok ? x[c] : -INFINITY;
+          }
         }
+        float mx[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) mx[i] = fmaxf(x[i], x[i + 8]);
+#pragma unroll
+        for (int c = 16; c < kBN; c += 16)
+#pragma unroll
+          for (int i = 0; i < 8; ++i) mx[i] = fmaxf(mx[i], fmaxf(x[c + i], x[c + 8 + i]));
+        const float tmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                                 fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) * sl2;
         const float m_new = fmaxf(m_used, tmax);
-        // Lazy rescale (threshold 2^8): O and l keep a stale max until it
-        // grows by more than 8 in log2 units.  tcgen05.ld/st are warp-wide, so
-        // the decision is warp-uniform.
-        const bool need = (j > 0) && (m_used != -INFINITY) && (m_new > m_used + 8.f);
+        // Lazy rescale (threshold 2^8): O and l keep a stale max until it grows
+        // by more than 8 in log2 units; tcgen05.ld/st are warp-wide, so the
+        // decision is warp-uniform.
+        const bool need = (m_used != -INFINITY) && (m_new > m_used + 8.f);
         float alpha = 1.f;
         if (__any_sync(0xffffffffu, need)) {
           if (m_used != -INFINITY) alpha = fast_exp2(m_used - m_new);
@@ -341,20 +415,19 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
         }
         l_sum *= alpha;
         const float msub = m_used == -INFINITY ? 0.f : m_used;
-        float psum = 0.f;
+        float ps[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int c = 0; c < kBN; c += 8) {
           float e[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            e[i] = fast_exp2(x[c + i] - msub);
-            psum += e[i];
-          }
+          for (int i = 0; i < 8; ++i) e[i] = fast_exp2(fmaf(x[c + i], sl2, -msub));
+#pragma unroll
+          for (int i = 0; i < 8; ++i) ps[i & 3] += e[i];
           uint4 *d = reinterpret_cast<uint4 *>(p_tile + swz_offset(trow, c / 8, 128));
           *d = make_uint4(pack_bf16(e[0], e[1]), pack_bf16(e[2], e[3]), pack_bf16(e[4], e[5]),
                           pack_bf16(e[6], e[7]));
         }
-        l_sum += psum;
+        l_sum += (ps[0] + ps[1]) + (ps[2] + ps[3]);
         // Segment boundary: re-stage Q with the next segment's RoPE shift.  QK of
         // this tile is complete (s_full), so the Q tile is free.
         if (tt == nt - 1 && si + 1 < w.seg_end) {

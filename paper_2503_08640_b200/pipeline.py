@@ -138,7 +138,9 @@ class EncodedPool:
 
 
 def _device_model(weights):
-    return weights if isinstance(weights, engine.DeviceModel) else weights.device()
+    from .model import ModelWeights
+
+    return weights.device() if isinstance(weights, ModelWeights) else weights
 
 
 def render_block(template: PromptTemplate, pool, members):
