@@ -28,6 +28,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 
 #include "../../include/dbsa_b200.h"
 #include "dbsa_internal.h"
@@ -47,14 +48,14 @@ struct AttnCfg {
   static constexpr int K_BYTES = kBN * HDP * 2;
   static constexpr int V_BYTES = HDP * kBN * 2;
   static constexpr int STAGE_BYTES = K_BYTES + V_BYTES;
-  static constexpr int FIXED = NUM_M * (Q_BYTES + P_BYTES);
+  static constexpr int FIXED = NUM_M * Q_BYTES;  // P lives in TMEM (aliasing S)
   static constexpr int BAR_BYTES = 1024;
   static constexpr int SMEM_LIMIT = 232448 - 1024 /*align slack*/;
   static constexpr int STAGES_FIT = (SMEM_LIMIT - FIXED - BAR_BYTES) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_FIT > 6 ? 6 : STAGES_FIT;
   static constexpr int SMEM = FIXED + STAGES * STAGE_BYTES + BAR_BYTES + 1024;
   static constexpr int THREADS = 128 + 128 * NUM_M;
-  static constexpr int TMEM_NEED = NUM_M * (HDP + kBN);
+  static constexpr int TMEM_NEED = NUM_M * (HDP + 2 * kBN);  // O + double-buffered S per M tile
   static constexpr int TMEM_COLS =
       TMEM_NEED <= 32 ? 32 : TMEM_NEED <= 64 ? 64 : TMEM_NEED <= 128 ? 128 : TMEM_NEED <= 256 ? 256 : 512;
   static_assert(STAGES >= 2, "not enough shared memory for a 2-stage pipeline");
@@ -76,6 +77,7 @@ struct AttnParams {
   int64_t out_tok_stride;
   float *part_o;
   float *part_lse;
+  int dbg;  // profiling switches (DBSA_DEBUG_MODE): 1 = skip softmax math, 2 = skip MMAs, 4 = skip TMA loads
 };
 
 __device__ __forceinline__ float fast_exp2(float x) {
@@ -186,16 +188,16 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *sQ = smem;                             // NUM_M x Q_BYTES
-  uint8_t *sP = sQ + NUM_M * C::Q_BYTES;          // NUM_M x P_BYTES
-  uint8_t *sK = sP + NUM_M * C::P_BYTES;          // STAGES x K_BYTES
+  uint8_t *sK = sQ + NUM_M * C::Q_BYTES;          // STAGES x K_BYTES
   uint8_t *sV = sK + C::STAGES * C::K_BYTES;      // STAGES x V_BYTES
   uint64_t *bars = reinterpret_cast<uint64_t *>(sV + C::STAGES * C::V_BYTES);
   uint64_t *kv_full = bars;                       // [STAGES]
   uint64_t *kv_empty = kv_full + C::STAGES;       // [STAGES]
   uint64_t *q_full = kv_empty + C::STAGES;        // [NUM_M]
-  uint64_t *s_full = q_full + NUM_M;              // [NUM_M]
-  uint64_t *p_full = s_full + NUM_M;              // [NUM_M]
-  uint64_t *o_full = p_full + NUM_M;              // [NUM_M]
+  uint64_t *s_full = q_full + NUM_M;              // [NUM_M][2]  S buffer b of M tile m ready
+  uint64_t *p_full = s_full + 2 * NUM_M;          // [NUM_M][2]  P(m, j) in TMEM buffer j & 1
+  uint64_t *pv_done = p_full + 2 * NUM_M;         // [NUM_M]     P.V of M tile m retired
+  uint64_t *o_full = pv_done + NUM_M;             // [NUM_M]
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(o_full + NUM_M);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -208,8 +210,11 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
     }
     for (int m = 0; m < NUM_M; ++m) {
       mbar_init(&q_full[m], 128);
-      mbar_init(&s_full[m], 1);
-      mbar_init(&p_full[m], 128);
+      mbar_init(&s_full[2 * m], 1);
+      mbar_init(&s_full[2 * m + 1], 1);
+      mbar_init(&p_full[2 * m], 128);
+      mbar_init(&p_full[2 * m + 1], 128);
+      mbar_init(&pv_done[m], 1);
       mbar_init(&o_full[m], 1);
     }
     fence_mbar_init();
@@ -237,6 +242,10 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
         for (int tt = 0; tt < nt; ++tt, ++j) {
           const int st = j % C::STAGES;
           if (j >= C::STAGES) mbar_wait(&kv_empty[st], ((j / C::STAGES) & 1) ^ 1);
+          if (p.dbg & 4) {  // profiling: no loads
+            mbar_arrive(&kv_full[st]);
+            continue;
+          }
           mbar_arrive_expect_tx(&kv_full[st], C::STAGE_BYTES);
           const int row = sg.row0 - off + tt * kBN;  // tiles start on 64-row page boundaries
 #pragma unroll
@@ -252,56 +261,84 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
     if (lane == 0) {
       constexpr uint32_t idesc_s = umma_idesc_bf16(128, kBN);
       constexpr uint32_t idesc_o = umma_idesc_bf16(128, HDP);
-      const uint32_t sQa = smem_u32(sQ), sPa = smem_u32(sP), sKa = smem_u32(sK), sVa = smem_u32(sV);
+      const uint32_t sQa = smem_u32(sQ), sKa = smem_u32(sK), sVa = smem_u32(sV);
       int n_tiles = 0;
       for (int si = w.seg_begin; si < w.seg_end; ++si)
         n_tiles += ((p.segs[si].row0 & (kBN - 1)) + p.segs[si].n_tok + kBN - 1) / kBN;
 
+      // S(m, j) lands in TMEM buffer j & 1, so QK of tile j+1 (and j+2) can run
+      // on the tensor pipe while the softmax warps still work on tile j.  The
+      // one exception is a RoPE-shift boundary (stage-2 chunk with a different
+      // query rotation): QK of the first tile after it waits until the softmax
+      // warps have re-staged Q (their p_full of the previous tile).
       auto issue_qk = [&](int m, int j) {
         const int st = j % C::STAGES;
-        const uint32_t d = tbase + NUM_M * HDP + m * kBN;
+        const uint32_t d = tbase + NUM_M * HDP + (2 * m + (j & 1)) * kBN;
 #pragma unroll
         for (int kk = 0; kk < HDP / 16; ++kk) {
           const int a = (kk * 16) / C::KATOM;
           const int off = ((kk * 16) % C::KATOM) * 2;
           const uint64_t ad = umma_desc_kmajor(sQa + m * C::Q_BYTES + a * 128 * C::QSW + off, C::QSW);
           const uint64_t bd = umma_desc_kmajor(sKa + st * C::K_BYTES + a * kBN * C::QSW + off, C::QSW);
-          umma_bf16_ss(d, ad, bd, idesc_s, kk > 0 ? 1u : 0u);
+          if (!(p.dbg & 2)) umma_bf16_ss(d, ad, bd, idesc_s, kk > 0 ? 1u : 0u);
         }
-        umma_commit(&s_full[m]);
+        umma_commit(&s_full[2 * m + (j & 1)]);
       };
+      // O(m) += P(m, j) . V(j): P is bf16 in TMEM, packed two keys per column
+      // in the first kBN/2 columns of S buffer j & 1 (the TS form of tcgen05.mma).
       auto issue_pv = [&](int m, int j) {
         const int st = j % C::STAGES;
         const uint32_t d = tbase + m * HDP;
+        const uint32_t pa = tbase + NUM_M * HDP + (2 * m + (j & 1)) * kBN;
 #pragma unroll
         for (int kk = 0; kk < kBN / 16; ++kk) {
-          const uint64_t ad = umma_desc_kmajor(sPa + m * C::P_BYTES + kk * 32, 128);
           const uint64_t bd = umma_desc_kmajor(sVa + st * C::V_BYTES + kk * 32, 128);
-          umma_bf16_ss(d, ad, bd, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+          if (!(p.dbg & 2)) umma_bf16_ts(d, pa + kk * 8, bd, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
         }
+        umma_commit(&pv_done[m]);
+      };
+      // tile iterator of the next QK to issue: (segment, tile-in-segment)
+      int qi_seg = w.seg_begin, qi_tt = 0;
+      int qi_nt = qi_seg < w.seg_end ? ((p.segs[qi_seg].row0 & (kBN - 1)) + p.segs[qi_seg].n_tok + kBN - 1) / kBN : 0;
+      bool qi_boundary = false;  // next tile starts a segment whose rotation differs from the previous one
+      auto advance = [&]() {
+        if (++qi_tt >= qi_nt) {
+          const int prev_rot = p.segs[qi_seg].rot;
+          ++qi_seg;
+          qi_tt = 0;
+          if (qi_seg < w.seg_end) {
+            qi_nt = ((p.segs[qi_seg].row0 & (kBN - 1)) + p.segs[qi_seg].n_tok + kBN - 1) / kBN;
+            qi_boundary = p.segs[qi_seg].rot != prev_rot;
+          }
+        } else {
+          qi_boundary = false;
+        }
+      };
+      auto issue_tile = [&](int t) {
+        mbar_wait(&kv_full[t % C::STAGES], (t / C::STAGES) & 1);
+        tc_fence_after();
+        for (int m = 0; m < NUM_M; ++m) issue_qk(m, t);
+        advance();
       };
 
       if (n_tiles > 0) {
-        mbar_wait(&kv_full[0], 0);
-        tc_fence_after();
         for (int m = 0; m < NUM_M; ++m) {
           mbar_wait(&q_full[m], 0);
           tc_fence_after();
-          issue_qk(m, 0);
         }
+        int issued = 0;
+        issue_tile(issued++);
+        if (issued < n_tiles && !qi_boundary) issue_tile(issued++);
         for (int j = 0; j < n_tiles; ++j) {
           for (int m = 0; m < NUM_M; ++m) {
-            mbar_wait(&p_full[m], j & 1);
+            mbar_wait(&p_full[2 * m + (j & 1)], (j >> 1) & 1);
             tc_fence_after();
             issue_pv(m, j);
-            if (m == NUM_M - 1) umma_commit(&kv_empty[j % C::STAGES]);
-            if (j + 1 < n_tiles) {
-              if (m == 0) {
-                mbar_wait(&kv_full[(j + 1) % C::STAGES], ((j + 1) / C::STAGES) & 1);
-                tc_fence_after();
-              }
-              issue_qk(m, j + 1);
-            }
+          }
+          umma_commit(&kv_empty[j % C::STAGES]);
+          while (issued < n_tiles && issued <= j + 2) {
+            if (issued == j + 2 && qi_boundary) break;  // Q is re-staged by softmax(j + 1) first
+            issue_tile(issued++);
           }
         }
       }
@@ -320,9 +357,8 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
     const int rl = t - w.self_tok0;
     const int lo = (p.tok_lo && valid) ? p.tok_lo[t] : 0;
     uint8_t *q_tile = sQ + m * C::Q_BYTES;
-    uint8_t *p_tile = sP + m * C::P_BYTES;
     const uint32_t lane_base = tbase + ((uint32_t)(q4 * 32) << 16);
-    const uint32_t t_s = lane_base + NUM_M * HDP + m * kBN;
+    const uint32_t t_s0 = lane_base + NUM_M * HDP + 2 * m * kBN;  // S buffer 0; buffer 1 follows
     const uint32_t t_o = lane_base + m * HDP;
 
     int cur_rot = w.seg_end > w.seg_begin ? p.segs[w.seg_begin].rot : -1;
@@ -355,12 +391,13 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
         const int c_lo = max(0, -k0), c_hi = min(kBN, vis_hi - k0);
         const int b_lo = band_lo - k0, b_hi = band_hi - k0;
         const bool full = c_lo == 0 && c_hi == kBN && (b_hi <= 0 || b_lo >= kBN || b_lo >= b_hi);
-        mbar_wait(&s_full[m], j & 1);
+        mbar_wait(&s_full[2 * m + (j & 1)], (j >> 1) & 1);
         tc_fence_after();
-        if (warp_dead) {  // no valid row in this warp: its P rows only feed its own (discarded) O rows
+        const uint32_t t_s = t_s0 + (j & 1) * kBN;
+        if (warp_dead || (p.dbg & 1)) {  // no valid row in this warp: its P rows only feed its own (discarded) O rows
           if (tt == nt - 1 && si + 1 < w.seg_end) cur_rot = p.segs[si + 1].rot;
           tc_fence_before();
-          mbar_arrive(&p_full[m]);
+          mbar_arrive(&p_full[2 * m + (j & 1)]);
           continue;
         }
         float x[kBN];
@@ -398,6 +435,7 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
         const bool need = (m_used != -INFINITY) && (m_new > m_used + 8.f);
         float alpha = 1.f;
         if (__any_sync(0xffffffffu, need)) {
+          if (j > 0) mbar_wait(&pv_done[m], (j - 1) & 1);  // O is still accumulated by P.V(j-1)
           if (m_used != -INFINITY) alpha = fast_exp2(m_used - m_new);
           m_used = m_new;
 #pragma unroll 1
@@ -416,17 +454,15 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
         l_sum *= alpha;
         const float msub = m_used == -INFINITY ? 0.f : m_used;
         float ps[4] = {0.f, 0.f, 0.f, 0.f};
+        uint32_t pk[kBN / 2];
 #pragma unroll
-        for (int c = 0; c < kBN; c += 8) {
-          float e[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) e[i] = fast_exp2(fmaf(x[c + i], sl2, -msub));
-#pragma unroll
-          for (int i = 0; i < 8; ++i) ps[i & 3] += e[i];
-          uint4 *d = reinterpret_cast<uint4 *>(p_tile + swz_offset(trow, c / 8, 128));
-          *d = make_uint4(pack_bf16(e[0], e[1]), pack_bf16(e[2], e[3]), pack_bf16(e[4], e[5]),
-                          pack_bf16(e[6], e[7]));
+        for (int c = 0; c < kBN; c += 2) {
+          const float e0 = fast_exp2(fmaf(x[c], sl2, -msub));
+          const float e1 = fast_exp2(fmaf(x[c + 1], sl2, -msub));
+          ps[(c >> 1) & 3] += e0 + e1;
+          pk[c >> 1] = pack_bf16(e0, e1);
         }
+        tmem_st32(t_s, pk);  // P(j) over the first kBN/2 columns of S(j)
         l_sum += (ps[0] + ps[1]) + (ps[2] + ps[3]);
         // Segment boundary: re-stage Q with the next segment's RoPE shift.  QK of
         // this tile is complete (s_full), so the Q tile is free.
@@ -435,11 +471,15 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
           if (nrot != cur_rot) {
             cur_rot = nrot;
             load_q_row<HDP>(p, q_tile, trow, valid, t, head, cur_rot);
+            fence_proxy_async_smem();
           }
         }
-        fence_proxy_async_smem();
+        tmem_wait_st();
+        // p_full is double-buffered like S: arrivals for tile j+1 go to the other
+        // barrier, and tile j+2 cannot start before the MMA warp consumed p_full(j)
+        // (QK(j+2) is issued after it), so phases never mix or overrun.
         tc_fence_before();
-        mbar_arrive(&p_full[m]);
+        mbar_arrive(&p_full[2 * m + (j & 1)]);
       }
     }
 
@@ -575,6 +615,10 @@ extern "C" int dbsa_attention(const DbsaAttnArgs *args, void *stream) {
   p.out_tok_stride = a.out_tok_stride;
   p.part_o = a.part_o;
   p.part_lse = a.part_lse;
+  {
+    const char *e = getenv("DBSA_DEBUG_MODE");
+    p.dbg = e ? atoi(e) : 0;
+  }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   switch (a.hd_pad * 10 + a.num_m) {
     case 161: return launch_attn<16, 1>(a, p, maps, s);
