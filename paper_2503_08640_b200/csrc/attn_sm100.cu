@@ -15,13 +15,19 @@
 //            shift) + the query/label tokens (SELF, causal tree)
 //                                          -- Runner.infer / score_label (pipeline.py:410-421, model.py:420-443)
 //
-// Roles (warp-specialised, one CTA per work item):
-//   warp 0      TMA producer: K tile [64 x HDP] + V^T tile [HDP x 64] per stage
-//   warp 1      MMA issuer (one thread): S = Q K^T and O += P V on tcgen05
+// Roles (warp-specialised, one CTA per work item; FA4-style ping-pong):
+//   warp 0      TMA producer: K tile [128 keys x HDP] into a K ring, V^T tile
+//               [HDP x 128 keys] into a V ring (K runs one tile ahead of V)
+//   warp 1      MMA warp (converged; one elected lane issues): per M tile m,
+//               O(m) += P(m, j-1) V(j-1)  (A = P from TMEM)  then
+//               S(m) = Q(m) K(j)^T        (A = Q from smem)
 //   warp 2      TMEM allocator
 //   warps 4..   softmax warpgroups, one per 128-row M tile, one row per thread:
-//               Q prologue (load + RoPE + swizzled st.shared), S from TMEM,
-//               online softmax with lazy O rescale, P -> smem, epilogue.
+//               Q prologue (load + RoPE + per-segment shift, swizzled
+//               st.shared), S from TMEM, online softmax with lazy O rescale,
+//               P (bf16) back into TMEM over S, epilogue.
+// With two M tiles the tensor pipe works on tile m' while the softmax warps
+// of tile m run, and vice versa.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -36,29 +42,29 @@
 
 namespace dbsa {
 
-constexpr int kBN = 64;  // keys per tile
+constexpr int kBN = 128;  // keys per tile
 
 template <int HDP, int NUM_M>
 struct AttnCfg {
-  static constexpr int QSW = HDP >= 64 ? 128 : HDP * 2;   // swizzle width of Q / K rows (bytes)
-  static constexpr int KATOM = HDP >= 64 ? 64 : HDP;      // K-dim elements per atom column
-  static constexpr int NATOM = HDP / KATOM;               // atom columns along head_dim
+  static constexpr int QSW = HDP >= 64 ? 128 : HDP * 2;  // swizzle width of Q / K rows (bytes)
+  static constexpr int KATOM = HDP >= 64 ? 64 : HDP;     // head-dim elements per K atom column
+  static constexpr int NATOM = HDP / KATOM;              // atom columns along head_dim
   static constexpr int Q_BYTES = 128 * HDP * 2;
-  static constexpr int P_BYTES = 128 * kBN * 2;
   static constexpr int K_BYTES = kBN * HDP * 2;
-  static constexpr int V_BYTES = HDP * kBN * 2;
-  static constexpr int STAGE_BYTES = K_BYTES + V_BYTES;
-  static constexpr int FIXED = NUM_M * Q_BYTES;  // P lives in TMEM (aliasing S)
+  static constexpr int V_BYTES = HDP * kBN * 2;  // V^T: HDP rows, 2 atoms of 64 keys (128B swizzle)
+  static constexpr int FIXED = NUM_M * Q_BYTES;
   static constexpr int BAR_BYTES = 1024;
-  static constexpr int SMEM_LIMIT = 232448 - 1024 /*align slack*/;
-  static constexpr int STAGES_FIT = (SMEM_LIMIT - FIXED - BAR_BYTES) / STAGE_BYTES;
-  static constexpr int STAGES = STAGES_FIT > 6 ? 6 : STAGES_FIT;
-  static constexpr int SMEM = FIXED + STAGES * STAGE_BYTES + BAR_BYTES + 1024;
+  static constexpr int AVAIL = 232448 - 1024 /*align slack*/ - BAR_BYTES - FIXED;
+  static constexpr int PAIRS = AVAIL / (K_BYTES + V_BYTES) > 4 ? 4 : AVAIL / (K_BYTES + V_BYTES);
+  static constexpr int KST = PAIRS + ((AVAIL - PAIRS * (K_BYTES + V_BYTES)) >= K_BYTES ? 1 : 0);
+  static constexpr int VST = PAIRS;
+  static constexpr int SMEM = FIXED + KST * K_BYTES + VST * V_BYTES + BAR_BYTES + 1024;
   static constexpr int THREADS = 128 + 128 * NUM_M;
-  static constexpr int TMEM_NEED = NUM_M * (HDP + 2 * kBN);  // O + double-buffered S per M tile
+  static constexpr int REG_CTRL = 56, REG_SOFTMAX = 224;  // 128*56 + 256*224 <= 64K (NUM_M == 2)
+  static constexpr int TMEM_NEED = NUM_M * (HDP + kBN);  // O(m) + S/P(m)
   static constexpr int TMEM_COLS =
       TMEM_NEED <= 32 ? 32 : TMEM_NEED <= 64 ? 64 : TMEM_NEED <= 128 ? 128 : TMEM_NEED <= 256 ? 256 : 512;
-  static_assert(STAGES >= 2, "not enough shared memory for a 2-stage pipeline");
+  static_assert(PAIRS >= 2, "not enough shared memory for a 2-stage pipeline");
 };
 
 struct AttnParams {
@@ -187,34 +193,36 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
   using C = AttnCfg<HDP, NUM_M>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t *sQ = smem;                             // NUM_M x Q_BYTES
-  uint8_t *sK = sQ + NUM_M * C::Q_BYTES;          // STAGES x K_BYTES
-  uint8_t *sV = sK + C::STAGES * C::K_BYTES;      // STAGES x V_BYTES
-  uint64_t *bars = reinterpret_cast<uint64_t *>(sV + C::STAGES * C::V_BYTES);
-  uint64_t *kv_full = bars;                       // [STAGES]
-  uint64_t *kv_empty = kv_full + C::STAGES;       // [STAGES]
-  uint64_t *q_full = kv_empty + C::STAGES;        // [NUM_M]
-  uint64_t *s_full = q_full + NUM_M;              // [NUM_M][2]  S buffer b of M tile m ready
-  uint64_t *p_full = s_full + 2 * NUM_M;          // [NUM_M][2]  P(m, j) in TMEM buffer j & 1
-  uint64_t *pv_done = p_full + 2 * NUM_M;         // [NUM_M]     P.V of M tile m retired
-  uint64_t *o_full = pv_done + NUM_M;             // [NUM_M]
+  uint8_t *sQ = smem;                         // NUM_M x Q_BYTES
+  uint8_t *sK = sQ + NUM_M * C::Q_BYTES;      // KST x K_BYTES
+  uint8_t *sV = sK + C::KST * C::K_BYTES;     // VST x V_BYTES
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sV + C::VST * C::V_BYTES);
+  uint64_t *k_full = bars;                    // [KST]
+  uint64_t *k_empty = k_full + C::KST;        // [KST]
+  uint64_t *v_full = k_empty + C::KST;        // [VST]
+  uint64_t *v_empty = v_full + C::VST;        // [VST]
+  uint64_t *q_full = v_empty + C::VST;        // [NUM_M]
+  uint64_t *s_full = q_full + NUM_M;          // [NUM_M]  S(m, j) in TMEM
+  uint64_t *p_full = s_full + NUM_M;          // [NUM_M]  P(m, j) in TMEM (S consumed)
+  uint64_t *o_full = p_full + NUM_M;          // [NUM_M]
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(o_full + NUM_M);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const DbsaAttnWork w = p.works[blockIdx.x];
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < C::STAGES; ++s) {
-      mbar_init(&kv_full[s], 1);
-      mbar_init(&kv_empty[s], 1);
+    for (int s = 0; s < C::KST; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+    }
+    for (int s = 0; s < C::VST; ++s) {
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
     }
     for (int m = 0; m < NUM_M; ++m) {
       mbar_init(&q_full[m], 128);
-      mbar_init(&s_full[2 * m], 1);
-      mbar_init(&s_full[2 * m + 1], 1);
-      mbar_init(&p_full[2 * m], 128);
-      mbar_init(&p_full[2 * m + 1], 128);
-      mbar_init(&pv_done[m], 1);
+      mbar_init(&s_full[m], 1);
+      mbar_init(&p_full[m], 128);
       mbar_init(&o_full[m], 1);
     }
     fence_mbar_init();
@@ -232,48 +240,63 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
-      int j = 0;
+      // K(t) is issued one tile ahead of V(t - 1): QK needs K early, P.V needs V late.
+      int kj = 0, vj = 0;
+      auto load_v = [&](const DbsaAttnSeg &sg, int row) {
+        const int st = vj % C::VST;
+        if (vj >= C::VST) mbar_wait(&v_empty[st], ((vj / C::VST) & 1) ^ 1);
+        if (p.dbg & 4) {
+          mbar_arrive(&v_full[st]);
+        } else {
+          const CUtensorMap *tv = sg.src ? &tm_v1 : &tm_v0;
+          mbar_arrive_expect_tx(&v_full[st], C::V_BYTES);
+#pragma unroll
+          for (int a = 0; a < 2; ++a)
+            tma_load_4d(sV + st * C::V_BYTES + a * HDP * 128, tv, &v_full[st], row + a * 64, 0, w.kv_head, sg.layer);
+        }
+        ++vj;
+      };
+      DbsaAttnSeg pend_sg{};
+      int pend_row = -1;
       for (int si = w.seg_begin; si < w.seg_end; ++si) {
         const DbsaAttnSeg sg = p.segs[si];
-        const CUtensorMap *tk = sg.src ? &tm_k1 : &tm_k0;
-        const CUtensorMap *tv = sg.src ? &tm_v1 : &tm_v0;
-        const int off = sg.row0 & (kBN - 1);
+        const int off = sg.row0 & 63;  // tiles start on 64-row page boundaries
         const int nt = (off + sg.n_tok + kBN - 1) / kBN;
-        for (int tt = 0; tt < nt; ++tt, ++j) {
-          const int st = j % C::STAGES;
-          if (j >= C::STAGES) mbar_wait(&kv_empty[st], ((j / C::STAGES) & 1) ^ 1);
-          if (p.dbg & 4) {  // profiling: no loads
-            mbar_arrive(&kv_full[st]);
-            continue;
-          }
-          mbar_arrive_expect_tx(&kv_full[st], C::STAGE_BYTES);
-          const int row = sg.row0 - off + tt * kBN;  // tiles start on 64-row page boundaries
+        const CUtensorMap *tk = sg.src ? &tm_k1 : &tm_k0;
+        for (int tt = 0; tt < nt; ++tt) {
+          const int row = sg.row0 - off + tt * kBN;
+          const int st = kj % C::KST;
+          if (kj >= C::KST) mbar_wait(&k_empty[st], ((kj / C::KST) & 1) ^ 1);
+          if (p.dbg & 4) {
+            mbar_arrive(&k_full[st]);
+          } else {
+            mbar_arrive_expect_tx(&k_full[st], C::K_BYTES);
 #pragma unroll
-          for (int a = 0; a < C::NATOM; ++a)
-            tma_load_4d(sK + st * C::K_BYTES + a * kBN * C::QSW, tk, &kv_full[st], a * C::KATOM, row,
-                        w.kv_head, sg.layer);
-          tma_load_4d(sV + st * C::V_BYTES, tv, &kv_full[st], row, 0, w.kv_head, sg.layer);
+            for (int a = 0; a < C::NATOM; ++a)
+              tma_load_4d(sK + st * C::K_BYTES + a * kBN * C::QSW, tk, &k_full[st], a * C::KATOM, row, w.kv_head,
+                          sg.layer);
+          }
+          ++kj;
+          if (pend_row >= 0) load_v(pend_sg, pend_row);
+          pend_sg = sg;
+          pend_row = row;
         }
       }
+      if (pend_row >= 0) load_v(pend_sg, pend_row);
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc_s = umma_idesc_bf16(128, kBN);
-      constexpr uint32_t idesc_o = umma_idesc_bf16(128, HDP);
-      const uint32_t sQa = smem_u32(sQ), sKa = smem_u32(sK), sVa = smem_u32(sV);
-      int n_tiles = 0;
-      for (int si = w.seg_begin; si < w.seg_end; ++si)
-        n_tiles += ((p.segs[si].row0 & (kBN - 1)) + p.segs[si].n_tok + kBN - 1) / kBN;
-
-      // S(m, j) lands in TMEM buffer j & 1, so QK of tile j+1 (and j+2) can run
-      // on the tensor pipe while the softmax warps still work on tile j.  The
-      // one exception is a RoPE-shift boundary (stage-2 chunk with a different
-      // query rotation): QK of the first tile after it waits until the softmax
-      // warps have re-staged Q (their p_full of the previous tile).
-      auto issue_qk = [&](int m, int j) {
-        const int st = j % C::STAGES;
-        const uint32_t d = tbase + NUM_M * HDP + (2 * m + (j & 1)) * kBN;
+    // ------------------------------------------------------------ MMA warp
+    constexpr uint32_t idesc_s = umma_idesc_bf16(128, kBN);
+    constexpr uint32_t idesc_o = umma_idesc_bf16(128, HDP);
+    const uint32_t sQa = smem_u32(sQ), sKa = smem_u32(sK), sVa = smem_u32(sV);
+    int n_tiles = 0;
+    for (int si = w.seg_begin; si < w.seg_end; ++si)
+      n_tiles += ((p.segs[si].row0 & 63) + p.segs[si].n_tok + kBN - 1) / kBN;
+    const bool leader = elect_one();
+    auto qk = [&](int m, int j) {  // S(m) = Q(m) K(j)^T, K = head_dim
+      const int st = j % C::KST;
+      const uint32_t d = tbase + NUM_M * HDP + m * kBN;
+      if (leader) {
 #pragma unroll
         for (int kk = 0; kk < HDP / 16; ++kk) {
           const int a = (kk * 16) / C::KATOM;
@@ -282,67 +305,59 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
           const uint64_t bd = umma_desc_kmajor(sKa + st * C::K_BYTES + a * kBN * C::QSW + off, C::QSW);
           if (!(p.dbg & 2)) umma_bf16_ss(d, ad, bd, idesc_s, kk > 0 ? 1u : 0u);
         }
-        umma_commit(&s_full[2 * m + (j & 1)]);
-      };
-      // O(m) += P(m, j) . V(j): P is bf16 in TMEM, packed two keys per column
-      // in the first kBN/2 columns of S buffer j & 1 (the TS form of tcgen05.mma).
-      auto issue_pv = [&](int m, int j) {
-        const int st = j % C::STAGES;
-        const uint32_t d = tbase + m * HDP;
-        const uint32_t pa = tbase + NUM_M * HDP + (2 * m + (j & 1)) * kBN;
+        umma_commit(&s_full[m]);
+      }
+      __syncwarp();
+    };
+    auto pv = [&](int m, int j) {  // O(m) += P(m, j) V(j), K = kBN keys, P from TMEM
+      const int st = j % C::VST;
+      const uint32_t d = tbase + m * HDP;
+      const uint32_t pa = tbase + NUM_M * HDP + m * kBN;
+      if (leader) {
 #pragma unroll
         for (int kk = 0; kk < kBN / 16; ++kk) {
-          const uint64_t bd = umma_desc_kmajor(sVa + st * C::V_BYTES + kk * 32, 128);
+          const int a = kk / 4;             // 64-key atom column
+          const int off = (kk % 4) * 32;    // byte offset inside the 128-byte atom row
+          const uint64_t bd = umma_desc_kmajor(sVa + st * C::V_BYTES + a * HDP * 128 + off, 128);
           if (!(p.dbg & 2)) umma_bf16_ts(d, pa + kk * 8, bd, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
         }
-        umma_commit(&pv_done[m]);
-      };
-      // tile iterator of the next QK to issue: (segment, tile-in-segment)
-      int qi_seg = w.seg_begin, qi_tt = 0;
-      int qi_nt = qi_seg < w.seg_end ? ((p.segs[qi_seg].row0 & (kBN - 1)) + p.segs[qi_seg].n_tok + kBN - 1) / kBN : 0;
-      bool qi_boundary = false;  // next tile starts a segment whose rotation differs from the previous one
-      auto advance = [&]() {
-        if (++qi_tt >= qi_nt) {
-          const int prev_rot = p.segs[qi_seg].rot;
-          ++qi_seg;
-          qi_tt = 0;
-          if (qi_seg < w.seg_end) {
-            qi_nt = ((p.segs[qi_seg].row0 & (kBN - 1)) + p.segs[qi_seg].n_tok + kBN - 1) / kBN;
-            qi_boundary = p.segs[qi_seg].rot != prev_rot;
-          }
-        } else {
-          qi_boundary = false;
-        }
-      };
-      auto issue_tile = [&](int t) {
-        mbar_wait(&kv_full[t % C::STAGES], (t / C::STAGES) & 1);
-        tc_fence_after();
-        for (int m = 0; m < NUM_M; ++m) issue_qk(m, t);
-        advance();
-      };
-
-      if (n_tiles > 0) {
-        for (int m = 0; m < NUM_M; ++m) {
-          mbar_wait(&q_full[m], 0);
-          tc_fence_after();
-        }
-        int issued = 0;
-        issue_tile(issued++);
-        if (issued < n_tiles && !qi_boundary) issue_tile(issued++);
-        for (int j = 0; j < n_tiles; ++j) {
-          for (int m = 0; m < NUM_M; ++m) {
-            mbar_wait(&p_full[2 * m + (j & 1)], (j >> 1) & 1);
-            tc_fence_after();
-            issue_pv(m, j);
-          }
-          umma_commit(&kv_empty[j % C::STAGES]);
-          while (issued < n_tiles && issued <= j + 2) {
-            if (issued == j + 2 && qi_boundary) break;  // Q is re-staged by softmax(j + 1) first
-            issue_tile(issued++);
-          }
-        }
       }
-      for (int m = 0; m < NUM_M; ++m) umma_commit(&o_full[m]);
+      __syncwarp();
+    };
+    auto commit = [&](uint64_t *bar) {
+      if (leader) umma_commit(bar);
+      __syncwarp();
+    };
+    if (n_tiles > 0) {
+      for (int m = 0; m < NUM_M; ++m) mbar_wait(&q_full[m], 0);
+      tc_fence_after();
+      for (int j = 0; j < n_tiles; ++j) {
+        mbar_wait(&k_full[j % C::KST], (j / C::KST) & 1);
+        tc_fence_after();
+        for (int m = 0; m < NUM_M; ++m) {
+          if (j > 0) {
+            // P(m, j-1) ready (and S(m) free): accumulate it, then reuse S(m) for tile j
+            mbar_wait(&p_full[m], (j - 1) & 1);
+            if (m == 0) mbar_wait(&v_full[(j - 1) % C::VST], ((j - 1) / C::VST) & 1);
+            tc_fence_after();
+            pv(m, j - 1);
+            if (m == NUM_M - 1) commit(&v_empty[(j - 1) % C::VST]);
+          }
+          qk(m, j);
+        }
+        commit(&k_empty[j % C::KST]);
+      }
+      const int j = n_tiles - 1;
+      for (int m = 0; m < NUM_M; ++m) {
+        mbar_wait(&p_full[m], j & 1);
+        if (m == 0) mbar_wait(&v_full[j % C::VST], (j / C::VST) & 1);
+        tc_fence_after();
+        pv(m, j);
+        commit(&o_full[m]);
+      }
+      commit(&v_empty[j % C::VST]);
+    } else {
+      for (int m = 0; m < NUM_M; ++m) commit(&o_full[m]);
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ softmax warpgroups
@@ -358,7 +373,7 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
     const int lo = (p.tok_lo && valid) ? p.tok_lo[t] : 0;
     uint8_t *q_tile = sQ + m * C::Q_BYTES;
     const uint32_t lane_base = tbase + ((uint32_t)(q4 * 32) << 16);
-    const uint32_t t_s0 = lane_base + NUM_M * HDP + 2 * m * kBN;  // S buffer 0; buffer 1 follows
+    const uint32_t t_s = lane_base + NUM_M * HDP + m * kBN;
     const uint32_t t_o = lane_base + m * HDP;
 
     int cur_rot = w.seg_end > w.seg_begin ? p.segs[w.seg_begin].rot : -1;
@@ -366,16 +381,15 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
     fence_proxy_async_smem();
     mbar_arrive(&q_full[m]);
 
-    // Online softmax in the log2 domain.  m_used is the (scaled) running max
-    // the O accumulator and l_sum are relative to; scale is folded into the
-    // exp2 FFMA: p = 2^(x * scale_log2 - m_used).
+    // Online softmax in the log2 domain; the scale is folded into the exp2
+    // FFMA: p = 2^(x * scale_log2 - m_used).
     const float sl2 = p.scale_log2;
     const bool warp_dead = __all_sync(0xffffffffu, !valid);
     float m_used = -INFINITY, l_sum = 0.f;
     int j = 0;
     for (int si = w.seg_begin; si < w.seg_end; ++si) {
       const DbsaAttnSeg sg = p.segs[si];
-      const int off = sg.row0 & (kBN - 1);
+      const int off = sg.row0 & 63;
       const int nt = (off + sg.n_tok + kBN - 1) / kBN;
       const bool is_self = sg.kind == DBSA_SEG_SELF;
       // visible local keys of this row: [0, vis_hi) minus the band [band_lo, band_hi)
@@ -391,27 +405,19 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
         const int c_lo = max(0, -k0), c_hi = min(kBN, vis_hi - k0);
         const int b_lo = band_lo - k0, b_hi = band_hi - k0;
         const bool full = c_lo == 0 && c_hi == kBN && (b_hi <= 0 || b_lo >= kBN || b_lo >= b_hi);
-        mbar_wait(&s_full[2 * m + (j & 1)], (j >> 1) & 1);
+        const bool restage = tt == nt - 1 && si + 1 < w.seg_end && p.segs[si + 1].rot != cur_rot;
+        mbar_wait(&s_full[m], j & 1);
         tc_fence_after();
-        const uint32_t t_s = t_s0 + (j & 1) * kBN;
-        if (warp_dead || (p.dbg & 1)) {  // no valid row in this warp: its P rows only feed its own (discarded) O rows
-          if (tt == nt - 1 && si + 1 < w.seg_end) cur_rot = p.segs[si + 1].rot;
+        if (warp_dead || (p.dbg & 1)) {  // no valid row: its P rows only feed its own (discarded) O rows
+          if (restage) cur_rot = p.segs[si + 1].rot;
           tc_fence_before();
-          mbar_arrive(&p_full[2 * m + (j & 1)]);
+          mbar_arrive(&p_full[m]);
           continue;
         }
         float x[kBN];
-        {
-          float a[32], b[32];
-          tmem_ld32(t_s, a);
-          tmem_ld32(t_s + 32, b);
-          tmem_wait_ld();
 #pragma unroll
-          for (int c = 0; c < 32; ++c) {
-            x[c] = a[c];
-            x[c + 32] = b[c];
-          }
-        }
+        for (int c = 0; c < kBN; c += 32) tmem_ld32(t_s + c, *reinterpret_cast<float(*)[32]>(&x[c]));
+        tmem_wait_ld();
         if (!__all_sync(0xffffffffu, full)) {
 #pragma unroll
           for (int c = 0; c < kBN; ++c) {
@@ -429,13 +435,12 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
         const float tmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
                                  fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) * sl2;
         const float m_new = fmaxf(m_used, tmax);
-        // Lazy rescale (threshold 2^8): O and l keep a stale max until it grows
-        // by more than 8 in log2 units; tcgen05.ld/st are warp-wide, so the
-        // decision is warp-uniform.
+        // Lazy rescale (threshold 2^8).  S(m, j) being complete implies P.V(m, j-1)
+        // retired (issued before QK(m, j) on the in-order tensor pipe), so O(m)
+        // is quiescent here.  tcgen05.ld/st are warp-wide: the decision is warp-uniform.
         const bool need = (m_used != -INFINITY) && (m_new > m_used + 8.f);
         float alpha = 1.f;
         if (__any_sync(0xffffffffu, need)) {
-          if (j > 0) mbar_wait(&pv_done[m], (j - 1) & 1);  // O is still accumulated by P.V(j-1)
           if (m_used != -INFINITY) alpha = fast_exp2(m_used - m_new);
           m_used = m_new;
 #pragma unroll 1
@@ -447,39 +452,33 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
             for (int i = 0; i < 16; ++i) o[i] *= alpha;
             tmem_st16(t_o + c0, o);
           }
-          tmem_wait_st();
         } else if (m_used == -INFINITY) {
-          m_used = m_new;  // first finite max: O row holds only zeros (or nothing yet)
+          m_used = m_new;  // first finite max: O row holds nothing yet
         }
         l_sum *= alpha;
         const float msub = m_used == -INFINITY ? 0.f : m_used;
         float ps[4] = {0.f, 0.f, 0.f, 0.f};
-        uint32_t pk[kBN / 2];
 #pragma unroll
-        for (int c = 0; c < kBN; c += 2) {
-          const float e0 = fast_exp2(fmaf(x[c], sl2, -msub));
-          const float e1 = fast_exp2(fmaf(x[c + 1], sl2, -msub));
-          ps[(c >> 1) & 3] += e0 + e1;
-          pk[c >> 1] = pack_bf16(e0, e1);
-        }
-        tmem_st32(t_s, pk);  // P(j) over the first kBN/2 columns of S(j)
-        l_sum += (ps[0] + ps[1]) + (ps[2] + ps[3]);
-        // Segment boundary: re-stage Q with the next segment's RoPE shift.  QK of
-        // this tile is complete (s_full), so the Q tile is free.
-        if (tt == nt - 1 && si + 1 < w.seg_end) {
-          const int nrot = p.segs[si + 1].rot;
-          if (nrot != cur_rot) {
-            cur_rot = nrot;
-            load_q_row<HDP>(p, q_tile, trow, valid, t, head, cur_rot);
-            fence_proxy_async_smem();
+        for (int h = 0; h < 2; ++h) {
+          uint32_t pk[32];
+#pragma unroll
+          for (int c = 0; c < 64; c += 2) {
+            const float e0 = fast_exp2(fmaf(x[h * 64 + c], sl2, -msub));
+            const float e1 = fast_exp2(fmaf(x[h * 64 + c + 1], sl2, -msub));
+            ps[(c >> 1) & 3] += e0 + e1;
+            pk[c >> 1] = pack_bf16(e0, e1);
           }
+          tmem_st32(t_s + h * 32, pk);  // P(j): keys 64h..64h+63 over S columns 32h..32h+31
+        }
+        l_sum += (ps[0] + ps[1]) + (ps[2] + ps[3]);
+        if (restage) {  // QK(m, j) retired (S read) and QK(m, j+1) waits for p_full(m, j)
+          cur_rot = p.segs[si + 1].rot;
+          load_q_row<HDP>(p, q_tile, trow, valid, t, head, cur_rot);
+          fence_proxy_async_smem();
         }
         tmem_wait_st();
-        // p_full is double-buffered like S: arrivals for tile j+1 go to the other
-        // barrier, and tile j+2 cannot start before the MMA warp consumed p_full(j)
-        // (QK(j+2) is issued after it), so phases never mix or overrun.
         tc_fence_before();
-        mbar_arrive(&p_full[2 * m + (j & 1)]);
+        mbar_arrive(&p_full[m]);
       }
     }
 
@@ -507,7 +506,14 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
           }
         } else {
           float *dst = p.part_o + (w.part_row0 + r) * (int64_t)hd + c0;
-          for (int i = 0; i < 16 && c0 + i < hd; ++i) dst[i] = o[i] * inv_l;
+          if (hd % 16 == 0) {
+            float4 *d4 = reinterpret_cast<float4 *>(dst);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              d4[i] = make_float4(o[4 * i] * inv_l, o[4 * i + 1] * inv_l, o[4 * i + 2] * inv_l, o[4 * i + 3] * inv_l);
+          } else {
+            for (int i = 0; i < 16 && c0 + i < hd; ++i) dst[i] = o[i] * inv_l;
+          }
         }
       }
     }
@@ -545,7 +551,7 @@ static bool encode_plane_maps(const DbsaAttnArgs &a, const void *k, const void *
     cuuint64_t dims[4] = {(cuuint64_t)rows, (cuuint64_t)HDP, (cuuint64_t)a.n_kv_heads, (cuuint64_t)layers};
     cuuint64_t strides[3] = {(cuuint64_t)rows * 2, (cuuint64_t)HDP * rows * 2,
                              (cuuint64_t)a.n_kv_heads * HDP * rows * 2};
-    cuuint32_t box[4] = {(cuuint32_t)kBN, (cuuint32_t)HDP, 1, 1};
+    cuuint32_t box[4] = {64u, (cuuint32_t)HDP, 1, 1};  // one 64-key atom column of the V^T tile
     cuuint32_t estr[4] = {1, 1, 1, 1};
     if (!encode_tiled_bf16(tv, v, 4, dims, strides, box, estr, CU_TENSOR_MAP_SWIZZLE_128B)) return false;
   }
