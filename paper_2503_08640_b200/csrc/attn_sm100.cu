@@ -86,6 +86,23 @@ struct AttnParams {
   int dbg;  // profiling switches (DBSA_DEBUG_MODE): 1 = skip softmax math, 2 = skip MMAs, 4 = skip TMA loads
 };
 
+// 2^x for a pair on the FMA/ALU pipes (FA4's MUFU offload): round to the
+// nearest integer with the 1.5*2^23 trick, a cubic for 2^f on f in [-0.5, 0.5]
+// (rel. error < 7e-4, below bf16's 2^-8 resolution of P), integer part added
+// to the exponent field.  Inputs are clamped at -126 (masked -inf -> ~1e-38).
+__device__ __forceinline__ float2 exp2_fma2(float2 x) {
+  x = make_float2(fmaxf(x.x, -126.f), fmaxf(x.y, -126.f));
+  const float2 magic = make_float2(12582912.f, 12582912.f);
+  const float2 t = fadd2(x, magic);
+  const float2 r = fadd2(t, make_float2(-12582912.f, -12582912.f));  // round(x)
+  const float2 f = ffma2(r, make_float2(-1.f, -1.f), x);              // x - round(x)
+  float2 q = ffma2(f, make_float2(0.0555041087f, 0.0555041087f), make_float2(0.2402265070f, 0.2402265070f));
+  q = ffma2(q, f, make_float2(0.6931471806f, 0.6931471806f));
+  q = ffma2(q, f, make_float2(1.f, 1.f));
+  return make_float2(__int_as_float(__float_as_int(q.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(q.y) + (__float_as_int(t.y) << 23)));
+}
+
 __device__ __forceinline__ float fast_exp2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -427,13 +444,14 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
         }
         float mx[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) mx[i] = fmaxf(x[i], x[i + 8]);
+        for (int i = 0; i < 8; ++i) mx[i] = fmax3(x[i], x[i + 8], x[i + 16]);
 #pragma unroll
-        for (int c = 16; c < kBN; c += 16)
+        for (int c = 24; c + 16 < kBN; c += 16)
 #pragma unroll
-          for (int i = 0; i < 8; ++i) mx[i] = fmaxf(mx[i], fmaxf(x[c + i], x[c + 8 + i]));
-        const float tmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
-                                 fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) * sl2;
+          for (int i = 0; i < 8; ++i) mx[i] = fmax3(mx[i], x[c + i], x[c + 8 + i]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) mx[i] = fmaxf(mx[i], x[kBN - 8 + i]);
+        const float tmax = fmax3(fmax3(mx[0], mx[1], mx[2]), fmax3(mx[3], mx[4], mx[5]), fmaxf(mx[6], mx[7])) * sl2;
         const float m_new = fmaxf(m_used, tmax);
         // Lazy rescale (threshold 2^8).  S(m, j) being complete implies P.V(m, j-1)
         // retired (issued before QK(m, j) on the in-order tensor pipe), so O(m)
@@ -457,20 +475,25 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
         }
         l_sum *= alpha;
         const float msub = m_used == -INFINITY ? 0.f : m_used;
-        float ps[4] = {0.f, 0.f, 0.f, 0.f};
+        // exp2 of (x * scale_log2 - m) two lanes at a time (FFMA2 / FADD2); one
+        // pair in four goes through the FMA-pipe exp2 so the MUFU pipe
+        // (16/clk/SM) does not bound the tile.
+        const float2 sl2v = make_float2(sl2, sl2), nmv = make_float2(-msub, -msub);
+        float2 ps[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           uint32_t pk[32];
 #pragma unroll
           for (int c = 0; c < 64; c += 2) {
-            const float e0 = fast_exp2(fmaf(x[h * 64 + c], sl2, -msub));
-            const float e1 = fast_exp2(fmaf(x[h * 64 + c + 1], sl2, -msub));
-            ps[(c >> 1) & 3] += e0 + e1;
-            pk[c >> 1] = pack_bf16(e0, e1);
+            const float2 a = ffma2(make_float2(x[h * 64 + c], x[h * 64 + c + 1]), sl2v, nmv);
+            const float2 e = ((c >> 1) & 3) == 3 ? exp2_fma2(a) : make_float2(fast_exp2(a.x), fast_exp2(a.y));
+            ps[(c >> 1) & 1] = fadd2(ps[(c >> 1) & 1], e);
+            pk[c >> 1] = pack_bf16(e.x, e.y);
           }
           tmem_st32(t_s + h * 32, pk);  // P(j): keys 64h..64h+63 over S columns 32h..32h+31
         }
-        l_sum += (ps[0] + ps[1]) + (ps[2] + ps[3]);
+        const float2 pss = fadd2(ps[0], ps[1]);
+        l_sum += pss.x + pss.y;
         if (restage) {  // QK(m, j) retired (S read) and QK(m, j+1) waits for p_full(m, j)
           cur_rot = p.segs[si + 1].rot;
           load_q_row<HDP>(p, q_tile, trow, valid, t, head, cur_rot);

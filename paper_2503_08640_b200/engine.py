@@ -323,7 +323,13 @@ class Stage1Plan:
                 keys = n_ctx + t0 + nt
                 for kv in range(hkv):
                     works.append((keys, local0 + t0, nt, local0, kv, sb, len(segs), 0, 0, 0))
-        works.sort(key=lambda w: -w[0])  # longest key streams first: a shorter tail wave
+        # Group-major order: the slabs x kv heads of one group run together, so its
+        # context groups are read from HBM once and re-read from L2; among groups,
+        # the longest key streams go first (shorter tail wave).
+        longest = {}
+        for wk in works:
+            longest[wk[3]] = max(longest.get(wk[3], 0), wk[0])
+        works.sort(key=lambda wk: (-longest[wk[3]], wk[3], -wk[0]))
         self.pairs = pairs
         self.n_works = len(works)
         self.n_segs = len(segs)
@@ -394,7 +400,7 @@ def label_job(chunks, n_ctx, query_ids, labels) -> QueryJob:
 class Stage2Plan:
     """Device tables for a batch of QueryJobs."""
 
-    def __init__(self, dm, jobs, target_ctas: int | None = None):
+    def __init__(self, dm, jobs, target_ctas: int | None = None, order: str = "query"):
         torch = _torch()
         c = dm.config
         gs, hkv, hd = c.group_size, c.n_kv_heads, c.head_dim
@@ -449,6 +455,11 @@ class Stage2Plan:
                     if n_split > 1:
                         merges.append((base, rows, n_split, q0 + t0, kv))
                         part_rows += n_split * rows
+        if order == "chunk":
+            # works whose first chunk is the same group run together: L2 reuse across queries
+            first_row = [segs[wk[4]][2] if segs[wk[4]][0] == 0 else 1 << 30 for wk in works]
+            idx = sorted(range(len(works)), key=lambda i: (first_row[i], works[i][3]))
+            works = [works[i] for i in idx]
         self.kv_tokens = kv_bytes
         self.n_works, self.n_segs, self.n_merge = len(works), len(segs), len(merges)
         dev = dm.device

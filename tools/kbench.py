@@ -20,6 +20,7 @@ ap.add_argument("--gtok", type=int, default=1500)
 ap.add_argument("--hkv", type=int, default=8)
 ap.add_argument("--heads", type=int, default=32)
 ap.add_argument("--target", type=int, default=0)
+ap.add_argument("--order", default="query")
 args = ap.parse_args()
 
 dev = torch.device("cuda", 0)
@@ -70,7 +71,7 @@ if args.stage in ("2", "both"):
     q = [rng.integers(3, 1000, 32).tolist() for _ in range(B)]
     tabs, n_ctx = sess.chunks_for(ids)
     jobs = [engine.label_job(tabs[i], int(n_ctx[i]), q[i], sess.label_ids) for i in range(B)]
-    plan = engine.Stage2Plan(dm, jobs, args.target or None)
+    plan = engine.Stage2Plan(dm, jobs, args.target or None, args.order)
     qkv = torch.randn(plan.n_tok, stride, device=dev).to(torch.bfloat16)
     out = torch.empty(plan.n_tok, qw, dtype=torch.bfloat16, device=dev)
     aux = (plan.k_aux, plan.v_aux, plan.aux_rows, 1)
