@@ -421,7 +421,9 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
         const int k0 = tt * kBN - off;  // local key index of tile column 0
         const int c_lo = max(0, -k0), c_hi = min(kBN, vis_hi - k0);
         const int b_lo = band_lo - k0, b_hi = band_hi - k0;
-        const bool full = c_lo == 0 && c_hi == kBN && (b_hi <= 0 || b_lo >= kBN || b_lo >= b_hi);
+        // invalid rows (beyond the work's rows) count as full: their S is Q=0 . K = 0
+        // and their P only feeds their own (never stored) O rows
+        const bool full = !valid || (c_lo == 0 && c_hi == kBN && (b_hi <= 0 || b_lo >= kBN || b_lo >= b_hi));
         const bool restage = tt == nt - 1 && si + 1 < w.seg_end && p.segs[si + 1].rot != cur_rot;
         mbar_wait(&s_full[m], j & 1);
         tc_fence_after();

@@ -377,24 +377,32 @@ def encode_groups(dm, cache, new, ids, pattern, layers=None) -> int:
 class QueryJob:
     """One stage-2 forward: new tokens (query, then label branches) against a
     chunk table.  pos/lo are LOCAL (position = n_ctx + pos; lo = lowest
-    non-prefix self key visible, tree mask)."""
+    non-prefix self key visible, tree mask).  `labels` (label token lists)
+    is set for label-scoring jobs."""
 
-    __slots__ = ("chunks", "n_ctx", "ids", "pos", "lo", "prefix")
+    __slots__ = ("chunks", "n_ctx", "ids", "pos", "lo", "prefix", "labels")
 
-    def __init__(self, chunks, n_ctx, ids, pos, lo, prefix):
+    def __init__(self, chunks, n_ctx, ids, pos, lo, prefix, labels=None):
         self.chunks, self.n_ctx, self.ids, self.pos, self.lo, self.prefix = chunks, n_ctx, ids, pos, lo, prefix
+        self.labels = labels
 
 
 def label_job(chunks, n_ctx, query_ids, labels) -> QueryJob:
-    """Query followed by every label as a branch of a token tree."""
+    """Query followed by every label as a branch of a token tree.
+
+    The LAST token of each label is not fed: its logits are never scored
+    (score_label reads rows len(q)-1 .. len(q)+len(label)-2, model.py:441-443)
+    and no other token attends to it (it ends its branch), so dropping it
+    leaves every label score unchanged."""
     nq = len(query_ids)
     ids, pos, lo = list(query_ids), list(range(nq)), [0] * nq
     for lab in labels:
         start = len(ids)
-        ids += list(lab)
-        pos += list(range(nq, nq + len(lab)))
-        lo += [start] * len(lab)
-    return QueryJob(chunks, n_ctx, ids, pos, lo, nq)
+        fed = list(lab)[:-1]
+        ids += fed
+        pos += list(range(nq, nq + len(fed)))
+        lo += [start] * len(fed)
+    return QueryJob(chunks, n_ctx, ids, pos, lo, nq, [list(x) for x in labels])
 
 
 class Stage2Plan:
@@ -557,18 +565,16 @@ class LabelScorer:
             base = int(plan.tok0[qi])
             nq = j.prefix
             off = nq
-            for li in range(n_labels):
-                # label li occupies [off, off + len) with lo == off
-                ln = 0
-                while off + ln < len(j.ids) and j.lo[off + ln] == off:
-                    ln += 1
+            for li, lab in enumerate(j.labels):
+                # label token k is predicted by the last query row (k = 0) or by
+                # the fed label token k-1 at local index off + k - 1
                 prev = base + nq - 1
-                for k in range(ln):
+                for k, tok in enumerate(lab):
                     rows.append(prev)
-                    targets.append(j.ids[off + k])
+                    targets.append(tok)
                     owner.append(qi * n_labels + li)
                     prev = base + off + k
-                off += ln
+                off += len(lab) - 1
         dev = dm.device
         self.rows = torch.tensor(rows, dtype=torch.int64, device=dev)
         self.targets = torch.tensor(targets, dtype=torch.int32, device=dev)
