@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define DBSA_ABI_VERSION 1
+#define DBSA_ABI_VERSION 2
 #define DBSA_PAGE_TOKENS 64
 
 /* Error codes -> reference exceptions (errors.py:4-29). */
@@ -136,6 +136,8 @@ typedef struct DbsaMergeArgs {
   int32_t n_heads, n_kv_heads, head_dim;
   void *out; /* bf16 */
   int64_t out_tok_stride;
+  int64_t split_stride; /* rows between split s and s+1 of a group; 0 = the group's `rows`
+                           (a gathered [world][R] partial buffer uses R: the C5 shard merge) */
 } DbsaMergeArgs;
 int dbsa_lse_merge(const DbsaMergeArgs *args, void *stream);
 

@@ -29,7 +29,7 @@ EXPORTED_SYMBOLS = (
     "dbsa_last_error",
 )
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 PAGE_TOKENS = 64
 SEG_FULL = 0
 SEG_SELF = 1
@@ -73,6 +73,7 @@ class MergeArgs(ctypes.Structure):
     _fields_ = [
         ("part_o", _vp), ("part_lse", _vp), ("groups", _vp), ("n_groups", _i32), ("max_rows", _i32),
         ("n_heads", _i32), ("n_kv_heads", _i32), ("head_dim", _i32), ("out", _vp), ("out_tok_stride", _i64),
+        ("split_stride", _i64),
     ]
 
 

@@ -510,13 +510,18 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
     // ------------------------------------------------------------ epilogue
     mbar_wait(&o_full[m], 0);
     tc_fence_after();
-    const float inv_l = l_sum > 0.f ? 1.f / l_sum : 0.f;
+    const bool empty = !(l_sum > 0.f);  // no visible key (e.g. a shard without chunks): O = 0, LSE = -inf
+    const float inv_l = empty ? 0.f : 1.f / l_sum;
     const int hd = p.head_dim;
 #pragma unroll 1
     for (int c0 = 0; c0 < HDP; c0 += 16) {
       float o[16];
       tmem_ld16(t_o + c0, o);
       tmem_wait_ld();
+      if (empty) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) o[i] = 0.f;
+      }
       if (valid && c0 < hd) {
         if (w.out_mode == 0) {
           __nv_bfloat16 *dst = p.out + (int64_t)t * p.out_tok_stride + (int64_t)head * hd + c0;

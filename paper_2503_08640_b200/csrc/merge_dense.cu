@@ -30,12 +30,13 @@ __global__ void lse_merge_kernel(DbsaMergeArgs a) {
   const int lane = threadIdx.x & 31;
   if (r >= g.rows) return;
   const int hd = a.head_dim, gs = a.n_heads / a.n_kv_heads;
+  const int64_t sstride = a.split_stride > 0 ? a.split_stride : g.rows;
   float mx = -INFINITY;
-  for (int s = lane; s < g.n_splits; s += 32) mx = fmaxf(mx, a.part_lse[g.part_row0 + (int64_t)s * g.rows + r]);
+  for (int s = lane; s < g.n_splits; s += 32) mx = fmaxf(mx, a.part_lse[g.part_row0 + (int64_t)s * sstride + r]);
   mx = warp_max(mx);
   float tot = 0.f;
   for (int s = lane; s < g.n_splits; s += 32) {
-    const float l = a.part_lse[g.part_row0 + (int64_t)s * g.rows + r];
+    const float l = a.part_lse[g.part_row0 + (int64_t)s * sstride + r];
     tot += l == -INFINITY ? 0.f : __expf(l - mx);
   }
   tot = warp_sum(tot);
@@ -45,10 +46,10 @@ __global__ void lse_merge_kernel(DbsaMergeArgs a) {
   for (int d0 = 0; d0 < hd; d0 += 32 * 4) {
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
     for (int s = 0; s < g.n_splits; ++s) {
-      const float l = a.part_lse[g.part_row0 + (int64_t)s * g.rows + r];
+      const float l = a.part_lse[g.part_row0 + (int64_t)s * sstride + r];
       if (l == -INFINITY) continue;
       const float wgt = __expf(l - mx) * inv;
-      const float *src = a.part_o + (g.part_row0 + (int64_t)s * g.rows + r) * hd;
+      const float *src = a.part_o + (g.part_row0 + (int64_t)s * sstride + r) * hd;
       if ((hd & 3) == 0 && d0 + lane * 4 + 3 < hd) {
         const float4 v = *reinterpret_cast<const float4 *>(src + d0 + lane * 4);
         acc[0] += wgt * v.x;

@@ -263,10 +263,11 @@ class _Scratch:
         self.act = torch.empty((min(n_tok, self.ffn_chunk), c.ffn_dim), dtype=torch.bfloat16, device=dev)
 
 
-def _decoder(dm, ids_dev, attend, write_kv, n_layers=None):
-    """Pre-norm decoder body (model.py:319-359) over n new tokens.  `write_kv(l,
-    qkv)` stores the layer's keys/values, `attend(l, qkv, out)` fills the
-    attention output.  Returns the fp32 final hidden states."""
+def _decoder_gen(dm, ids_dev, attend, write_kv, n_layers=None):
+    """Pre-norm decoder body (model.py:319-359) over n new tokens, as a
+    generator: it yields after each layer's `write_kv(l, qkv)` (the point where
+    a multi-shard caller exchanges pages) and returns the fp32 final hidden
+    states.  `attend(l, qkv, out)` fills the attention output."""
     torch = _torch()
     c = dm.config
     n = ids_dev.shape[0]
@@ -278,6 +279,7 @@ def _decoder(dm, ids_dev, attend, write_kv, n_layers=None):
         ops.rmsnorm(h, lw["attn_norm"], c.norm_eps, out=s.x)
         torch.mm(s.x, lw["wqkv"], out=s.qkv)
         write_kv(layer, s.qkv)
+        yield layer
         attend(layer, s.qkv, s.att)
         mm_f32(s.att, lw["wo"], s.proj)
         h.add_(s.proj)
@@ -292,6 +294,18 @@ def _decoder(dm, ids_dev, attend, write_kv, n_layers=None):
     return h
 
 
+def _drain(gen):
+    try:
+        while True:
+            next(gen)
+    except StopIteration as e:
+        return e.value
+
+
+def _decoder(dm, ids_dev, attend, write_kv, n_layers=None):
+    return _drain(_decoder_gen(dm, ids_dev, attend, write_kv, n_layers))
+
+
 # ============================================================== stage 1 (K1 + K2w)
 class Stage1Plan:
     """Device tables of one layer-synchronous stage-1 encode of groups
@@ -300,8 +314,13 @@ class Stage1Plan:
     def __init__(self, dm, cache, new, pattern):
         c = dm.config
         gs, hkv = c.group_size, c.n_kv_heads
-        self.tok_base = new[0].pos_start
-        self.n_tok = new[-1].pos_end - self.tok_base
+        # token buffer = the listed groups' tokens back to back (groups need not be contiguous)
+        local_of = {}
+        acc = 0
+        for e in new:
+            local_of[e.block_id] = acc
+            acc += e.token_count
+        self.n_tok = acc
         longest = max(e.token_count for e in new)
         self.num_m = 2 if longest * gs > 128 else 1
         slab = (128 * self.num_m) // gs
@@ -312,7 +331,7 @@ class Stage1Plan:
         for e in new:
             ctx = [cache.blocks[j] for j in pattern.context_of(e.block_id)]
             n_ctx = sum(x.token_count for x in ctx)
-            local0 = e.pos_start - self.tok_base
+            local0 = local_of[e.block_id]
             t = e.token_count
             pairs += n_ctx * t + t * (t + 1) // 2
             for t0 in range(0, t, slab):
@@ -337,19 +356,21 @@ class Stage1Plan:
         dev = dm.device
         self.works = ops.to_device(_work_array([w[1:] for w in works]), dev)
         self.segs = ops.to_device(_per_layer_segs(_seg_array(segs), c.n_layers), dev)
-        pages = _pages_for([(e.pos_start - self.tok_base, e.token_count, e.row0) for e in new])
+        pages = _pages_for([(local_of[e.block_id], e.token_count, e.row0) for e in new])
         self.n_pages = len(pages)
         self.pages = ops.to_device(pages, dev)
         torch = _torch()
-        self.pos = torch.arange(self.tok_base, self.tok_base + self.n_tok, dtype=torch.int32, device=dev)
+        pos = np.concatenate([np.arange(e.pos_start, e.pos_end, dtype=np.int32) for e in new])
+        self.pos = torch.from_numpy(pos).to(dev, non_blocking=True)
 
     def segs_ptr(self, layer: int) -> int:
         return self.segs.data_ptr() + layer * self.n_segs * ops.SEG_DTYPE.itemsize
 
 
-def encode_groups(dm, cache, new, ids, pattern, layers=None) -> int:
-    """Stage 1 for groups `new` whose concatenated token ids are `ids`; writes
-    their pages in every layer.  Returns the attended pair count
+def encode_groups_gen(dm, cache, new, ids, pattern, layers=None):
+    """Stage 1 for groups `new` (BlockEntry list) whose concatenated token ids
+    are `ids`, as a generator pausing after each layer's page write (see
+    _decoder_gen).  Returns the attended pair count of these groups
     (pipeline.py:231-232)."""
     torch = _torch()
     c = dm.config
@@ -369,8 +390,57 @@ def encode_groups(dm, cache, new, ids, pattern, layers=None) -> int:
                       works_dev=plan.works, n_works=plan.n_works, segs_dev=plan.segs_ptr(layer), num_m=plan.num_m,
                       out=out, out_tok_stride=qw)
 
-    _decoder(dm, ids_dev, attend, write_kv, n_layers=layers)
+    yield from _decoder_gen(dm, ids_dev, attend, write_kv, n_layers=layers)
     return plan.pairs
+
+
+def encode_groups(dm, cache, new, ids, pattern, layers=None) -> int:
+    """Stage 1 for groups `new` on one device; returns attended pairs."""
+    return _drain(encode_groups_gen(dm, cache, new, ids, pattern, layers))
+
+
+def encode_pool_sharded(dm, blocks, pattern, comm, device=None):
+    """Group-sharded stage 1: the groups are split into
+    contiguous ranges, every rank re-encodes the sink, and per layer the K/V
+    pages its successors need travel as a halo (parallel.exchange_pages).
+
+    blocks: [(token ids, sha256 digest, demo spans)] of the whole pool.
+    Returns ({local rank: SegmentedKVCache holding that rank's groups, the sink
+    and its halo}, attended pairs of the local ranks' own groups, ranges).
+    """
+    from . import parallel
+    from .kvstore import SegmentedKVCache
+
+    c = dm.config
+    counts = [len(ids) for ids, _, _ in blocks]
+    n_blocks = len(blocks)
+    ranges = parallel.plan_group_shards(counts, comm.world)
+    halo = parallel.halo_plan(pattern, ranges, n_blocks)
+    caches, gens = {}, {}
+    for r in comm.local_ranks:
+        present = parallel.local_groups(pattern, ranges, r, n_blocks)
+        cache = SegmentedKVCache(c, device or dm.device, capacity_tokens=sum(counts[g] for g in present))
+        cache._reserve_subset(counts, [d for _, d, _ in blocks], [sp for _, _, sp in blocks], present)
+        compute = sorted({0} | set(range(*ranges[r])))
+        new = [cache.blocks[g] for g in compute]
+        ids = np.concatenate([np.asarray(blocks[g][0], np.int64) for g in compute])
+        caches[r] = cache
+        gens[r] = encode_groups_gen(dm, cache, new, ids, pattern)
+    pairs = {}
+    stores = {r: caches[r].store for r in caches}
+    entries = {r: {e.block_id: e for e in caches[r].blocks if e.row0 >= 0} for r in caches}
+    for layer in range(c.n_layers):
+        for r in caches:
+            next(gens[r])
+        parallel.exchange_pages(comm, layer, halo, stores, entries)
+    for r in caches:
+        pairs[r] = _drain(gens[r])
+        if r != 0:  # the sink's own pairs are counted once, on rank 0
+            t0 = counts[0]
+            pairs[r] -= t0 * (t0 + 1) // 2
+    for cache in caches.values():
+        cache.seal()
+    return caches, pairs, ranges
 
 
 # ============================================================== stage 2 (K3 + K3m)
@@ -405,80 +475,26 @@ def label_job(chunks, n_ctx, query_ids, labels) -> QueryJob:
     return QueryJob(chunks, n_ctx, ids, pos, lo, nq, [list(x) for x in labels])
 
 
-class Stage2Plan:
-    """Device tables for a batch of QueryJobs."""
+class NewTokens:
+    """The new (query / label) tokens of a stage-2 batch: ids, rotary positions,
+    tree bounds and their K/V pages (one aux page set, page-aligned per job)."""
 
-    def __init__(self, dm, jobs, target_ctas: int | None = None, order: str = "query"):
+    def __init__(self, dm, jobs):
         torch = _torch()
         c = dm.config
-        gs, hkv, hd = c.group_size, c.n_kv_heads, c.head_dim
+        gs = c.group_size
         self.n_jobs = len(jobs)
-        n_new = [len(j.ids) for j in jobs]
-        self.tok0 = np.concatenate([[0], np.cumsum(n_new)]).astype(np.int64)
+        self.n_new = [len(j.ids) for j in jobs]
+        self.tok0 = np.concatenate([[0], np.cumsum(self.n_new)]).astype(np.int64)
         self.n_tok = int(self.tok0[-1])
-        self.num_m = 2 if max(n_new) * gs > 128 else 1
-        slab = (128 * self.num_m) // gs
-        if slab < 1:
+        self.num_m = 2 if max(self.n_new) * gs > 128 else 1
+        self.slab = (128 * self.num_m) // gs
+        if self.slab < 1:
             raise ConfigError(f"group size {gs} exceeds the 256 rows of one K3 work")
-        aux_rows = [_round_page(n) for n in n_new]
-        self.aux_row0 = np.concatenate([[0], np.cumsum(aux_rows)]).astype(np.int64)
+        self.slabs = [[(t0, min(self.slab, n - t0)) for t0 in range(0, n, self.slab)] for n in self.n_new]
+        self.aux_row0 = np.concatenate([[0], np.cumsum([_round_page(n) for n in self.n_new])]).astype(np.int64)
         self.aux_rows = int(self.aux_row0[-1])
-        n_sms = 148
-        target = target_ctas or 4 * n_sms
-        segs, works, merges, rots = [], [], [], []
-        part_rows = 0
-        kv_bytes = 0
-        for qi, j in enumerate(jobs):
-            n = n_new[qi]
-            slabs = [(t0, min(slab, n - t0)) for t0 in range(0, n, slab)]
-            ch = np.asarray(j.chunks, dtype=np.int64).reshape(-1, 3)
-            kv_bytes += int(ch[:, 1].sum()) if len(ch) else 0
-            n_split = max(1, min(len(ch), -(-target // max(1, len(jobs) * hkv * len(slabs)))))
-            bounds = _split_bounds(ch[:, 1] if len(ch) else np.zeros(0, np.int64), n_split)
-            chunk_segs = []
-            for row, cnt, delta in ch:
-                rot = -1
-                if delta != 0:
-                    rot = len(rots)
-                    rots.append(int(delta))
-                chunk_segs.append((0, 0, int(row), int(cnt), SEG_FULL, rot))
-            split_ranges = []
-            for s in range(n_split):
-                sb = len(segs)
-                segs += chunk_segs[bounds[s]:bounds[s + 1]]
-                split_ranges.append((sb, len(segs)))
-            q0 = int(self.tok0[qi])
-            for t0, nt in slabs:
-                rows = nt * gs
-                last_sb = len(segs)
-                segs += chunk_segs[bounds[n_split - 1]:bounds[n_split]]
-                segs.append((1, 0, int(self.aux_row0[qi]), t0 + nt, SEG_SELF, -1))
-                last = (last_sb, len(segs))
-                for kv in range(hkv):
-                    base = part_rows
-                    mode = 1 if n_split > 1 else 0
-                    for s in range(n_split):
-                        sb, se = last if s == n_split - 1 else split_ranges[s]
-                        works.append((q0 + t0, nt, q0, kv, sb, se, j.prefix, mode, base + s * rows))
-                    if n_split > 1:
-                        merges.append((base, rows, n_split, q0 + t0, kv))
-                        part_rows += n_split * rows
-        if order == "chunk":
-            # works whose first chunk is the same group run together: L2 reuse across queries
-            first_row = [segs[wk[4]][2] if segs[wk[4]][0] == 0 else 1 << 30 for wk in works]
-            idx = sorted(range(len(works)), key=lambda i: (first_row[i], works[i][3]))
-            works = [works[i] for i in idx]
-        self.kv_tokens = kv_bytes
-        self.n_works, self.n_segs, self.n_merge = len(works), len(segs), len(merges)
         dev = dm.device
-        self.works = ops.to_device(_work_array(works), dev)
-        self.segs = ops.to_device(_per_layer_segs(_seg_array(segs), c.n_layers), dev)
-        self.merges = ops.to_device(_merge_array(merges), dev) if merges else None
-        self.max_rows = max((m[1] for m in merges), default=0)
-        self.rot = (torch.from_numpy(ops.shift_table(rots, hd, c.rope_theta)).to(dev) if rots
-                    else torch.zeros((1, hd // 2, 2), dtype=torch.float32, device=dev))
-        self.part_o = torch.empty((max(part_rows, 1), hd), dtype=torch.float32, device=dev)
-        self.part_lse = torch.empty((max(part_rows, 1),), dtype=torch.float32, device=dev)
         pos = np.concatenate([np.asarray(j.pos, np.int64) + j.n_ctx for j in jobs]).astype(np.int32)
         lo = np.concatenate([np.asarray(j.lo, np.int64) for j in jobs]).astype(np.int32)
         ids = np.concatenate([np.asarray(j.ids, np.int64) for j in jobs])
@@ -487,15 +503,144 @@ class Stage2Plan:
         self.pos = torch.from_numpy(pos).to(dev, non_blocking=True)
         self.lo = torch.from_numpy(lo).to(dev, non_blocking=True)
         self.ids = torch.from_numpy(ids).to(dev, non_blocking=True)
-        self.pages = ops.to_device(_pages_for([(int(self.tok0[i]), n_new[i], int(self.aux_row0[i]))
+        self.pages = ops.to_device(_pages_for([(int(self.tok0[i]), self.n_new[i], int(self.aux_row0[i]))
                                                for i in range(len(jobs))]), dev)
-        self.n_pages = int(sum(-(-n // PAGE) for n in n_new))
-        hdp = ops.hd_pad(hd)
-        self.k_aux = torch.zeros((1, hkv, self.aux_rows, hdp), dtype=torch.bfloat16, device=dev)
-        self.v_aux = torch.zeros((1, hkv, hdp, self.aux_rows), dtype=torch.bfloat16, device=dev)
+        self.n_pages = int(sum(-(-n // PAGE) for n in self.n_new))
+        hdp = ops.hd_pad(c.head_dim)
+        self.k_aux = torch.zeros((1, c.n_kv_heads, self.aux_rows, hdp), dtype=torch.bfloat16, device=dev)
+        self.v_aux = torch.zeros((1, c.n_kv_heads, hdp, self.aux_rows), dtype=torch.bfloat16, device=dev)
+        # canonical partial layout (sharded mode): one row block per (job, slab, kv head)
+        self.part_base = []
+        base = 0
+        for qi in range(len(jobs)):
+            per = []
+            for t0, nt in self.slabs[qi]:
+                per.append(base)
+                base += nt * gs * c.n_kv_heads
+            self.part_base.append(per)
+        self.canon_rows = base
+
+    def aux(self):
+        return (self.k_aux, self.v_aux, self.aux_rows, 1)
+
+
+class AttnSchedule:
+    """K3 works + segments (+ K3m merge groups) of a batch against chunk tables.
+
+    mode "split": each (job, kv head, slab) is cut into splits over its chunks
+    (split-KV for parallelism); partials of multi-split works merge in place.
+    mode "canonical": exactly one work per (job, kv head, slab) that has any
+    key on this shard, always writing an fp32 partial + LSE at the canonical
+    row block (NewTokens.part_base) -- the per-rank half of the C5 merge.
+    include_self: whether this schedule covers the jobs' own tokens (SELF).
+    """
+
+    def __init__(self, dm, jobs, nt: NewTokens, chunk_tables=None, target_ctas=None, order="query",
+                 mode="split", include_self=True):
+        torch = _torch()
+        c = dm.config
+        gs, hkv, hd = c.group_size, c.n_kv_heads, c.head_dim
+        tables = chunk_tables if chunk_tables is not None else [j.chunks for j in jobs]
+        target = target_ctas or 4 * 148
+        segs, works, merges, rots = [], [], [], []
+        part_rows = 0 if mode == "split" else nt.canon_rows
+        kv_tok = 0
+        for qi, j in enumerate(jobs):
+            n = nt.n_new[qi]
+            slabs = nt.slabs[qi]
+            ch = np.asarray(tables[qi], dtype=np.int64).reshape(-1, 3)
+            kv_tok += int(ch[:, 1].sum()) if len(ch) else 0
+            chunk_segs = []
+            for row, cnt, delta in ch:
+                rot = -1
+                if delta != 0:
+                    rot = len(rots)
+                    rots.append(int(delta))
+                chunk_segs.append((0, 0, int(row), int(cnt), SEG_FULL, rot))
+            q0 = int(nt.tok0[qi])
+            if mode == "canonical":
+                if not chunk_segs and not include_self:
+                    continue
+                for si, (t0, ntk) in enumerate(slabs):
+                    rows = ntk * gs
+                    sb = len(segs)
+                    segs += chunk_segs
+                    if include_self:
+                        segs.append((1, 0, int(nt.aux_row0[qi]), t0 + ntk, SEG_SELF, -1))
+                    for kv in range(hkv):
+                        works.append((q0 + t0, ntk, q0, kv, sb, len(segs), j.prefix, 1,
+                                      nt.part_base[qi][si] + kv * rows))
+                continue
+            n_split = max(1, min(len(ch), -(-target // max(1, len(jobs) * hkv * len(slabs)))))
+            bounds = _split_bounds(ch[:, 1] if len(ch) else np.zeros(0, np.int64), n_split)
+            split_ranges = []
+            for sp in range(n_split - 1):
+                sb = len(segs)
+                segs += chunk_segs[bounds[sp]:bounds[sp + 1]]
+                split_ranges.append((sb, len(segs)))
+            for t0, ntk in slabs:
+                rows = ntk * gs
+                last_sb = len(segs)
+                segs += chunk_segs[bounds[n_split - 1]:bounds[n_split]]
+                if include_self:
+                    segs.append((1, 0, int(nt.aux_row0[qi]), t0 + ntk, SEG_SELF, -1))
+                last = (last_sb, len(segs))
+                for kv in range(hkv):
+                    base = part_rows
+                    mode_w = 1 if n_split > 1 else 0
+                    for sp in range(n_split):
+                        sb, se = last if sp == n_split - 1 else split_ranges[sp]
+                        works.append((q0 + t0, ntk, q0, kv, sb, se, j.prefix, mode_w, base + sp * rows))
+                    if n_split > 1:
+                        merges.append((base, rows, n_split, q0 + t0, kv))
+                        part_rows += n_split * rows
+        if order == "chunk":
+            first_row = [segs[wk[4]][2] if wk[5] > wk[4] and segs[wk[4]][0] == 0 else 1 << 30 for wk in works]
+            idx = sorted(range(len(works)), key=lambda i: (first_row[i], works[i][3]))
+            works = [works[i] for i in idx]
+        self.kv_tokens = kv_tok
+        self.n_works, self.n_segs, self.n_merge = len(works), len(segs), len(merges)
+        dev = dm.device
+        self.works = ops.to_device(_work_array(works), dev)
+        self.segs = ops.to_device(_per_layer_segs(_seg_array(segs), c.n_layers), dev)
+        self.merges = ops.to_device(_merge_array(merges), dev) if merges else None
+        self.max_rows = max((m[1] for m in merges), default=0)
+        self.rot = (torch.from_numpy(ops.shift_table(rots, hd, c.rope_theta)).to(dev) if rots
+                    else torch.zeros((1, hd // 2, 2), dtype=torch.float32, device=dev))
+        self.part_rows = part_rows
+        self.part_o = torch.empty((max(part_rows, 1), hd), dtype=torch.float32, device=dev)
+        self.part_lse = torch.empty((max(part_rows, 1),), dtype=torch.float32, device=dev)
 
     def segs_ptr(self, layer: int) -> int:
         return self.segs.data_ptr() + layer * self.n_segs * ops.SEG_DTYPE.itemsize
+
+    def launch(self, dm, nt: NewTokens, layer, qkv, out, pool, part_o=None, part_lse=None):
+        c = dm.config
+        qw, kw = c.n_heads * c.head_dim, c.n_kv_heads * c.head_dim
+        if self.n_works == 0:
+            return
+        ops.attention(q=qkv, q_tok_stride=qw + 2 * kw, tok_pos=nt.pos, tok_lo=nt.lo, rope=dm.rope, rot=self.rot,
+                      pool=pool, aux=nt.aux(), n_heads=c.n_heads, n_kv_heads=c.n_kv_heads, head_dim=c.head_dim,
+                      works_dev=self.works, n_works=self.n_works, segs_dev=self.segs_ptr(layer), num_m=nt.num_m,
+                      out=out, out_tok_stride=qw, part_o=self.part_o if part_o is None else part_o,
+                      part_lse=self.part_lse if part_lse is None else part_lse)
+
+
+class Stage2Plan:
+    """Single-device tables for a batch of QueryJobs: NewTokens + a split-KV
+    AttnSchedule over the jobs' chunk tables."""
+
+    def __init__(self, dm, jobs, target_ctas: int | None = None, order: str = "query"):
+        self.new = NewTokens(dm, jobs)
+        self.sched = AttnSchedule(dm, jobs, self.new, target_ctas=target_ctas, order=order)
+        for name in ("tok0", "n_tok", "num_m", "pos", "lo", "ids", "pages", "n_pages", "k_aux", "v_aux", "aux_rows"):
+            setattr(self, name, getattr(self.new, name))
+        for name in ("works", "n_works", "n_segs", "n_merge", "merges", "max_rows", "rot", "part_o", "part_lse",
+                     "kv_tokens"):
+            setattr(self, name, getattr(self.sched, name))
+
+    def segs_ptr(self, layer: int) -> int:
+        return self.sched.segs_ptr(layer)
 
 
 def _split_bounds(counts: np.ndarray, n_split: int) -> list[int]:
@@ -526,26 +671,111 @@ def run_jobs(dm, store, jobs, target_ctas=None, plan=None):
     """Forward every job's new tokens; returns (plan, fp32 hidden [n_tok, d])."""
     c = dm.config
     plan = plan or Stage2Plan(dm, jobs, target_ctas)
+    nt, sched = plan.new, plan.sched
     qw, kw = c.n_heads * c.head_dim, c.n_kv_heads * c.head_dim
     stride = qw + 2 * kw
-    pool = store.planes() if store is not None and store.k is not None else (plan.k_aux, plan.v_aux, plan.aux_rows, 1)
-    aux = (plan.k_aux, plan.v_aux, plan.aux_rows, 1)
+    pool = store.planes() if store is not None and store.k is not None else nt.aux()
 
     def write_kv(layer, qkv):
-        ops.kv_write(qkv[:, qw:], qkv[:, qw + kw:], stride, plan.pos, dm.rope, plan.pages, plan.n_pages,
-                     plan.k_aux, plan.v_aux, plan.aux_rows, 1, 0, c.n_kv_heads, c.head_dim)
+        ops.kv_write(qkv[:, qw:], qkv[:, qw + kw:], stride, nt.pos, dm.rope, nt.pages, nt.n_pages, nt.k_aux,
+                     nt.v_aux, nt.aux_rows, 1, 0, c.n_kv_heads, c.head_dim)
 
     def attend(layer, qkv, out):
-        ops.attention(q=qkv, q_tok_stride=stride, tok_pos=plan.pos, tok_lo=plan.lo, rope=dm.rope, rot=plan.rot,
-                      pool=pool, aux=aux, n_heads=c.n_heads, n_kv_heads=c.n_kv_heads, head_dim=c.head_dim,
-                      works_dev=plan.works, n_works=plan.n_works, segs_dev=plan.segs_ptr(layer), num_m=plan.num_m,
-                      out=out, out_tok_stride=qw, part_o=plan.part_o, part_lse=plan.part_lse)
-        if plan.n_merge:
-            ops.lse_merge(plan.part_o, plan.part_lse, plan.merges, plan.n_merge, plan.max_rows, c.n_heads,
+        sched.launch(dm, nt, layer, qkv, out, pool)
+        if sched.n_merge:
+            ops.lse_merge(sched.part_o, sched.part_lse, sched.merges, sched.n_merge, sched.max_rows, c.n_heads,
                           c.n_kv_heads, c.head_dim, out, qw)
 
-    h = _decoder(dm, plan.ids, attend, write_kv)
+    h = _decoder(dm, nt.ids, attend, write_kv)
     return plan, h
+
+
+def shard_chunk_table(cache, units, ranges, rank):
+    """(row, n_tok, delta) of the units of one query owned by `rank`, with
+    GLOBAL new positions (all units count toward the re-positioned context)."""
+    from . import parallel
+
+    rows, new_start = [], 0
+    for b, s0, e0 in units:
+        n = e0 - s0
+        if parallel.owner_of(b, ranges) == rank:
+            ent = cache.blocks[b]
+            rows.append((ent.row0 + s0, n, new_start - (ent.pos_start + s0)))
+        new_start += n
+    return np.asarray(rows, dtype=np.int64).reshape(-1, 3), new_start
+
+
+class ShardedStage2:
+    """C5 stage 2 over a group-sharded cache: per layer every rank computes
+    canonical (O, LSE) partials over its own chunks (rank `self_rank` also over
+    the new tokens), the partials are all-gathered and merged by K3m."""
+
+    def __init__(self, dm, caches, comm, ranges, units_per_query, query_ids, labels, self_rank=0):
+        torch = _torch()
+        c = dm.config
+        self.dm, self.caches, self.comm, self.ranges = dm, caches, comm, ranges
+        any_cache = next(iter(caches.values()))
+        tables = {r: [] for r in caches}
+        jobs = []
+        for q, units in zip(query_ids, units_per_query):
+            n_ctx = 0
+            for r in caches:
+                tab, n_ctx = shard_chunk_table(caches[r], units, ranges, r)
+                tables[r].append(tab)
+            if not caches:
+                n_ctx = sum(e - s for _, s, e in units)
+            jobs.append(label_job(np.zeros((0, 3), np.int64), n_ctx, q, labels))
+        del any_cache
+        self.jobs = jobs
+        self.nt = NewTokens(dm, jobs)
+        self.scheds = {r: AttnSchedule(dm, jobs, self.nt, chunk_tables=tables[r], mode="canonical",
+                                       include_self=(r == self_rank)) for r in caches}
+        gs, hkv = c.group_size, c.n_kv_heads
+        merges = []
+        for qi in range(len(jobs)):
+            q0 = int(self.nt.tok0[qi])
+            for si, (t0, ntk) in enumerate(self.nt.slabs[qi]):
+                rows = ntk * gs
+                for kv in range(hkv):
+                    merges.append((self.nt.part_base[qi][si] + kv * rows, rows, comm.world, q0 + t0, kv))
+        self.merges = ops.to_device(_merge_array(merges), dm.device)
+        self.n_merge = len(merges)
+        self.max_rows = max(m[1] for m in merges)
+        R = self.nt.canon_rows
+        self.R = R
+        n_local = len(caches)
+        self.part_o = torch.empty((n_local, R, c.head_dim), dtype=torch.float32, device=dm.device)
+        self.part_lse = torch.empty((n_local, R), dtype=torch.float32, device=dm.device)
+
+    def forward(self):
+        c = self.dm.config
+        nt = self.nt
+        qw, kw = c.n_heads * c.head_dim, c.n_kv_heads * c.head_dim
+        stride = qw + 2 * kw
+        ranks = list(self.caches)
+
+        def write_kv(layer, qkv):
+            ops.kv_write(qkv[:, qw:], qkv[:, qw + kw:], stride, nt.pos, self.dm.rope, nt.pages, nt.n_pages,
+                         nt.k_aux, nt.v_aux, nt.aux_rows, 1, 0, c.n_kv_heads, c.head_dim)
+
+        def attend(layer, qkv, out):
+            self.part_lse.fill_(-float("inf"))
+            for i, r in enumerate(ranks):
+                self.scheds[r].launch(self.dm, nt, layer, qkv, out, self.caches[r].store.planes(),
+                                      part_o=self.part_o[i], part_lse=self.part_lse[i])
+            if len(ranks) == self.comm.world:
+                go, gl = self.part_o, self.part_lse  # all shards are local: already [world, R, ...]
+            else:
+                go = self.comm.all_gather([self.part_o[0]])
+                gl = self.comm.all_gather([self.part_lse[0]])
+            ops.lse_merge(go, gl, self.merges, self.n_merge, self.max_rows, c.n_heads, c.n_kv_heads, c.head_dim,
+                          out, qw, split_stride=self.R)
+
+        return _decoder(self.dm, nt.ids, attend, write_kv)
+
+    def scores(self):
+        h = self.forward()
+        return LabelScorer(self.dm, self.nt, self.jobs, len(self.jobs[0].labels))(self.dm, h)
 
 
 def _final_logits(dm, h_rows):

@@ -106,6 +106,21 @@ class SegmentedKVCache:
         self.blocks.extend(new)
         return new
 
+    def _reserve_subset(self, counts, digests, spans_list, present) -> list[BlockEntry]:
+        """Metadata for every group, pages only for the groups in `present`
+        (a group-sharded cache, parallel.py); absent groups get row0 = -1."""
+        if self.sealed or self.blocks:
+            raise ValidationError("a sharded cache is reserved once, empty")
+        present = set(int(g) for g in present)
+        rows = iter(self.store.reserve([int(counts[g]) for g in sorted(present)]))
+        row_of = {g: next(rows) for g in sorted(present)}
+        start = 0
+        for g, (n, dg, sp) in enumerate(zip(counts, digests, spans_list)):
+            n = int(n)
+            self.blocks.append(BlockEntry(g, n, start, start + n, bytes(dg), _check_spans(sp, n), row_of.get(g, -1)))
+            start += n
+        return self.blocks
+
     def append_block(self, block_id: int, pre_rotation_kv, text_digest: bytes,
                      example_spans: tuple[tuple[int, int], ...] = ()) -> "SegmentedKVCache":
         """Append one group's host pre-rotation K/V (kvstore.py:70-106): the
@@ -132,6 +147,8 @@ class SegmentedKVCache:
         """(pre-rotation K, V) float32 (T, Hkv, hd) of one group, read back from
         the pages and un-rotated on the host (cold path)."""
         e = self.blocks[block_id]
+        if e.row0 < 0:
+            raise ValidationError(f"group {block_id} is held by another shard")
         k_rot, v = self.store.read_rows(layer, e.row0, e.token_count)
         pos = np.arange(e.pos_start, e.pos_end, dtype=np.int64)
         return model.rope_rotate_heads(k_rot, -pos, self.config.rope_theta), v

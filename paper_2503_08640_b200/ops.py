@@ -123,10 +123,11 @@ def attention(*, q, q_tok_stride, tok_pos, tok_lo, rope, rot, pool, aux, n_heads
 
 
 def lse_merge(part_o, part_lse, groups_dev, n_groups, max_rows, n_heads, n_kv_heads, head_dim, out,
-              out_tok_stride):
+              out_tok_stride, split_stride=0):
     a = nat.MergeArgs(part_o=part_o.data_ptr(), part_lse=part_lse.data_ptr(), groups=groups_dev.data_ptr(),
                       n_groups=n_groups, max_rows=max_rows, n_heads=n_heads, n_kv_heads=n_kv_heads,
-                      head_dim=head_dim, out=out.data_ptr(), out_tok_stride=out_tok_stride)
+                      head_dim=head_dim, out=out.data_ptr(), out_tok_stride=out_tok_stride,
+                      split_stride=split_stride)
     nat.check(nat.load_library().dbsa_lse_merge(ctypes.byref(a), nat.stream_handle()))
     _launched()
 
