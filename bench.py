@@ -215,17 +215,42 @@ def run_ours(args):
         s1_times.append(a.elapsed_time(b))
     cache.seal()
     s1_ms = s1_times[-1]
+    s1_mode = "single GPU"
+    if world > 1:
+        # group-sharded stage 1 with the per-layer NCCL halo (parallel.py); the
+        # replicated cache above stays the stage-2 cache (query data-parallel)
+        from paper_2503_08640_b200 import parallel
+
+        try:
+            comm = parallel.DistComm()
+            sh_ms = []
+            for it in range(2):
+                dist.barrier()
+                torch.cuda.synchronize()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                _, sh_pairs, _ = engine.encode_pool_sharded(dm, blocks, pattern, comm)
+                b.record()
+                torch.cuda.synchronize()
+                sh_ms.append(a.elapsed_time(b))
+            t = torch.tensor([sh_ms[-1]], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            s1_ms = float(t.item())
+            s1_mode = f"group-sharded over {world} GPUs, NCCL halo per layer"
+        except Exception as exc:  # keep the stage-2 measurement if the sharded path fails
+            s1_mode = f"replicated (sharded stage 1 failed: {type(exc).__name__}: {exc})"
     hbm, tf_burst, tf_sus, peak_src = peaks()
     k1_ms = k1.mean_ms()
     k1_flops = pairs * 4 * cfg.head_dim * cfg.n_heads  # one layer (metrics.py:21-22)
     stage1 = {"metric": "stage-1 pre-encode tok/s", "value": N_GROUPS * GROUP_TOK / (s1_ms / 1e3), "unit": "tok/s",
-              "ms": s1_ms, "pool_tokens": N_GROUPS * GROUP_TOK, "attended_pairs": pairs,
+              "ms": s1_ms, "pool_tokens": N_GROUPS * GROUP_TOK, "attended_pairs": pairs, "mode": s1_mode,
               "roofline": {"kernel": "dbsa_attn_kernel (K1)", "bound": "tensor",
                            "achieved": k1_flops / (k1_ms / 1e3) / 1e12 if k1_ms else None,
                            "peak": tf_burst, "unit": "TFLOP/s",
                            "frac": (k1_flops / (k1_ms / 1e3) / 1e12) / tf_burst if k1_ms else None,
                            "traffic": traffic_for("k1", "c2"), "launch_ms": k1_ms,
-                           "flops_per_launch": k1_flops, "share_of_step": (k1_ms * cfg.n_layers) / s1_ms,
+                           "flops_per_launch": k1_flops,
+                           "share_of_step": (k1_ms * cfg.n_layers) / s1_times[-1] if k1_ms else None,
                            "peak_source": peak_src}}
 
     # ---------------- stage 2 (C3 at 30 %)

@@ -149,6 +149,8 @@ class DistComm:
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self.local_ranks = [self.rank]
+        # a collective every rank joins, before any batched P2P (NCCL requirement)
+        dist.barrier(group=group)
 
     def exchange(self, sends, recv_like=None):
         """Point-to-point halo exchange.  sends: {(src, dst, key): tensor} for
