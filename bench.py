@@ -322,6 +322,48 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
 
+    # ---------------- batch-1 latency (the paper's setting) and the
+    # dense comparator: K3 over ONE contiguous run of T' pool rows vs the same
+    # queries over their selected chunks (north-star target: within 10 %).
+    extra = {}
+    if not args.no_extras:
+        lat = []
+        for s_i in range(3 + 5):
+            q, sc = synth_queries(1, seed=555000 + s_i)
+            torch.cuda.synchronize()
+            e0b, e1b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0b.record()
+            _, _, best1 = sess.answer(sc, q)
+            best1.cpu()
+            e1b.record()
+            torch.cuda.synchronize()
+            lat.append(e0b.elapsed_time(e1b))
+        extra["latency_b1_ms"] = float(np.median(lat[3:]))
+        st0 = steps[W]
+        jobs0, plan0c = st0[3], st0[4]
+        Tp = sess.budget * GROUP_TOK
+        dense_jobs = [engine.label_job(np.array([[0, Tp, 0]], np.int64), Tp, q_, sess.label_ids) for q_ in st0[0]]
+        plan_d = engine.Stage2Plan(dm, dense_jobs)
+        qkv = torch.randn(plan0c.n_tok, cfg.n_heads * cfg.head_dim + 2 * cfg.n_kv_heads * cfg.head_dim,
+                          device=dev).to(torch.bfloat16)
+        att = torch.empty(plan0c.n_tok, cfg.n_heads * cfg.head_dim, dtype=torch.bfloat16, device=dev)
+
+        def time_k3(plan_x, reps=5):
+            plan_x.sched.launch(dm, plan_x.new, 0, qkv, att, cache.store.planes())
+            torch.cuda.synchronize()
+            a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_.record()
+            for _ in range(reps):
+                plan_x.sched.launch(dm, plan_x.new, 0, qkv, att, cache.store.planes())
+            b_.record()
+            torch.cuda.synchronize()
+            return a_.elapsed_time(b_) / reps
+
+        t_sel, t_dense = time_k3(plan0c), time_k3(plan_d)
+        extra["dense_comparator"] = {"k3_selected_chunks_ms": t_sel, "k3_dense_contiguous_ms": t_dense,
+                                     "ratio": t_sel / t_dense,
+                                     "note": f"same {B} queries, T'={Tp}: {sess.budget} chunks vs one contiguous run"}
+
     # roofline of K3 (dominant stage-2 kernel): algorithmic bytes per launch =
     # selected KV (2 * Hkv * hd * 2 B per token, one layer) + Q in + O out.
     plan0 = steps[W][4]
@@ -348,6 +390,7 @@ def run_ours(args):
                      "share_of_step": (k3_ms * cfg.n_layers) / (dev_ms / K) if k3_ms else None,
                      "peak_source": peak_src},
         "stage1": stage1,
+        **extra,
         "gpu_launches": launches,
         "clocks": clocks,
     }
@@ -456,6 +499,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the batch-1 latency and dense-comparator probes")
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--ratio", type=float, default=0.30)
     args = ap.parse_args()

@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define DBSA_ABI_VERSION 2
+#define DBSA_ABI_VERSION 3
 #define DBSA_PAGE_TOKENS 64
 
 /* Error codes -> reference exceptions (errors.py:4-29). */
@@ -78,7 +78,8 @@ typedef struct DbsaAttnSeg {
   int32_t row0;  /* first row */
   int32_t n_tok; /* > 0 */
   int32_t kind;  /* DBSA_SEG_FULL / DBSA_SEG_SELF */
-  int32_t rot;   /* row of rot_table applied to the queries, -1 = none */
+  int32_t shift; /* stage-2 re-positioning delta = new start - original start of the
+                    chunk: the rows' queries use rope row (tok_pos - shift); 0 = none */
   int32_t pad0, pad1;
 } DbsaAttnSeg;
 
@@ -87,18 +88,19 @@ typedef struct DbsaAttnSeg {
  * kernels.masked_attention (kernels.py:73-100) as called from
  * model._forward (model.py:327-351) including the rotary application of
  * model.py:327-328: queries are read UNROTATED from `q` and rotated in the
- * prologue at tok_pos[t] (rope_table), composed with the per-segment shift
- * rot_table[seg.rot] (the stage-2 re-positioning of kvstore.py:201-218 moved
- * to the query side: R(p_q - delta) q . R(p_orig) k == R(p_q) q . R(p_new) k).
+ * prologue with rope_table row (tok_pos[t] - seg.shift): the stage-2
+ * re-positioning of kvstore.py:201-218 moved to the query side,
+ * R(p_q - delta) q . R(p_orig) k == R(p_q) q . R(p_new) k, with the rotation
+ * angle formed in float64 for the exact integer position p_q - delta.
  */
 typedef struct DbsaAttnArgs {
   const void *q;        /* bf16, element (t, head, d) at q[t*q_tok_stride + head*head_dim + d] */
   int64_t q_tok_stride; /* elements */
   const int32_t *tok_pos; /* [tokens] rotary position of each query token */
   const int32_t *tok_lo;  /* [tokens] tree mask: lowest visible non-prefix SELF key (local); NULL = 0 */
-  const float *rope_table; /* float2 [rope_rows][head_dim/2]: cos, sin of pos*theta^(-2i/hd) */
+  const float *rope_table; /* float2 [rope_rows][head_dim/2]: cos, sin of pos*theta^(-2i/hd);
+                              rows must cover every tok_pos - shift */
   int64_t rope_rows;
-  const float *rot_table;  /* float2 [n_rot][head_dim/2]: cos, sin of (-delta)*theta^(-2i/hd) */
   const void *k_pool, *v_pool; /* bf16 planes, see layout above */
   int64_t pool_rows;
   int32_t pool_layers;
@@ -177,6 +179,15 @@ int dbsa_rope_table(float *table, int64_t rows, const double *inv_freq, int32_t 
  * retrieval.select + retrieval.order (retrieval.py:352-388). */
 int dbsa_topk_select(const double *scores, int64_t n_queries, int64_t n_units, int64_t budget,
                      int32_t ordering, int32_t *out_ids, void *stream);
+
+/* GPU BM25: out[q][u] = sum over the query's term ids
+ * (row q of term_ids, -1 = skip) of idf[t] * tf[t][u] * k1p1 / (tf[t][u] + norm[u]),
+ * float64 in query-term order without FMA contraction -- bit-identical to
+ * Bm25Index.score (retrieval.py:129-141) given the host's idf / norm.  tf is a
+ * dense uint16 [n_terms][n_units] matrix. */
+int dbsa_bm25_scores(const int32_t *term_ids, int64_t n_queries, int32_t max_terms, const uint16_t *tf,
+                     const double *idf, const double *norm, int64_t n_units, double k1p1, double *out,
+                     void *stream);
 
 /* Dense-path helpers fused for the pre-norm block (model.py:321,355,358;
  * kernels.py:103-123): RMSNorm fp32 -> bf16, and silu(gate) * up. */

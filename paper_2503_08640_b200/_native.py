@@ -25,11 +25,12 @@ EXPORTED_SYMBOLS = (
     "dbsa_rmsnorm",
     "dbsa_silu_mul",
     "dbsa_label_logprob",
+    "dbsa_bm25_scores",
     "dbsa_abi_version",
     "dbsa_last_error",
 )
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 PAGE_TOKENS = 64
 SEG_FULL = 0
 SEG_SELF = 1
@@ -48,14 +49,14 @@ class AttnWork(ctypes.Structure):
 class AttnSeg(ctypes.Structure):
     _fields_ = [
         ("src", _i32), ("layer", _i32), ("row0", _i32), ("n_tok", _i32),
-        ("kind", _i32), ("rot", _i32), ("pad0", _i32), ("pad1", _i32),
+        ("kind", _i32), ("shift", _i32), ("pad0", _i32), ("pad1", _i32),
     ]
 
 
 class AttnArgs(ctypes.Structure):
     _fields_ = [
         ("q", _vp), ("q_tok_stride", _i64), ("tok_pos", _vp), ("tok_lo", _vp),
-        ("rope_table", _vp), ("rope_rows", _i64), ("rot_table", _vp),
+        ("rope_table", _vp), ("rope_rows", _i64),
         ("k_pool", _vp), ("v_pool", _vp), ("pool_rows", _i64), ("pool_layers", _i32),
         ("k_aux", _vp), ("v_aux", _vp), ("aux_rows", _i64), ("aux_layers", _i32),
         ("n_heads", _i32), ("n_kv_heads", _i32), ("head_dim", _i32), ("hd_pad", _i32),
@@ -129,6 +130,7 @@ def load_library(path: Path | str | None = None) -> ctypes.CDLL:
         lib.dbsa_rmsnorm.argtypes = [_vp, _vp, _vp, _i64, _i64, _f32, _vp]
         lib.dbsa_silu_mul.argtypes = [_vp, _vp, _i64, _i64, _vp]
         lib.dbsa_label_logprob.argtypes = [_vp, _i64, _i64, _vp, _vp, _vp]
+        lib.dbsa_bm25_scores.argtypes = [_vp, _i64, _i32, _vp, _vp, _vp, _i64, ctypes.c_double, _vp, _vp]
         for name in EXPORTED_SYMBOLS[:-2]:
             getattr(lib, name).restype = ctypes.c_int
         if lib.dbsa_abi_version() != ABI_VERSION:

@@ -74,7 +74,6 @@ struct AttnParams {
   const int32_t *tok_lo;
   const float2 *rope;
   int64_t rope_rows;
-  const float2 *rot;
   int32_t n_heads, n_kv_heads, head_dim, gs;
   float scale_log2;
   const DbsaAttnWork *works;
@@ -117,7 +116,7 @@ __device__ __forceinline__ float fast_exp2(float x) {
 // use so one row costs a few memory round trips, not one per element.
 template <int HDP>
 __device__ __forceinline__ void load_q_row(const AttnParams &p, uint8_t *q_tile, int row, bool valid,
-                                           int t, int head, int rot) {
+                                           int t, int head, int shift) {
   constexpr int QSW = AttnCfg<HDP, 1>::QSW;
   const int hd = p.head_dim, half = hd >> 1;
   auto put = [&](int c, const float (&o)[8]) {
@@ -132,48 +131,39 @@ __device__ __forceinline__ void load_q_row(const AttnParams &p, uint8_t *q_tile,
     return;
   }
   const __nv_bfloat16 *src = p.q + (int64_t)t * p.q_tok_stride + (int64_t)head * hd;
-  const float2 *rp = p.rope + (int64_t)p.tok_pos[t] * half;
-  const float2 *rr = rot >= 0 ? p.rot + (int64_t)rot * half : nullptr;
+  const float2 *rp = p.rope + (int64_t)(p.tok_pos[t] - shift) * half;
   if (HDP >= 32 && hd == HDP && (p.q_tok_stride & 7) == 0) {
-    // fast path: full-width head, every 8-element chunk lies in one half, 16-byte aligned rows
+    // fast path: full-width head, every 8-element chunk lies in one half, 16-byte
+    // aligned rows.  Two passes, each issuing all of its loads before any use.
+    constexpr int NCH = HDP / 16;           // 8-pair chunks per half
+    constexpr int PASS = NCH >= 4 ? NCH / 2 : NCH;
 #pragma unroll
-    for (int c0 = 0; c0 < HDP / 16; c0 += 2) {
-      uint4 lo4[2], hi4[2];
-      float4 cs4[2][4], rr4[2][4];
+    for (int c0 = 0; c0 < NCH; c0 += PASS) {
+      uint4 lo4[PASS], hi4[PASS];
+      float4 cs4[PASS][4];
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < PASS; ++u) {
         const int i0 = (c0 + u) * 8;  // pair index of this chunk
         lo4[u] = *reinterpret_cast<const uint4 *>(src + i0);
         hi4[u] = *reinterpret_cast<const uint4 *>(src + half + i0);
 #pragma unroll
         for (int v = 0; v < 4; ++v) cs4[u][v] = reinterpret_cast<const float4 *>(rp + i0)[v];
-        if (rr) {
-#pragma unroll
-          for (int v = 0; v < 4; ++v) rr4[u][v] = reinterpret_cast<const float4 *>(rr + i0)[v];
-        }
       }
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < PASS; ++u) {
         const __nv_bfloat16 *lo = reinterpret_cast<const __nv_bfloat16 *>(&lo4[u]);
         const __nv_bfloat16 *hi = reinterpret_cast<const __nv_bfloat16 *>(&hi4[u]);
         const float *cs = reinterpret_cast<const float *>(cs4[u]);
-        const float *dd = reinterpret_cast<const float *>(rr4[u]);
         float a[8], b[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          float c = cs[2 * j], sn = cs[2 * j + 1];
-          if (rr) {
-            const float dc = dd[2 * j], ds = dd[2 * j + 1];
-            const float c2 = c * dc - sn * ds;
-            sn = sn * dc + c * ds;
-            c = c2;
-          }
+          const float c = cs[2 * j], sn = cs[2 * j + 1];
           const float x = __bfloat162float(lo[j]), y = __bfloat162float(hi[j]);
           a[j] = x * c - y * sn;
           b[j] = x * sn + y * c;
         }
         put(c0 + u, a);
-        put(HDP / 16 + c0 + u, b);
+        put(NCH + c0 + u, b);
       }
     }
     return;
@@ -189,11 +179,7 @@ __device__ __forceinline__ void load_q_row(const AttnParams &p, uint8_t *q_tile,
         const int i = e < half ? e : e - half;
         const float lo = __bfloat162float(src[i]);
         const float hi = __bfloat162float(src[i + half]);
-        float2 cs = rp[i];
-        if (rr) {
-          const float2 d = rr[i];
-          cs = make_float2(cs.x * d.x - cs.y * d.y, cs.y * d.x + cs.x * d.y);
-        }
+        const float2 cs = rp[i];
         val = e < half ? (lo * cs.x - hi * cs.y) : (lo * cs.y + hi * cs.x);
       }
       o[j] = val;
@@ -393,7 +379,7 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
     const uint32_t t_s = lane_base + NUM_M * HDP + m * kBN;
     const uint32_t t_o = lane_base + m * HDP;
 
-    int cur_rot = w.seg_end > w.seg_begin ? p.segs[w.seg_begin].rot : -1;
+    int cur_rot = w.seg_end > w.seg_begin ? p.segs[w.seg_begin].shift : 0;
     load_q_row<HDP>(p, q_tile, trow, valid, t, head, cur_rot);
     fence_proxy_async_smem();
     mbar_arrive(&q_full[m]);
@@ -424,11 +410,11 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
         // invalid rows (beyond the work's rows) count as full: their S is Q=0 . K = 0
         // and their P only feeds their own (never stored) O rows
         const bool full = !valid || (c_lo == 0 && c_hi == kBN && (b_hi <= 0 || b_lo >= kBN || b_lo >= b_hi));
-        const bool restage = tt == nt - 1 && si + 1 < w.seg_end && p.segs[si + 1].rot != cur_rot;
+        const bool restage = tt == nt - 1 && si + 1 < w.seg_end && p.segs[si + 1].shift != cur_rot;
         mbar_wait(&s_full[m], j & 1);
         tc_fence_after();
         if (warp_dead || (p.dbg & 1)) {  // no valid row: its P rows only feed its own (discarded) O rows
-          if (restage) cur_rot = p.segs[si + 1].rot;
+          if (restage) cur_rot = p.segs[si + 1].shift;
           tc_fence_before();
           mbar_arrive(&p_full[m]);
           continue;
@@ -497,7 +483,7 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
         const float2 pss = fadd2(ps[0], ps[1]);
         l_sum += pss.x + pss.y;
         if (restage) {  // QK(m, j) retired (S read) and QK(m, j+1) waits for p_full(m, j)
-          cur_rot = p.segs[si + 1].rot;
+          cur_rot = p.segs[si + 1].shift;
           load_q_row<HDP>(p, q_tile, trow, valid, t, head, cur_rot);
           fence_proxy_async_smem();
         }
@@ -639,7 +625,6 @@ extern "C" int dbsa_attention(const DbsaAttnArgs *args, void *stream) {
   p.tok_lo = a.tok_lo;
   p.rope = reinterpret_cast<const float2 *>(a.rope_table);
   p.rope_rows = a.rope_rows;
-  p.rot = reinterpret_cast<const float2 *>(a.rot_table);
   p.n_heads = a.n_heads;
   p.n_kv_heads = a.n_kv_heads;
   p.head_dim = a.head_dim;

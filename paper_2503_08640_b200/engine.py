@@ -117,6 +117,14 @@ class DeviceModel:
         embed = torch.empty((c.vocab_size, c.d_model), dtype=torch.float32, device=dev).uniform_(-0.1, 0.1, generator=g)
         return cls(c, dev, embed, layers, ones(c.d_model), u((c.d_model, c.vocab_size), c.d_model))
 
+    def rope_for(self, rows: int):
+        """Rope table covering positions [0, rows) (stage 2 reads rows
+        position - delta, which may exceed max_seq_len); grown on demand."""
+        if rows > self.rope.shape[0]:
+            self.rope = ops.rope_table(max(rows, 2 * self.rope.shape[0]), self.config.head_dim,
+                                       self.config.rope_theta, self.device)
+        return self.rope
+
     def nbytes(self) -> int:
         n = self.embed.numel() * 4 + self.lm_head.numel() * 2
         for lw in self.layers:
@@ -214,7 +222,7 @@ def _seg_array(segs) -> np.ndarray:
     a = np.zeros(len(segs), dtype=ops.SEG_DTYPE)
     if segs:
         s = np.asarray(segs, dtype=np.int32).reshape(len(segs), -1)
-        for i, name in enumerate(("src", "layer", "row0", "n_tok", "kind", "rot")):
+        for i, name in enumerate(("src", "layer", "row0", "n_tok", "kind", "shift")):
             a[name] = s[:, i]
     return a
 
@@ -337,8 +345,8 @@ class Stage1Plan:
             for t0 in range(0, t, slab):
                 nt = min(slab, t - t0)
                 sb = len(segs)
-                segs += [(0, 0, x.row0, x.token_count, SEG_FULL, -1) for x in ctx]
-                segs.append((0, 0, e.row0, t0 + nt, SEG_SELF, -1))
+                segs += [(0, 0, x.row0, x.token_count, SEG_FULL, 0) for x in ctx]
+                segs.append((0, 0, e.row0, t0 + nt, SEG_SELF, 0))
                 keys = n_ctx + t0 + nt
                 for kv in range(hkv):
                     works.append((keys, local0 + t0, nt, local0, kv, sb, len(segs), 0, 0, 0))
@@ -385,7 +393,7 @@ def encode_groups_gen(dm, cache, new, ids, pattern, layers=None):
                      store.v, store.rows, c.n_layers, layer, c.n_kv_heads, c.head_dim)
 
     def attend(layer, qkv, out):
-        ops.attention(q=qkv, q_tok_stride=stride, tok_pos=plan.pos, tok_lo=None, rope=dm.rope, rot=None,
+        ops.attention(q=qkv, q_tok_stride=stride, tok_pos=plan.pos, tok_lo=None, rope=dm.rope,
                       pool=store.planes(), aux=None, n_heads=c.n_heads, n_kv_heads=c.n_kv_heads, head_dim=c.head_dim,
                       works_dev=plan.works, n_works=plan.n_works, segs_dev=plan.segs_ptr(layer), num_m=plan.num_m,
                       out=out, out_tok_stride=qw)
@@ -500,6 +508,7 @@ class NewTokens:
         ids = np.concatenate([np.asarray(j.ids, np.int64) for j in jobs])
         if int(pos.max()) >= c.max_seq_len:
             raise ValidationError(f"position {int(pos.max())} exceeds max_seq_len {c.max_seq_len}")
+        self.max_pos = int(pos.max())
         self.pos = torch.from_numpy(pos).to(dev, non_blocking=True)
         self.lo = torch.from_numpy(lo).to(dev, non_blocking=True)
         self.ids = torch.from_numpy(ids).to(dev, non_blocking=True)
@@ -542,7 +551,8 @@ class AttnSchedule:
         gs, hkv, hd = c.group_size, c.n_kv_heads, c.head_dim
         tables = chunk_tables if chunk_tables is not None else [j.chunks for j in jobs]
         target = target_ctas or 4 * 148
-        segs, works, merges, rots = [], [], [], []
+        segs, works, merges = [], [], []
+        min_shift = 0
         part_rows = 0 if mode == "split" else nt.canon_rows
         kv_tok = 0
         for qi, j in enumerate(jobs):
@@ -552,11 +562,9 @@ class AttnSchedule:
             kv_tok += int(ch[:, 1].sum()) if len(ch) else 0
             chunk_segs = []
             for row, cnt, delta in ch:
-                rot = -1
-                if delta != 0:
-                    rot = len(rots)
-                    rots.append(int(delta))
-                chunk_segs.append((0, 0, int(row), int(cnt), SEG_FULL, rot))
+                # queries of this chunk use rope row (position - delta)
+                chunk_segs.append((0, 0, int(row), int(cnt), SEG_FULL, int(delta)))
+                min_shift = min(min_shift, int(delta))
             q0 = int(nt.tok0[qi])
             if mode == "canonical":
                 if not chunk_segs and not include_self:
@@ -566,7 +574,7 @@ class AttnSchedule:
                     sb = len(segs)
                     segs += chunk_segs
                     if include_self:
-                        segs.append((1, 0, int(nt.aux_row0[qi]), t0 + ntk, SEG_SELF, -1))
+                        segs.append((1, 0, int(nt.aux_row0[qi]), t0 + ntk, SEG_SELF, 0))
                     for kv in range(hkv):
                         works.append((q0 + t0, ntk, q0, kv, sb, len(segs), j.prefix, 1,
                                       nt.part_base[qi][si] + kv * rows))
@@ -583,7 +591,7 @@ class AttnSchedule:
                 last_sb = len(segs)
                 segs += chunk_segs[bounds[n_split - 1]:bounds[n_split]]
                 if include_self:
-                    segs.append((1, 0, int(nt.aux_row0[qi]), t0 + ntk, SEG_SELF, -1))
+                    segs.append((1, 0, int(nt.aux_row0[qi]), t0 + ntk, SEG_SELF, 0))
                 last = (last_sb, len(segs))
                 for kv in range(hkv):
                     base = part_rows
@@ -605,8 +613,7 @@ class AttnSchedule:
         self.segs = ops.to_device(_per_layer_segs(_seg_array(segs), c.n_layers), dev)
         self.merges = ops.to_device(_merge_array(merges), dev) if merges else None
         self.max_rows = max((m[1] for m in merges), default=0)
-        self.rot = (torch.from_numpy(ops.shift_table(rots, hd, c.rope_theta)).to(dev) if rots
-                    else torch.zeros((1, hd // 2, 2), dtype=torch.float32, device=dev))
+        self.rope = dm.rope_for(nt.max_pos - min_shift + 1)
         self.part_rows = part_rows
         self.part_o = torch.empty((max(part_rows, 1), hd), dtype=torch.float32, device=dev)
         self.part_lse = torch.empty((max(part_rows, 1),), dtype=torch.float32, device=dev)
@@ -619,7 +626,7 @@ class AttnSchedule:
         qw, kw = c.n_heads * c.head_dim, c.n_kv_heads * c.head_dim
         if self.n_works == 0:
             return
-        ops.attention(q=qkv, q_tok_stride=qw + 2 * kw, tok_pos=nt.pos, tok_lo=nt.lo, rope=dm.rope, rot=self.rot,
+        ops.attention(q=qkv, q_tok_stride=qw + 2 * kw, tok_pos=nt.pos, tok_lo=nt.lo, rope=self.rope,
                       pool=pool, aux=nt.aux(), n_heads=c.n_heads, n_kv_heads=c.n_kv_heads, head_dim=c.head_dim,
                       works_dev=self.works, n_works=self.n_works, segs_dev=self.segs_ptr(layer), num_m=nt.num_m,
                       out=out, out_tok_stride=qw, part_o=self.part_o if part_o is None else part_o,
@@ -635,7 +642,7 @@ class Stage2Plan:
         self.sched = AttnSchedule(dm, jobs, self.new, target_ctas=target_ctas, order=order)
         for name in ("tok0", "n_tok", "num_m", "pos", "lo", "ids", "pages", "n_pages", "k_aux", "v_aux", "aux_rows"):
             setattr(self, name, getattr(self.new, name))
-        for name in ("works", "n_works", "n_segs", "n_merge", "merges", "max_rows", "rot", "part_o", "part_lse",
+        for name in ("works", "n_works", "n_segs", "n_merge", "merges", "max_rows", "rope", "part_o", "part_lse",
                      "kv_tokens"):
             setattr(self, name, getattr(self.sched, name))
 
@@ -884,8 +891,8 @@ def forward_explicit_context(dm, tokens, context):
         nt = min(slab, t - t0)
         sb = len(segs)
         if n_ctx:
-            segs.append((0, 0, rows[0], n_ctx, SEG_FULL, -1))
-        segs.append((0, 0, self_row, t0 + nt, SEG_SELF, -1))
+            segs.append((0, 0, rows[0], n_ctx, SEG_FULL, 0))
+        segs.append((0, 0, self_row, t0 + nt, SEG_SELF, 0))
         for kv in range(c.n_kv_heads):
             works.append((t0, nt, 0, kv, sb, len(segs), 0, 0, 0))
     wdev = ops.to_device(_work_array(works), dev)
@@ -899,7 +906,7 @@ def forward_explicit_context(dm, tokens, context):
                     qkv[:, qw + kw:].float().reshape(t, c.n_kv_heads, c.head_dim).cpu().numpy()))
 
     def attend(layer, qkv, out):
-        ops.attention(q=qkv, q_tok_stride=stride, tok_pos=pos, tok_lo=None, rope=dm.rope, rot=None,
+        ops.attention(q=qkv, q_tok_stride=stride, tok_pos=pos, tok_lo=None, rope=dm.rope,
                       pool=store.planes(), aux=None, n_heads=c.n_heads, n_kv_heads=c.n_kv_heads, head_dim=c.head_dim,
                       works_dev=wdev, n_works=len(works),
                       segs_dev=sdev.data_ptr() + layer * len(segs) * ops.SEG_DTYPE.itemsize, num_m=num_m, out=out,

@@ -35,7 +35,7 @@ WORK_DTYPE = np.dtype(
      ("part_row0", "<i8")], align=True)
 SEG_DTYPE = np.dtype(
     [("src", "<i4"), ("layer", "<i4"), ("row0", "<i4"), ("n_tok", "<i4"),
-     ("kind", "<i4"), ("rot", "<i4"), ("pad0", "<i4"), ("pad1", "<i4")], align=True)
+     ("kind", "<i4"), ("shift", "<i4"), ("pad0", "<i4"), ("pad1", "<i4")], align=True)
 PAGE_DTYPE = np.dtype([("tok0", "<i4"), ("n_tok", "<i4"), ("row0", "<i4"), ("pad", "<i4")], align=True)
 MERGE_DTYPE = np.dtype(
     [("part_row0", "<i8"), ("rows", "<i4"), ("n_splits", "<i4"), ("q_tok0", "<i4"), ("kv_head", "<i4")],
@@ -85,13 +85,6 @@ def rope_table(rows: int, head_dim: int, theta: float, device, pos0: int = 0):
     return table
 
 
-def shift_table(deltas, head_dim: int, theta: float) -> np.ndarray:
-    """Host float64 (cos, sin) of (-delta) * inv_freq for each delta -> float32 [n, hd/2, 2]."""
-    f = inv_freq(head_dim, theta)
-    ang = -np.asarray(deltas, dtype=np.float64)[:, None] * f[None, :]
-    return np.stack([np.cos(ang), np.sin(ang)], axis=-1).astype(np.float32)
-
-
 def kv_write(k_src, v_src, src_tok_stride, tok_pos, rope, pages_dev, n_pages, k_dst, v_dst, dst_rows,
              dst_layers, layer, n_kv_heads, head_dim):
     a = nat.KvWriteArgs(
@@ -104,7 +97,7 @@ def kv_write(k_src, v_src, src_tok_stride, tok_pos, rope, pages_dev, n_pages, k_
     _launched()
 
 
-def attention(*, q, q_tok_stride, tok_pos, tok_lo, rope, rot, pool, aux, n_heads, n_kv_heads, head_dim,
+def attention(*, q, q_tok_stride, tok_pos, tok_lo, rope, pool, aux, n_heads, n_kv_heads, head_dim,
               works_dev, n_works, segs_dev, num_m, out, out_tok_stride, part_o=None, part_lse=None):
     """Launch K1/K3.  `pool` / `aux` are (k_planes, v_planes, rows, layers)."""
     kp, vp, prow, pl = pool
@@ -112,7 +105,7 @@ def attention(*, q, q_tok_stride, tok_pos, tok_lo, rope, rot, pool, aux, n_heads
     a = nat.AttnArgs(
         q=q.data_ptr(), q_tok_stride=q_tok_stride, tok_pos=tok_pos.data_ptr(),
         tok_lo=nat.ptr(tok_lo), rope_table=rope.data_ptr(), rope_rows=rope.shape[0],
-        rot_table=nat.ptr(rot), k_pool=kp.data_ptr(), v_pool=vp.data_ptr(), pool_rows=prow,
+        k_pool=kp.data_ptr(), v_pool=vp.data_ptr(), pool_rows=prow,
         pool_layers=pl, k_aux=nat.ptr(ka), v_aux=nat.ptr(va), aux_rows=arow, aux_layers=al,
         n_heads=n_heads, n_kv_heads=n_kv_heads, head_dim=head_dim, hd_pad=hd_pad(head_dim),
         scale=float(1.0 / math.sqrt(head_dim)), num_m=num_m, works=_p(works_dev),
@@ -174,5 +167,19 @@ def label_logprob(logits, targets):
     out = torch.empty(logits.shape[0], dtype=torch.float32, device=logits.device)
     nat.check(nat.load_library().dbsa_label_logprob(logits.data_ptr(), logits.shape[0], logits.shape[1],
                                                      targets.data_ptr(), out.data_ptr(), nat.stream_handle()))
+    _launched()
+    return out
+
+
+def bm25_scores(term_ids, tf, idf, norm, k1p1: float):
+    """term_ids int32 [Q, T] (-1 pad), tf uint16 [V, U], idf f64 [V], norm f64 [U] -> f64 [Q, U]."""
+    import torch
+
+    n_q, max_terms = term_ids.shape
+    n_units = tf.shape[1]
+    out = torch.empty((n_q, n_units), dtype=torch.float64, device=tf.device)
+    nat.check(nat.load_library().dbsa_bm25_scores(term_ids.data_ptr(), n_q, max_terms, tf.data_ptr(), idf.data_ptr(),
+                                                   norm.data_ptr(), n_units, float(k1p1), out.data_ptr(),
+                                                   nat.stream_handle()))
     _launched()
     return out

@@ -252,12 +252,14 @@ class Stage2Session:
         tab = np.stack([self.u_row[ids], ln, delta], axis=-1)
         return tab, ln.sum(axis=1)
 
-    def select(self, scores: np.ndarray):
-        """K4 on the device: float64 scores [B, n_units] -> ordered ids (host int64)."""
+    def select(self, scores):
+        """K4 on the device: float64 scores [B, n_units] (host array or device
+        tensor) -> ordered unit ids (host int64)."""
         import torch
 
-        ids = engine.ops.topk_select(torch.from_numpy(np.ascontiguousarray(scores)).to(self.dm.device), self.budget,
-                                     self.ordering)
+        if not isinstance(scores, torch.Tensor):
+            scores = torch.from_numpy(np.ascontiguousarray(scores))
+        ids = engine.ops.topk_select(scores.to(self.dm.device), self.budget, self.ordering)
         return ids.cpu().numpy().astype(np.int64)
 
     def plan(self, ids: np.ndarray, query_ids_list, target_ctas=None):
@@ -368,7 +370,8 @@ class Runner:
             texts = list(query_texts[b0:b0 + max_batch])
             t0 = time.perf_counter()
             q_ids = [tokenizer.encode(self.task.template.render_query(t)) for t in texts]
-            scores = self.index.score_matrix([retrieval.bm25_tokenize(t) for t in texts])
+            # GPU BM25 (bit-identical to the host scores) straight into K4
+            scores = self.index.score_matrix_device([retrieval.bm25_tokenize(t) for t in texts], self.dm.device)
             ids, _, best = sess.answer(scores, q_ids)
             best = best.cpu().numpy()
             dt = (time.perf_counter() - t0) / len(texts)

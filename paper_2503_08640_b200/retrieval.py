@@ -165,6 +165,47 @@ class Bm25Index:
                     acc += r
         return out
 
+    def device_tables(self, device=None):
+        """(vocab {term: id}, tf uint16 [V, U], idf f64 [V], norm f64 [U]) on the
+        GPU, built once; idf and norm are computed on the host with the
+        reference's exact expressions (retrieval.py:125-134)."""
+        from .engine import default_device
+
+        dev = default_device(device)
+        key = str(dev)
+        cache = getattr(self, "_device_tables", None)
+        if cache is None:
+            cache = self._device_tables = {}
+        if key not in cache:
+            import torch
+
+            vocab = {t: i for i, t in enumerate(sorted(self.df))}
+            tf = np.zeros((max(1, len(vocab)), self.n_docs), np.uint16)
+            for u, counter in enumerate(self.doc_terms):
+                for t, f in counter.items():
+                    if f > 65535:
+                        raise ValidationError("term frequency above 65535 is not supported by the GPU BM25")
+                    tf[vocab[t], u] = f
+            idf = np.array([self.idf(t) for t in sorted(self.df)] or [0.0], np.float64)
+            cache[key] = (vocab, torch.from_numpy(tf).to(dev), torch.from_numpy(idf).to(dev),
+                          torch.from_numpy(self._norms()).to(dev))
+        return cache[key]
+
+    def score_matrix_device(self, queries_terms, device=None):
+        """GPU BM25 (csrc/bm25.cu): float64 [n_queries, n_units] on the device,
+        bit-identical to score_matrix."""
+        import torch
+
+        from . import ops
+
+        vocab, tf, idf, norm = self.device_tables(device)
+        width = max(1, max((len(t) for t in queries_terms), default=1))
+        ids = np.full((len(queries_terms), width), -1, np.int32)
+        for qi, terms in enumerate(queries_terms):
+            for i, t in enumerate(terms):
+                ids[qi, i] = vocab.get(t, -1)
+        return ops.bm25_scores(torch.from_numpy(ids).to(tf.device), tf, idf, norm, self.k1 + 1.0)
+
     def to_json(self) -> dict:
         return {"granularity": self.granularity, "k1": self.k1, "b": self.b,
                 "unit_refs": [list(r) for r in self.unit_refs], "unit_examples": [list(e) for e in self.unit_examples],

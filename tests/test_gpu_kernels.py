@@ -119,8 +119,8 @@ def _stage1_case(hd, H, Hkv, lengths, j=2, layer=0, layers=1):
                 nt = min(slab_tok, n - t0)
                 sb = len(segs)
                 for c in ctx:
-                    segs.append((0, layer, pool.row0(c), lengths[c], ops.nat.SEG_FULL, -1, 0, 0))
-                segs.append((0, layer, pool.row0(b), t0 + nt, ops.nat.SEG_SELF, -1, 0, 0))
+                    segs.append((0, layer, pool.row0(c), lengths[c], ops.nat.SEG_FULL, 0, 0, 0))
+                segs.append((0, layer, pool.row0(b), t0 + nt, ops.nat.SEG_SELF, 0, 0, 0))
                 works.append((int(pool.pos_start[b]) + t0, nt, int(pool.pos_start[b]), kv, sb, len(segs), 0, 0, 0))
     W = np.array([w[:8] for w in works], dtype=np.int32)
     wa = np.zeros(len(works), dtype=ops.WORK_DTYPE)
@@ -130,7 +130,7 @@ def _stage1_case(hd, H, Hkv, lengths, j=2, layer=0, layers=1):
     out = torch.zeros(T, H, hd, dtype=torch.bfloat16, device=dev)
     qd = q.to(dev)
     pos = torch.arange(T, dtype=torch.int32, device=dev)
-    ops.attention(q=qd, q_tok_stride=H * hd, tok_pos=pos, tok_lo=None, rope=pool.rope, rot=None,
+    ops.attention(q=qd, q_tok_stride=H * hd, tok_pos=pos, tok_lo=None, rope=pool.rope,
                   pool=(pool.kp, pool.vp, pool.rows, layers), aux=None, n_heads=H, n_kv_heads=Hkv, head_dim=hd,
                   works_dev=ops.to_device(wa, dev), n_works=len(wa), segs_dev=ops.to_device(sa, dev), num_m=num_m,
                   out=out, out_tok_stride=H * hd)
@@ -194,16 +194,15 @@ def _stage2_case(hd, H, Hkv, lengths, sel, n_q, labels, splits, theta=10000.0):
                      dtype=np.int32).view(ops.PAGE_DTYPE).reshape(-1)
     ops.kv_write(kn.to(dev).reshape(n_new, -1), vn.to(dev).reshape(n_new, -1), Hkv * hd, posd, pool.rope,
                  ops.to_device(pages, dev), len(pages), ka, va, aux_rows, 1, 0, Hkv, hd)
-    # chunks: selected groups at new positions, delta = new_start - orig_start
-    deltas, chunk_segs, new_start = [], [], 0
+    # chunks: selected groups at new positions; the queries of a chunk use rope
+    # row (position - delta), delta = new_start - orig_start
+    chunk_segs, new_start = [], 0
     for b in sel:
-        deltas.append(new_start - int(pool.pos_start[b]))
-        chunk_segs.append((0, 0, pool.row0(b), lengths[b], ops.nat.SEG_FULL, len(deltas) - 1, 0, 0))
+        chunk_segs.append((0, 0, pool.row0(b), lengths[b], ops.nat.SEG_FULL, new_start - int(pool.pos_start[b]), 0, 0))
         new_start += lengths[b]
-    rot = torch.from_numpy(ops.shift_table(deltas, hd, theta)).to(dev)
     per = -(-len(chunk_segs) // splits)
     groups_segs = [chunk_segs[i:i + per] for i in range(0, len(chunk_segs), per)]
-    groups_segs[-1] = groups_segs[-1] + [(1, 0, 0, n_new, ops.nat.SEG_SELF, -1, 0, 0)]
+    groups_segs[-1] = groups_segs[-1] + [(1, 0, 0, n_new, ops.nat.SEG_SELF, 0, 0, 0)]
     S = len(groups_segs)
     num_m = 2 if n_new * gs > 128 else 1
     assert n_new * gs <= 128 * num_m
@@ -225,7 +224,7 @@ def _stage2_case(hd, H, Hkv, lengths, sel, n_q, labels, splits, theta=10000.0):
     part_o = torch.zeros(Hkv * S * rows, hd, dtype=torch.float32, device=dev)
     part_l = torch.zeros(Hkv * S * rows, dtype=torch.float32, device=dev)
     ops.attention(q=qn.to(dev), q_tok_stride=H * hd, tok_pos=posd, tok_lo=torch.tensor(lo, dtype=torch.int32,
-                  device=dev), rope=pool.rope, rot=rot, pool=(pool.kp, pool.vp, pool.rows, 1), aux=(ka, va, aux_rows, 1),
+                  device=dev), rope=pool.rope, pool=(pool.kp, pool.vp, pool.rows, 1), aux=(ka, va, aux_rows, 1),
                   n_heads=H, n_kv_heads=Hkv, head_dim=hd, works_dev=ops.to_device(wa, dev), n_works=len(wa),
                   segs_dev=ops.to_device(sa, dev), num_m=num_m, out=out, out_tok_stride=H * hd, part_o=part_o,
                   part_lse=part_l)

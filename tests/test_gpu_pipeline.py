@@ -218,3 +218,21 @@ def test_errors_map_to_reference_exceptions():
         P.Runner(P.init_random(other, 0), enc.cache, enc.index, task, mc)
     with pytest.raises(P.ValidationError):
         P.score_label(w, None, [], [5])
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_gpu_bm25_bit_exact(name):
+    """GPU BM25 (csrc/bm25.cu) equals the reference's float64 scores bit for
+    bit, and K4 over them reproduces the reference's selections."""
+    meta, a, w, task, mc, enc = _encoded(name)
+    texts = [q["query"] for q in meta["queries"]] + ["zzz unknown terms only", "key0001 key0001 lookup"]
+    terms = [retrieval.bm25_tokenize(t) for t in texts]
+    dev_scores = enc.index.score_matrix_device(terms).cpu().numpy()
+    host = enc.index.score_matrix(terms)
+    np.testing.assert_array_equal(dev_scores, host)
+    for qi in range(len(meta["queries"])):
+        np.testing.assert_array_equal(dev_scores[qi], a[f"q{qi}_bm25"])
+    runner = P.Runner(w, enc.cache, enc.index, task, mc)
+    ids = runner.session().select(enc.index.score_matrix_device(terms[: len(meta["queries"])]))
+    for qi in range(len(meta["queries"])):
+        np.testing.assert_array_equal(ids[qi], a[f"q{qi}_units"])

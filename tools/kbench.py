@@ -26,8 +26,20 @@ args = ap.parse_args()
 dev = torch.device("cuda", 0)
 cfg = P.ModelConfig(d_model=args.heads * 128, n_layers=1, n_heads=args.heads, n_kv_heads=args.hkv, head_dim=128,
                     ffn_dim=14336, vocab_size=128256, rope_theta=500000.0, max_seq_len=131072)
-dm = types.SimpleNamespace(config=cfg, device=dev)
 rope = ops.rope_table(cfg.max_seq_len, 128, cfg.rope_theta, dev)
+
+
+class _DM:  # the two attributes the plans read, plus the rope table
+    config, device = cfg, dev
+
+    def rope_for(self, rows):
+        global rope
+        if rows > rope.shape[0]:
+            rope = ops.rope_table(rows, 128, cfg.rope_theta, dev)
+        return rope
+
+
+dm = _DM()
 cache = P.SegmentedKVCache(cfg, dev, capacity_tokens=args.groups * args.gtok)
 new = cache._reserve([args.gtok] * args.groups, [b"\0" * 32] * args.groups, [()] * args.groups)
 g = torch.Generator(device=dev).manual_seed(0)
@@ -52,7 +64,7 @@ if args.stage in ("1", "both"):
     qkv = torch.randn(T, stride, device=dev).to(torch.bfloat16)
     out = torch.empty(T, qw, dtype=torch.bfloat16, device=dev)
     def k1():
-        ops.attention(q=qkv, q_tok_stride=stride, tok_pos=plan.pos, tok_lo=None, rope=rope, rot=None,
+        ops.attention(q=qkv, q_tok_stride=stride, tok_pos=plan.pos, tok_lo=None, rope=rope,
                       pool=st.planes(), aux=None, n_heads=cfg.n_heads, n_kv_heads=cfg.n_kv_heads, head_dim=128,
                       works_dev=plan.works, n_works=plan.n_works, segs_dev=plan.segs_ptr(0), num_m=plan.num_m,
                       out=out, out_tok_stride=qw)
@@ -62,7 +74,7 @@ if args.stage in ("1", "both"):
 
 if args.stage in ("2", "both"):
     rng = np.random.default_rng(1)
-    sess = P.Stage2Session(types.SimpleNamespace(config=cfg, device=dev), cache,
+    sess = P.Stage2Session(dm, cache,
                            [(b, 0, args.gtok) for b in range(args.groups)], [[5, 6, 7, 8]] * 4, args.ratio, "in-order")
     B = args.batch
     scores = rng.random((B, args.groups))
@@ -76,7 +88,7 @@ if args.stage in ("2", "both"):
     out = torch.empty(plan.n_tok, qw, dtype=torch.bfloat16, device=dev)
     aux = (plan.k_aux, plan.v_aux, plan.aux_rows, 1)
     def k3():
-        ops.attention(q=qkv, q_tok_stride=stride, tok_pos=plan.pos, tok_lo=plan.lo, rope=rope, rot=plan.rot,
+        ops.attention(q=qkv, q_tok_stride=stride, tok_pos=plan.pos, tok_lo=plan.lo, rope=plan.rope,
                       pool=st.planes(), aux=aux, n_heads=cfg.n_heads, n_kv_heads=cfg.n_kv_heads, head_dim=128,
                       works_dev=plan.works, n_works=plan.n_works, segs_dev=plan.segs_ptr(0), num_m=plan.num_m,
                       out=out, out_tok_stride=qw, part_o=plan.part_o, part_lse=plan.part_lse)
