@@ -208,7 +208,8 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
   uint64_t *s_full = q_full + NUM_M;          // [NUM_M]  S(m, j) in TMEM
   uint64_t *p_full = s_full + NUM_M;          // [NUM_M]  P(m, j) in TMEM (S consumed)
   uint64_t *o_full = p_full + NUM_M;          // [NUM_M]
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(o_full + NUM_M);
+  uint64_t *q_ready = o_full + NUM_M;         // [NUM_M]  Q(m) re-staged for a new RoPE shift
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(q_ready + NUM_M);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const DbsaAttnWork w = p.works[blockIdx.x];
@@ -227,6 +228,7 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
       mbar_init(&s_full[m], 1);
       mbar_init(&p_full[m], 128);
       mbar_init(&o_full[m], 1);
+      mbar_init(&q_ready[m], 128);
     }
     fence_mbar_init();
     tma_prefetch(&tm_k0);
@@ -334,7 +336,23 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
     if (n_tiles > 0) {
       for (int m = 0; m < NUM_M; ++m) mbar_wait(&q_full[m], 0);
       tc_fence_after();
+      // segment iterator: tile j is a "shift boundary" when it opens a segment
+      // whose RoPE shift differs from the previous segment's -- QK(m, j) must
+      // then wait for the softmax warps to re-stage Q(m) (q_ready), while
+      // P.V(m, j-1) does not.
+      int it_seg = w.seg_begin, it_tt = 0;
+      int it_nt = ((p.segs[it_seg].row0 & 63) + p.segs[it_seg].n_tok + kBN - 1) / kBN;
+      int n_bound = 0;
       for (int j = 0; j < n_tiles; ++j) {
+        bool boundary = false;
+        if (it_tt == it_nt) {  // advance to the next segment
+          const int prev_shift = p.segs[it_seg].shift;
+          ++it_seg;
+          it_tt = 0;
+          it_nt = ((p.segs[it_seg].row0 & 63) + p.segs[it_seg].n_tok + kBN - 1) / kBN;
+          boundary = p.segs[it_seg].shift != prev_shift;
+        }
+        ++it_tt;
         mbar_wait(&k_full[j % C::KST], (j / C::KST) & 1);
         tc_fence_after();
         for (int m = 0; m < NUM_M; ++m) {
@@ -346,8 +364,13 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
             pv(m, j - 1);
             if (m == NUM_M - 1) commit(&v_empty[(j - 1) % C::VST]);
           }
+          if (boundary) {
+            mbar_wait(&q_ready[m], n_bound & 1);
+            tc_fence_after();
+          }
           qk(m, j);
         }
+        n_bound += boundary;
         commit(&k_empty[j % C::KST]);
       }
       const int j = n_tiles - 1;
@@ -414,7 +437,10 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
         mbar_wait(&s_full[m], j & 1);
         tc_fence_after();
         if (warp_dead || (p.dbg & 1)) {  // no valid row: its P rows only feed its own (discarded) O rows
-          if (restage) cur_rot = p.segs[si + 1].shift;
+          if (restage) {
+            cur_rot = p.segs[si + 1].shift;
+            mbar_arrive(&q_ready[m]);  // nothing to re-stage for invalid rows
+          }
           tc_fence_before();
           mbar_arrive(&p_full[m]);
           continue;
@@ -482,14 +508,15 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
         }
         const float2 pss = fadd2(ps[0], ps[1]);
         l_sum += pss.x + pss.y;
-        if (restage) {  // QK(m, j) retired (S read) and QK(m, j+1) waits for p_full(m, j)
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&p_full[m]);  // P.V(m, j) may start now
+        if (restage) {  // QK(m, j) retired (S read); QK(m, j+1) waits for q_ready(m)
           cur_rot = p.segs[si + 1].shift;
           load_q_row<HDP>(p, q_tile, trow, valid, t, head, cur_rot);
           fence_proxy_async_smem();
+          mbar_arrive(&q_ready[m]);
         }
-        tmem_wait_st();
-        tc_fence_before();
-        mbar_arrive(&p_full[m]);
       }
     }
 
