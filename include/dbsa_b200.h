@@ -168,6 +168,23 @@ typedef struct DbsaKvWriteArgs {
 } DbsaKvWriteArgs;
 int dbsa_kv_write(const DbsaKvWriteArgs *args, void *stream);
 
+/* Component K2r: page read-back (inverse of K2w) for cache serialisation
+ * (kvstore.serialize, kvstore.py:238-258): fp32 pre-rotation K (un-rotated at
+ * tok_pos) and V, token-major [t][kvh][head_dim], for a set of pages. */
+typedef struct DbsaKvReadArgs {
+  const void *k_src, *v_src; /* planes */
+  int64_t src_rows;
+  int32_t src_layers, layer;
+  const int32_t *tok_pos; /* position of each output token */
+  const float *rope_table;
+  int64_t rope_rows;
+  const DbsaPage *pages; /* device; tok0 indexes the output */
+  int32_t n_pages;
+  int32_t n_kv_heads, head_dim, hd_pad;
+  float *k_dst, *v_dst;
+} DbsaKvReadArgs;
+int dbsa_kv_read(const DbsaKvReadArgs *args, void *stream);
+
 /* Rotary table: table[p][i] = (cos, sin)(p * inv_freq[i]) with the angle
  * formed in float64 exactly as model.rope_angles (model.py:205-209). */
 int dbsa_rope_table(float *table, int64_t rows, const double *inv_freq, int32_t half,

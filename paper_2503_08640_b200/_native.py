@@ -20,6 +20,7 @@ EXPORTED_SYMBOLS = (
     "dbsa_attention",
     "dbsa_lse_merge",
     "dbsa_kv_write",
+    "dbsa_kv_read",
     "dbsa_rope_table",
     "dbsa_topk_select",
     "dbsa_rmsnorm",
@@ -91,6 +92,14 @@ class KvWriteArgs(ctypes.Structure):
     ]
 
 
+class KvReadArgs(ctypes.Structure):
+    _fields_ = [
+        ("k_src", _vp), ("v_src", _vp), ("src_rows", _i64), ("src_layers", _i32), ("layer", _i32),
+        ("tok_pos", _vp), ("rope_table", _vp), ("rope_rows", _i64), ("pages", _vp), ("n_pages", _i32),
+        ("n_kv_heads", _i32), ("head_dim", _i32), ("hd_pad", _i32), ("k_dst", _vp), ("v_dst", _vp),
+    ]
+
+
 _ERRORS = {
     1: errors.ShapeError,
     2: errors.MaskError,
@@ -125,6 +134,7 @@ def load_library(path: Path | str | None = None) -> ctypes.CDLL:
         lib.dbsa_attention.argtypes = [ctypes.POINTER(AttnArgs), _vp]
         lib.dbsa_lse_merge.argtypes = [ctypes.POINTER(MergeArgs), _vp]
         lib.dbsa_kv_write.argtypes = [ctypes.POINTER(KvWriteArgs), _vp]
+        lib.dbsa_kv_read.argtypes = [ctypes.POINTER(KvReadArgs), _vp]
         lib.dbsa_rope_table.argtypes = [_vp, _i64, _vp, _i32, _i64, _vp]
         lib.dbsa_topk_select.argtypes = [_vp, _i64, _i64, _i64, _i32, _vp, _vp]
         lib.dbsa_rmsnorm.argtypes = [_vp, _vp, _vp, _i64, _i64, _f32, _vp]

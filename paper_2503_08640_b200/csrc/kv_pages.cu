@@ -71,6 +71,35 @@ __global__ void kv_write_kernel(DbsaKvWriteArgs a) {
   }
 }
 
+// K2r: page read-back for serialisation -- the inverse of K2w.  For every
+// token of the given pages: K un-rotated at tok_pos (x c + y s, -x s + y c)
+// and V, both fp32, token-major [t][kvh][d] (the reference's segment layout,
+// kvstore.py:59-60).  grid (n_pages, n_kv_heads), 128 threads.
+__global__ void kv_read_kernel(DbsaKvReadArgs a) {
+  const DbsaPage pg = a.pages[blockIdx.x];
+  const int head = blockIdx.y;
+  const int hd = a.head_dim, half = hd >> 1, HDP = a.hd_pad;
+  const float2 *rope = reinterpret_cast<const float2 *>(a.rope_table);
+  const int64_t plane = (int64_t)a.layer * a.n_kv_heads + head;
+  const __nv_bfloat16 *ks = reinterpret_cast<const __nv_bfloat16 *>(a.k_src) + plane * a.src_rows * HDP;
+  const __nv_bfloat16 *vs = reinterpret_cast<const __nv_bfloat16 *>(a.v_src) + plane * a.src_rows * HDP;
+  for (int it = threadIdx.x; it < pg.n_tok * half; it += blockDim.x) {
+    const int i = it / half, e = it % half;
+    const int t = pg.tok0 + i;
+    const __nv_bfloat16 *kr = ks + (int64_t)(pg.row0 + i) * HDP;
+    const float x = __bfloat162float(kr[e]), y = __bfloat162float(kr[e + half]);
+    const float2 cs = rope[(int64_t)a.tok_pos[t] * half + e];
+    float *kd = a.k_dst + ((int64_t)t * a.n_kv_heads + head) * hd;
+    kd[e] = x * cs.x + y * cs.y;
+    kd[e + half] = y * cs.x - x * cs.y;
+  }
+  for (int it = threadIdx.x; it < pg.n_tok * hd; it += blockDim.x) {
+    const int i = it % pg.n_tok, d = it / pg.n_tok;  // token-fastest: coalesced V^T reads
+    a.v_dst[((int64_t)(pg.tok0 + i) * a.n_kv_heads + head) * hd + d] =
+        __bfloat162float(vs[(int64_t)d * a.src_rows + pg.row0 + i]);
+  }
+}
+
 // table[p][i] = (cos, sin)((pos0 + p) * inv_freq[i]), angle formed in float64
 // (model.rope_angles, model.py:205-209), rounded once to float32.
 __global__ void rope_table_kernel(float2 *table, int64_t rows, const double *inv_freq, int half, int64_t pos0) {
@@ -101,6 +130,21 @@ extern "C" int dbsa_kv_write(const DbsaKvWriteArgs *args, void *stream) {
   dim3 grid(a.n_pages, a.n_kv_heads);
   kv_write_kernel<<<grid, 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(a);
   return check_launch("kv_write");
+}
+
+extern "C" int dbsa_kv_read(const DbsaKvReadArgs *args, void *stream) {
+  using namespace dbsa;
+  if (!args) return set_error(DBSA_ERR_VALIDATION, "dbsa_kv_read: null args");
+  const DbsaKvReadArgs &a = *args;
+  if (a.n_pages < 0) return set_error(DBSA_ERR_VALIDATION, "n_pages < 0");
+  if (a.n_pages == 0) return DBSA_OK;
+  if (!(a.hd_pad == 16 || a.hd_pad == 32 || a.hd_pad == 64 || a.hd_pad == 128) || a.head_dim > a.hd_pad ||
+      a.head_dim % 2)
+    return set_error(DBSA_ERR_CONFIG, "bad head_dim %d / hd_pad %d", a.head_dim, a.hd_pad);
+  if (a.layer < 0 || a.layer >= a.src_layers) return set_error(DBSA_ERR_VALIDATION, "layer out of range");
+  dim3 grid(a.n_pages, a.n_kv_heads);
+  kv_read_kernel<<<grid, 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(a);
+  return check_launch("kv_read");
 }
 
 extern "C" int dbsa_rope_table(float *table, int64_t rows, const double *inv_freq, int32_t half, int64_t pos0,

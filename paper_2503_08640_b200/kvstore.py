@@ -28,7 +28,10 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import model
-from .errors import CompatibilityError, ShapeError, ValidationError
+from .errors import CompatibilityError, FormatError, ShapeError, ValidationError
+
+CACHE_MAGIC = b"DBSACACH"  # on-disk format of kvstore.py:238-316
+CACHE_VERSION = 1
 
 BLOCK_GRANULARITY = "block"
 EXAMPLE_GRANULARITY = "example"
@@ -286,3 +289,121 @@ def storage_bytes(config: model.ModelConfig, n_tokens: int, bytes_per_value: int
 def check_compatible(cache: SegmentedKVCache, config: model.ModelConfig) -> None:
     if cache.config_hash != config.hash_bytes():
         raise CompatibilityError("cache and weights were built for different configs")
+
+
+# ------------------------------------------------------------------ cache files
+# Byte-compatible with the reference's DBSACACH format (kvstore.py:238-316):
+# header, block table, then per layer, per group, float32 pre-rotation K
+# followed by V in [t, Hkv, hd] order.  Pages are read/written on the GPU: K2r
+# un-rotates a whole layer of pages in one launch, and K2w writes a whole
+# layer from the file in one launch.
+def _header_bytes(cache) -> bytes:
+    import struct
+
+    cfg = cache.config
+    out = [CACHE_MAGIC, struct.pack("<I", CACHE_VERSION), cache.config_hash,
+           struct.pack("<III", cfg.n_layers, cfg.n_kv_heads, cfg.head_dim), struct.pack("<I", cache.n_blocks)]
+    for e in cache.blocks:
+        out.append(struct.pack("<IIQQ", e.block_id, e.token_count, e.pos_start, e.pos_end))
+        out.append(e.text_digest)
+        out.append(struct.pack("<I", len(e.example_spans)))
+        out += [struct.pack("<II", a, b) for a, b in e.example_spans]
+    return b"".join(out)
+
+
+def serialize(cache: SegmentedKVCache, path) -> None:
+    """Write the cache in the reference's file format (kvstore.py:238-258)."""
+    import torch
+
+    from . import engine, ops
+
+    cfg = cache.config
+    if any(e.row0 < 0 for e in cache.blocks):
+        raise ValidationError("a group-sharded cache holds only part of the pool; serialize each owner's groups")
+    store, dev = cache.store, cache.device
+    total = cache.total_tokens
+    pos = torch.arange(total, dtype=torch.int32, device=dev)
+    pages = engine._pages_for([(e.pos_start, e.token_count, e.row0) for e in cache.blocks])
+    pdev = ops.to_device(pages, dev)
+    k = torch.empty((total, cfg.n_kv_heads, cfg.head_dim), dtype=torch.float32, device=dev)
+    v = torch.empty_like(k)
+    with open(path, "wb") as fh:
+        fh.write(_header_bytes(cache))
+        for layer in range(cfg.n_layers):
+            ops.kv_read(store.k, store.v, store.rows, cfg.n_layers, layer, pos, store.rope, pdev, len(pages),
+                        cfg.n_kv_heads, cfg.head_dim, k, v)
+            kh, vh = k.cpu().numpy(), v.cpu().numpy()
+            for e in cache.blocks:
+                fh.write(np.ascontiguousarray(kh[e.pos_start:e.pos_end], dtype="<f4").tobytes())
+                fh.write(np.ascontiguousarray(vh[e.pos_start:e.pos_end], dtype="<f4").tobytes())
+
+
+def deserialize(path, config: model.ModelConfig, device=None) -> SegmentedKVCache:
+    """Read a reference-format cache file straight into HBM pages
+    (kvstore.py:261-316): same validation and exceptions."""
+    import struct
+
+    import torch
+
+    from . import engine, ops
+
+    def read(fh, n: int, what: str) -> bytes:
+        data = fh.read(n)
+        if len(data) != n:
+            raise FormatError(f"truncated cache file while reading {what}")
+        return data
+
+    with open(path, "rb") as fh:
+        if read(fh, 8, "magic") != CACHE_MAGIC:
+            raise FormatError("not a KV cache file (bad magic)")
+        (version,) = struct.unpack("<I", read(fh, 4, "version"))
+        if version != CACHE_VERSION:
+            raise FormatError(f"unsupported cache file version {version}")
+        if read(fh, 32, "config hash") != config.hash_bytes():
+            raise CompatibilityError("cache file was built for a different model config")
+        dims = struct.unpack("<III", read(fh, 12, "dims"))
+        if dims != (config.n_layers, config.n_kv_heads, config.head_dim):
+            raise CompatibilityError("cache dims disagree with model config")
+        (n_blocks,) = struct.unpack("<I", read(fh, 4, "block count"))
+        table = []
+        for _ in range(n_blocks):
+            bid, count, start, end = struct.unpack("<IIQQ", read(fh, 24, "block entry"))
+            digest = read(fh, 32, "digest")
+            (n_spans,) = struct.unpack("<I", read(fh, 4, "span count"))
+            spans = tuple(struct.unpack("<II", read(fh, 8, "span")) for _ in range(n_spans))
+            table.append((bid, count, start, end, digest, spans))
+        expect_start = 0
+        for i, (bid, count, start, end, _, _) in enumerate(table):
+            if bid != i or start != expect_start or end != start + count or count <= 0:
+                raise FormatError(f"inconsistent block table entry {i}")
+            expect_start = end
+        cache = SegmentedKVCache(config, device, capacity_tokens=expect_start)
+        entries = cache._reserve([t[1] for t in table], [t[4] for t in table], [t[5] for t in table])
+        total, per_tok = expect_start, config.n_kv_heads * config.head_dim
+        dev = cache.device
+        pos = torch.arange(total, dtype=torch.int32, device=dev)
+        pages = engine._pages_for([(e.pos_start, e.token_count, e.row0) for e in entries])
+        pdev = ops.to_device(pages, dev)
+        st = cache.store
+        for layer in range(config.n_layers):
+            kb = np.empty((total, per_tok), np.float32)
+            vb = np.empty((total, per_tok), np.float32)
+            for e in entries:
+                n_vals = e.token_count * per_tok
+                kb[e.pos_start:e.pos_end] = np.frombuffer(read(fh, 4 * n_vals, "keys"), "<f4").reshape(-1, per_tok)
+                vb[e.pos_start:e.pos_end] = np.frombuffer(read(fh, 4 * n_vals, "values"), "<f4").reshape(-1, per_tok)
+            kd = torch.from_numpy(kb).to(dev).to(torch.bfloat16)
+            vd = torch.from_numpy(vb).to(dev).to(torch.bfloat16)
+            ops.kv_write(kd, vd, per_tok, pos, st.rope, pdev, len(pages), st.k, st.v, st.rows, config.n_layers,
+                         layer, config.n_kv_heads, config.head_dim)
+        if fh.read(1):
+            raise FormatError("trailing bytes after final segment")
+    torch.cuda.current_stream(dev).synchronize()
+    return cache.seal()
+
+
+def expected_file_size(config: model.ModelConfig, token_counts, spans_per_block) -> int:
+    """Bytes `serialize` writes (kvstore.py:319-324)."""
+    header = 8 + 4 + 32 + 12 + 4
+    table = sum(24 + 32 + 4 + 8 * len(s) if not isinstance(s, int) else 24 + 32 + 4 + 8 * s for s in spans_per_block)
+    return header + table + 2 * config.n_layers * config.n_kv_heads * config.head_dim * 4 * sum(token_counts)

@@ -97,6 +97,17 @@ def kv_write(k_src, v_src, src_tok_stride, tok_pos, rope, pages_dev, n_pages, k_
     _launched()
 
 
+def kv_read(k_planes, v_planes, rows, layers, layer, tok_pos, rope, pages_dev, n_pages, n_kv_heads, head_dim,
+            k_dst, v_dst):
+    """K2r: fp32 pre-rotation K and V (token-major) of a set of pages."""
+    a = nat.KvReadArgs(k_src=k_planes.data_ptr(), v_src=v_planes.data_ptr(), src_rows=rows, src_layers=layers,
+                       layer=layer, tok_pos=tok_pos.data_ptr(), rope_table=rope.data_ptr(), rope_rows=rope.shape[0],
+                       pages=pages_dev.data_ptr(), n_pages=n_pages, n_kv_heads=n_kv_heads, head_dim=head_dim,
+                       hd_pad=hd_pad(head_dim), k_dst=k_dst.data_ptr(), v_dst=v_dst.data_ptr())
+    nat.check(nat.load_library().dbsa_kv_read(ctypes.byref(a), nat.stream_handle()))
+    _launched()
+
+
 def attention(*, q, q_tok_stride, tok_pos, tok_lo, rope, pool, aux, n_heads, n_kv_heads, head_dim,
               works_dev, n_works, segs_dev, num_m, out, out_tok_stride, part_o=None, part_lse=None):
     """Launch K1/K3.  `pool` / `aux` are (k_planes, v_planes, rows, layers)."""

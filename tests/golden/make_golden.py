@@ -111,10 +111,36 @@ def run_case(name: str, spec: dict) -> None:
           f"infer {t_inf:.2f}s for {len(queries)} queries")
 
 
+def make_cache_file() -> None:
+    """A small DBSACACH file written by the reference's serialize
+    (kvstore.py:238-258) for the cache-file parity tests."""
+    from dbsa import kvstore, masks, model, pipeline, synthetic, tokenizer
+
+    spec = CASES["c1"]
+    cfg = model.ModelConfig(vocab_size=tokenizer.VOCAB_SIZE, **spec["model"])
+    weights = model.init_random(cfg, seed=0)
+    data = synthetic.generate_recall_task(n_demos=24, n_tests=2, n_labels=4, seed=3)
+    task = pipeline.TaskSpec(data.pool, data.labels)
+    mc = pipeline.MethodConfig(block_size=4, ratio=0.5, seed=3, granularity="example",
+                               pattern=masks.AttentionPattern.sink_prev_self(2))
+    enc = pipeline.encode_pool(weights, task, mc)
+    kvstore.serialize(enc.cache, OUT / "cache_tiny.dbsacache")
+    meta = dict(model=spec["model"], weight_seed=0, task=dict(n_demos=24, n_tests=2, n_labels=4, seed=3),
+                method=dict(block_size=4, ratio=0.5, seed=3, granularity="example"), n_blocks=enc.cache.n_blocks,
+                total_tokens=enc.cache.total_tokens,
+                file_size=(OUT / "cache_tiny.dbsacache").stat().st_size)
+    (OUT / "cache_tiny.json").write_text(json.dumps(meta, indent=1))
+    print(f"cache_tiny: {enc.cache.n_blocks} blocks, {enc.cache.total_tokens} tokens, {meta['file_size']} bytes")
+
+
 def main(names=None):
     sys.path.insert(0, str(REF))
+    if names == ["cache"]:
+        make_cache_file()
+        return
     for name in names or CASES:
         run_case(name, CASES[name])
+    make_cache_file()
 
 
 if __name__ == "__main__":
