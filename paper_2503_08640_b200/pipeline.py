@@ -273,10 +273,21 @@ class Stage2Session:
         scorer = engine.LabelScorer(self.dm, plan, jobs, len(self.label_ids))
         return scorer(self.dm, h)
 
-    def answer(self, scores: np.ndarray, query_ids_list):
+    def answer(self, scores, query_ids_list, graphed: bool = True):
+        """K4 selection, planning and the scored forward of one batch.  With
+        `graphed`, batches of a shape seen before replay a captured CUDA graph
+        (engine.GraphedStage2) instead of issuing every launch from the host."""
         ids = self.select(scores)
         jobs, plan = self.plan(ids, query_ids_list)
-        s, best = self.run(jobs, plan)
+        if not graphed:
+            s, best = self.run(jobs, plan)
+            return ids, s, best
+        scorer = engine.LabelScorer(self.dm, plan, jobs, len(self.label_ids))
+        key = engine.plan_key(plan, scorer)
+        graphs = self.__dict__.setdefault("_graphs", {})
+        if key not in graphs:
+            graphs[key] = engine.GraphedStage2(self.dm, self.cache.store, jobs, plan, len(self.label_ids))
+        s, best = graphs[key].replay(plan, scorer)
         return ids, s, best
 
 
