@@ -572,6 +572,459 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
   if (warp == 2) tmem_dealloc(tbase, C::TMEM_COLS);
 }
 
+
+// ============================================================================
+// Single-M-tile variant (num_m == 1): one 128-row M tile per CTA, Q held in
+// TMEM (QK is a TS MMA too, so smem carries only K/V and the rings are deep),
+// and S / P double-buffered in TMEM so QK(j+1) runs on the tensor pipe while
+// the softmax warpgroup works on tile j: the softmax never waits for its own
+// next S, which is the chain that bounds the two-tile kernel.
+//   TMEM: O [0, HDP) | S0 [HDP, HDP+128) | S1 [HDP+128, HDP+256) | Q [HDP+256, +HDP/2)
+// ============================================================================
+template <int HDP>
+struct Attn1Cfg {
+  static constexpr int K_BYTES = kBN * HDP * 2;
+  static constexpr int V_BYTES = HDP * kBN * 2;
+  static constexpr int QSW = HDP >= 64 ? 128 : HDP * 2;
+  static constexpr int KATOM = HDP >= 64 ? 64 : HDP;
+  static constexpr int NATOM = HDP / KATOM;
+  static constexpr int BAR_BYTES = 1024;
+  static constexpr int AVAIL = 232448 - 1024 - BAR_BYTES;
+  static constexpr int PAIRS = AVAIL / (K_BYTES + V_BYTES) > 4 ? 4 : AVAIL / (K_BYTES + V_BYTES);
+  static constexpr int KST = PAIRS + ((AVAIL - PAIRS * (K_BYTES + V_BYTES)) >= K_BYTES ? 1 : 0);
+  static constexpr int VST = PAIRS;
+  static constexpr int SMEM = KST * K_BYTES + VST * V_BYTES + BAR_BYTES + 1024;
+  static constexpr int THREADS = 256;
+  static constexpr int T_S0 = HDP, T_Q = HDP + 2 * kBN;
+  static constexpr int TMEM_COLS = 512;
+  static_assert(T_Q + HDP / 2 <= 512, "TMEM budget");
+  static_assert(PAIRS >= 2, "not enough shared memory for a 2-stage pipeline");
+};
+
+// Rotate this thread's query row at rope row (tok_pos - shift) and store it
+// into the TMEM Q columns (row = lane, two bf16 per 32-bit column: the
+// A-operand layout of the TS MMA).
+template <int HDP>
+__device__ __forceinline__ void q_row_to_tmem(const AttnParams &p, uint32_t tq, bool valid, int t, int head,
+                                              int shift) {
+  const int hd = p.head_dim, half = hd >> 1;
+  uint32_t pk[HDP / 2];
+  if (!valid) {
+#pragma unroll
+    for (int i = 0; i < HDP / 2; ++i) pk[i] = 0u;
+  } else {
+    const __nv_bfloat16 *src = p.q + (int64_t)t * p.q_tok_stride + (int64_t)head * hd;
+    const float2 *rp = p.rope + (int64_t)(p.tok_pos[t] - shift) * half;
+    if (HDP >= 32 && hd == HDP && (p.q_tok_stride & 7) == 0) {
+      constexpr int NCH = HDP / 16;  // 8-pair chunks per half of the head
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        const uint4 lo4 = *reinterpret_cast<const uint4 *>(src + c * 8);
+        const uint4 hi4 = *reinterpret_cast<const uint4 *>(src + HDP / 2 + c * 8);
+        float4 cs4[4];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) cs4[v] = reinterpret_cast<const float4 *>(rp + c * 8)[v];
+        const __nv_bfloat16 *lo = reinterpret_cast<const __nv_bfloat16 *>(&lo4);
+        const __nv_bfloat16 *hi = reinterpret_cast<const __nv_bfloat16 *>(&hi4);
+        const float *cs = reinterpret_cast<const float *>(cs4);
+        float a[8], b[8];
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          const float cc = cs[2 * jj], sn = cs[2 * jj + 1];
+          const float x = __bfloat162float(lo[jj]), y = __bfloat162float(hi[jj]);
+          a[jj] = x * cc - y * sn;
+          b[jj] = x * sn + y * cc;
+        }
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          pk[c * 4 + jj] = pack_bf16(a[2 * jj], a[2 * jj + 1]);
+          pk[HDP / 4 + c * 4 + jj] = pack_bf16(b[2 * jj], b[2 * jj + 1]);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int e2 = 0; e2 < HDP / 2; ++e2) {
+        float o2[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int e = 2 * e2 + u;
+          float val = 0.f;
+          if (e < hd) {
+            const int i = e < half ? e : e - half;
+            const float lo = __bfloat162float(src[i]);
+            const float hi = __bfloat162float(src[i + half]);
+            const float2 cs = rp[i];
+            val = e < half ? (lo * cs.x - hi * cs.y) : (lo * cs.y + hi * cs.x);
+          }
+          o2[u] = val;
+        }
+        pk[e2] = pack_bf16(o2[0], o2[1]);
+      }
+    }
+  }
+  if constexpr (HDP / 2 >= 32) {
+#pragma unroll
+    for (int c = 0; c < HDP / 2; c += 32) tmem_st32(tq + c, *reinterpret_cast<const uint32_t(*)[32]>(&pk[c]));
+  } else if constexpr (HDP / 2 == 16) {
+    tmem_st16u(tq, *reinterpret_cast<const uint32_t(*)[16]>(&pk[0]));
+  } else {
+    tmem_st8u(tq, *reinterpret_cast<const uint32_t(*)[8]>(&pk[0]));
+  }
+  tmem_wait_st();
+}
+
+template <int HDP>
+__global__ void __launch_bounds__(256, 1)
+    dbsa_attn1_kernel(const __grid_constant__ CUtensorMap tm_k0, const __grid_constant__ CUtensorMap tm_v0,
+                      const __grid_constant__ CUtensorMap tm_k1, const __grid_constant__ CUtensorMap tm_v1,
+                      const AttnParams p) {
+  using C = Attn1Cfg<HDP>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *sK = smem;                      // KST x K_BYTES
+  uint8_t *sV = sK + C::KST * C::K_BYTES;  // VST x V_BYTES
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sV + C::VST * C::V_BYTES);
+  uint64_t *k_full = bars;
+  uint64_t *k_empty = k_full + C::KST;
+  uint64_t *v_full = k_empty + C::KST;
+  uint64_t *v_empty = v_full + C::VST;
+  uint64_t *s_full = v_empty + C::VST;  // [2] S(j) in buffer j & 1
+  uint64_t *p_full = s_full + 2;        // [2] P(j) over S buffer j & 1
+  uint64_t *q_full = p_full + 2;        // Q staged in TMEM (initially and after each shift change)
+  uint64_t *pv_done = q_full + 1;       // P.V(j) retired (O may be rescaled)
+  uint64_t *o_full = pv_done + 1;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(o_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const DbsaAttnWork w = p.works[blockIdx.x];
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::KST; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+    }
+    for (int s = 0; s < C::VST; ++s) {
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&s_full[b], 1);
+      mbar_init(&p_full[b], 128);
+    }
+    mbar_init(q_full, 128);
+    mbar_init(pv_done, 1);
+    mbar_init(o_full, 1);
+    fence_mbar_init();
+    tma_prefetch(&tm_k0);
+    tma_prefetch(&tm_v0);
+    tma_prefetch(&tm_k1);
+    tma_prefetch(&tm_v1);
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int kj = 0, vj = 0;
+      auto load_v = [&](const DbsaAttnSeg &sg, int row) {
+        const int st = vj % C::VST;
+        if (vj >= C::VST) mbar_wait(&v_empty[st], ((vj / C::VST) & 1) ^ 1);
+        if (p.dbg & 4) {
+          mbar_arrive(&v_full[st]);
+        } else {
+          const CUtensorMap *tv = sg.src ? &tm_v1 : &tm_v0;
+          mbar_arrive_expect_tx(&v_full[st], C::V_BYTES);
+#pragma unroll
+          for (int a = 0; a < 2; ++a)
+            tma_load_4d(sV + st * C::V_BYTES + a * HDP * 128, tv, &v_full[st], row + a * 64, 0, w.kv_head, sg.layer);
+        }
+        ++vj;
+      };
+      DbsaAttnSeg pend_sg{};
+      int pend_row = -1;
+      for (int si = w.seg_begin; si < w.seg_end; ++si) {
+        const DbsaAttnSeg sg = p.segs[si];
+        const int off = sg.row0 & 63;
+        const int nt = (off + sg.n_tok + kBN - 1) / kBN;
+        const CUtensorMap *tk = sg.src ? &tm_k1 : &tm_k0;
+        for (int tt = 0; tt < nt; ++tt) {
+          const int row = sg.row0 - off + tt * kBN;
+          const int st = kj % C::KST;
+          if (kj >= C::KST) mbar_wait(&k_empty[st], ((kj / C::KST) & 1) ^ 1);
+          if (p.dbg & 4) {
+            mbar_arrive(&k_full[st]);
+          } else {
+            mbar_arrive_expect_tx(&k_full[st], C::K_BYTES);
+#pragma unroll
+            for (int a = 0; a < C::NATOM; ++a)
+              tma_load_4d(sK + st * C::K_BYTES + a * kBN * C::QSW, tk, &k_full[st], a * C::KATOM, row, w.kv_head,
+                          sg.layer);
+          }
+          ++kj;
+          if (pend_row >= 0) load_v(pend_sg, pend_row);
+          pend_sg = sg;
+          pend_row = row;
+        }
+      }
+      if (pend_row >= 0) load_v(pend_sg, pend_row);
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA warp
+    constexpr uint32_t idesc_s = umma_idesc_bf16(128, kBN);
+    constexpr uint32_t idesc_o = umma_idesc_bf16(128, HDP);
+    const uint32_t sKa = smem_u32(sK), sVa = smem_u32(sV);
+    int n_tiles = 0;
+    for (int si = w.seg_begin; si < w.seg_end; ++si)
+      n_tiles += ((p.segs[si].row0 & 63) + p.segs[si].n_tok + kBN - 1) / kBN;
+    const bool leader = elect_one();
+    auto commit = [&](uint64_t *bar) {
+      if (leader) umma_commit(bar);
+      __syncwarp();
+    };
+    auto qk = [&](int j) {  // S(j & 1) = Q K(j)^T: A = Q from TMEM, B = K tile (K-major smem)
+      const int st = j % C::KST;
+      const uint32_t d = tbase + C::T_S0 + (j & 1) * kBN;
+      if (leader) {
+#pragma unroll
+        for (int kk = 0; kk < HDP / 16; ++kk) {
+          const int a = (kk * 16) / C::KATOM;
+          const int off = ((kk * 16) % C::KATOM) * 2;
+          const uint64_t bd = umma_desc_kmajor(sKa + st * C::K_BYTES + a * kBN * C::QSW + off, C::QSW);
+          if (!(p.dbg & 2)) umma_bf16_ts(d, tbase + C::T_Q + kk * 8, bd, idesc_s, kk > 0 ? 1u : 0u);
+        }
+      }
+      __syncwarp();
+    };
+    auto pv = [&](int j) {  // O += P(j) V(j): A = P in S buffer j & 1
+      const int st = j % C::VST;
+      const uint32_t pa = tbase + C::T_S0 + (j & 1) * kBN;
+      if (leader) {
+#pragma unroll
+        for (int kk = 0; kk < kBN / 16; ++kk) {
+          const int a = kk / 4, off = (kk % 4) * 32;
+          const uint64_t bd = umma_desc_kmajor(sVa + st * C::V_BYTES + a * HDP * 128 + off, 128);
+          if (!(p.dbg & 2)) umma_bf16_ts(tbase, pa + kk * 8, bd, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+        }
+      }
+      __syncwarp();
+    };
+    if (n_tiles > 0) {
+      // segment iterator for QK(t): a "shift boundary" tile opens a segment whose
+      // RoPE shift differs from the previous one; its QK waits for the re-staged Q
+      int it_seg = w.seg_begin, it_tt = 0;
+      int it_nt = ((p.segs[it_seg].row0 & 63) + p.segs[it_seg].n_tok + kBN - 1) / kBN;
+      int q_phase = 0;
+      auto issue_qk = [&](int t) {
+        bool boundary = false;
+        if (it_tt == it_nt) {
+          const int prev_shift = p.segs[it_seg].shift;
+          ++it_seg;
+          it_tt = 0;
+          it_nt = ((p.segs[it_seg].row0 & 63) + p.segs[it_seg].n_tok + kBN - 1) / kBN;
+          boundary = p.segs[it_seg].shift != prev_shift;
+        }
+        ++it_tt;
+        if (boundary || t == 0) {
+          mbar_wait(q_full, q_phase & 1);
+          ++q_phase;
+        }
+        mbar_wait(&k_full[t % C::KST], (t / C::KST) & 1);
+        tc_fence_after();
+        qk(t);
+        commit(&s_full[t & 1]);
+        commit(&k_empty[t % C::KST]);
+      };
+      issue_qk(0);
+      for (int j = 0; j < n_tiles; ++j) {
+        // QK(j+1) into the other S buffer: its previous P(j-1) was consumed by
+        // P.V(j-1), issued in the last iteration (in-order tensor pipe)
+        if (j + 1 < n_tiles) issue_qk(j + 1);
+        mbar_wait(&p_full[j & 1], (j >> 1) & 1);
+        mbar_wait(&v_full[j % C::VST], (j / C::VST) & 1);
+        tc_fence_after();
+        pv(j);
+        commit(pv_done);
+        commit(&v_empty[j % C::VST]);
+      }
+    }
+    commit(o_full);
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ softmax warpgroup
+    const int q4 = warp & 3;
+    const int trow = q4 * 32 + lane;
+    const int rows = w.n_tok * p.gs;
+    const bool valid = trow < rows;
+    const int t = w.q_tok0 + (valid ? trow / p.gs : 0);
+    const int head = w.kv_head * p.gs + (valid ? trow % p.gs : 0);
+    const int rl = t - w.self_tok0;
+    const int lo = (p.tok_lo && valid) ? p.tok_lo[t] : 0;
+    const uint32_t lane_base = tbase + ((uint32_t)(q4 * 32) << 16);
+    const uint32_t t_o = lane_base;
+    const uint32_t t_q = lane_base + C::T_Q;
+
+    int cur_rot = w.seg_end > w.seg_begin ? p.segs[w.seg_begin].shift : 0;
+    q_row_to_tmem<HDP>(p, t_q, valid, t, head, cur_rot);
+    tc_fence_before();
+    mbar_arrive(q_full);
+
+    const float sl2 = p.scale_log2;
+    const bool warp_dead = __all_sync(0xffffffffu, !valid);
+    float m_used = -INFINITY, l_sum = 0.f;
+    int j = 0;
+    for (int si = w.seg_begin; si < w.seg_end; ++si) {
+      const DbsaAttnSeg sg = p.segs[si];
+      const int off = sg.row0 & 63;
+      const int nt = (off + sg.n_tok + kBN - 1) / kBN;
+      const bool is_self = sg.kind == DBSA_SEG_SELF;
+      int vis_hi = valid ? sg.n_tok : 0;
+      int band_lo = 0, band_hi = 0;
+      if (is_self) {
+        vis_hi = min(vis_hi, rl + 1);
+        band_lo = w.prefix;
+        band_hi = lo;
+      }
+      for (int tt = 0; tt < nt; ++tt, ++j) {
+        const int k0 = tt * kBN - off;
+        const int c_lo = max(0, -k0), c_hi = min(kBN, vis_hi - k0);
+        const int b_lo = band_lo - k0, b_hi = band_hi - k0;
+        const bool full = !valid || (c_lo == 0 && c_hi == kBN && (b_hi <= 0 || b_lo >= kBN || b_lo >= b_hi));
+        const bool restage = tt == nt - 1 && si + 1 < w.seg_end && p.segs[si + 1].shift != cur_rot;
+        const uint32_t t_s = lane_base + C::T_S0 + (j & 1) * kBN;
+        mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+        tc_fence_after();
+        if (restage) {
+          // QK(j) retired (S(j) ready), QK(j+1) waits for q_full: re-stage Q now so
+          // the next tile's QK overlaps this tile's softmax
+          cur_rot = p.segs[si + 1].shift;
+          q_row_to_tmem<HDP>(p, t_q, valid, t, head, cur_rot);
+          tc_fence_before();
+          mbar_arrive(q_full);
+        }
+        if (warp_dead || (p.dbg & 1)) {
+          tc_fence_before();
+          mbar_arrive(&p_full[j & 1]);
+          continue;
+        }
+        float x[kBN];
+#pragma unroll
+        for (int c = 0; c < kBN; c += 32) tmem_ld32(t_s + c, *reinterpret_cast<float(*)[32]>(&x[c]));
+        tmem_wait_ld();
+        if (!__all_sync(0xffffffffu, full)) {
+#pragma unroll
+          for (int c = 0; c < kBN; ++c) {
+            const bool ok = (c >= c_lo) & (c < c_hi) & ((c < b_lo) | (c >= b_hi));
+            x[c] = ok ? x[c] : -INFINITY;
+          }
+        }
+        float mx[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) mx[i] = fmax3(x[i], x[i + 8], x[i + 16]);
+#pragma unroll
+        for (int c = 24; c + 16 < kBN; c += 16)
+#pragma unroll
+          for (int i = 0; i < 8; ++i) mx[i] = fmax3(mx[i], x[c + i], x[c + 8 + i]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) mx[i] = fmaxf(mx[i], x[kBN - 8 + i]);
+        const float tmax = fmax3(fmax3(mx[0], mx[1], mx[2]), fmax3(mx[3], mx[4], mx[5]), fmaxf(mx[6], mx[7])) * sl2;
+        const float m_new = fmaxf(m_used, tmax);
+        const bool need = (m_used != -INFINITY) && (m_new > m_used + 8.f);
+        float alpha = 1.f;
+        if (__any_sync(0xffffffffu, need)) {
+          // O is accumulated by P.V(j-1), issued once P(j-1) arrived: wait for it
+          if (j > 0) mbar_wait(pv_done, (j - 1) & 1);
+          tc_fence_after();
+          if (m_used != -INFINITY) alpha = fast_exp2(m_used - m_new);
+          m_used = m_new;
+#pragma unroll 1
+          for (int c0 = 0; c0 < HDP; c0 += 16) {
+            float o[16];
+            tmem_ld16(t_o + c0, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) o[i] *= alpha;
+            tmem_st16(t_o + c0, o);
+          }
+          tmem_wait_st();
+        } else if (m_used == -INFINITY) {
+          m_used = m_new;
+        }
+        l_sum *= alpha;
+        const float msub = m_used == -INFINITY ? 0.f : m_used;
+        const float2 sl2v = make_float2(sl2, sl2), nmv = make_float2(-msub, -msub);
+        float2 ps[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          uint32_t pk[32];
+#pragma unroll
+          for (int c = 0; c < 64; c += 2) {
+            const float2 a = ffma2(make_float2(x[hh * 64 + c], x[hh * 64 + c + 1]), sl2v, nmv);
+            const float2 e = ((c >> 1) & 3) == 3 ? exp2_fma2(a) : make_float2(fast_exp2(a.x), fast_exp2(a.y));
+            ps[(c >> 1) & 1] = fadd2(ps[(c >> 1) & 1], e);
+            pk[c >> 1] = pack_bf16(e.x, e.y);
+          }
+          tmem_st32(t_s + hh * 32, pk);
+        }
+        const float2 pss = fadd2(ps[0], ps[1]);
+        l_sum += pss.x + pss.y;
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&p_full[j & 1]);
+      }
+    }
+
+    // ------------------------------------------------------------ epilogue
+    mbar_wait(o_full, 0);
+    tc_fence_after();
+    const bool empty = !(l_sum > 0.f);
+    const float inv_l = empty ? 0.f : 1.f / l_sum;
+    const int hd = p.head_dim;
+#pragma unroll 1
+    for (int c0 = 0; c0 < HDP; c0 += 16) {
+      float o[16];
+      tmem_ld16(t_o + c0, o);
+      tmem_wait_ld();
+      if (empty) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) o[i] = 0.f;
+      }
+      if (valid && c0 < hd) {
+        if (w.out_mode == 0) {
+          __nv_bfloat16 *dst = p.out + (int64_t)t * p.out_tok_stride + (int64_t)head * hd + c0;
+          if (hd % 16 == 0) {
+            uint4 *d4 = reinterpret_cast<uint4 *>(dst);
+            d4[0] = make_uint4(pack_bf16(o[0] * inv_l, o[1] * inv_l), pack_bf16(o[2] * inv_l, o[3] * inv_l),
+                               pack_bf16(o[4] * inv_l, o[5] * inv_l), pack_bf16(o[6] * inv_l, o[7] * inv_l));
+            d4[1] = make_uint4(pack_bf16(o[8] * inv_l, o[9] * inv_l), pack_bf16(o[10] * inv_l, o[11] * inv_l),
+                               pack_bf16(o[12] * inv_l, o[13] * inv_l), pack_bf16(o[14] * inv_l, o[15] * inv_l));
+          } else {
+            for (int i = 0; i < 16 && c0 + i < hd; ++i) dst[i] = __float2bfloat16(o[i] * inv_l);
+          }
+        } else {
+          float *dst = p.part_o + (w.part_row0 + trow) * (int64_t)hd + c0;
+          if (hd % 16 == 0) {
+            float4 *d4 = reinterpret_cast<float4 *>(dst);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              d4[i] = make_float4(o[4 * i] * inv_l, o[4 * i + 1] * inv_l, o[4 * i + 2] * inv_l, o[4 * i + 3] * inv_l);
+          } else {
+            for (int i = 0; i < 16 && c0 + i < hd; ++i) dst[i] = o[i] * inv_l;
+          }
+        }
+      }
+    }
+    if (valid && w.out_mode == 1)
+      p.part_lse[w.part_row0 + trow] = l_sum > 0.f ? (m_used + log2f(l_sum)) * 0.69314718055994531f : -INFINITY;
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc(tbase, C::TMEM_COLS);
+}
+
 // ---------------------------------------------------------------- host side
 
 static bool encode_plane_maps(const DbsaAttnArgs &a, const void *k, const void *v, int64_t rows, int layers,
@@ -599,6 +1052,22 @@ static bool encode_plane_maps(const DbsaAttnArgs &a, const void *k, const void *
     if (!encode_tiled_bf16(tv, v, 4, dims, strides, box, estr, CU_TENSOR_MAP_SWIZZLE_128B)) return false;
   }
   return true;
+}
+
+template <int HDP>
+static int launch_attn1(const DbsaAttnArgs &a, const AttnParams &p, const CUtensorMap *maps, cudaStream_t s) {
+  using C = Attn1Cfg<HDP>;
+  auto kern = dbsa_attn1_kernel<HDP>;
+  static thread_local bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return set_error(DBSA_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+    attr_set = true;
+  }
+  kern<<<a.n_works, C::THREADS, C::SMEM, s>>>(maps[0], maps[1], maps[2], maps[3], p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(DBSA_ERR_CUDA, "attention launch: %s", cudaGetErrorString(e));
+  return DBSA_OK;
 }
 
 template <int HDP, int NUM_M>
@@ -668,14 +1137,28 @@ extern "C" int dbsa_attention(const DbsaAttnArgs *args, void *stream) {
     p.dbg = e ? atoi(e) : 0;
   }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  // num_m 1 runs the single-M-tile kernel (Q in TMEM, double-buffered S) unless
+  // DBSA_ATTN1=0 selects the one-tile instance of the two-tile kernel
+  static const bool attn1 = [] {
+    const char *e = getenv("DBSA_ATTN1");
+    return !(e && e[0] == '0');
+  }();
+  if (a.num_m == 1 && !attn1) {
+    switch (a.hd_pad) {
+      case 16: return launch_attn<16, 1>(a, p, maps, s);
+      case 32: return launch_attn<32, 1>(a, p, maps, s);
+      case 64: return launch_attn<64, 1>(a, p, maps, s);
+      case 128: return launch_attn<128, 1>(a, p, maps, s);
+    }
+  }
   switch (a.hd_pad * 10 + a.num_m) {
-    case 161: return launch_attn<16, 1>(a, p, maps, s);
+    case 161: return launch_attn1<16>(a, p, maps, s);
     case 162: return launch_attn<16, 2>(a, p, maps, s);
-    case 321: return launch_attn<32, 1>(a, p, maps, s);
+    case 321: return launch_attn1<32>(a, p, maps, s);
     case 322: return launch_attn<32, 2>(a, p, maps, s);
-    case 641: return launch_attn<64, 1>(a, p, maps, s);
+    case 641: return launch_attn1<64>(a, p, maps, s);
     case 642: return launch_attn<64, 2>(a, p, maps, s);
-    case 1281: return launch_attn<128, 1>(a, p, maps, s);
+    case 1281: return launch_attn1<128>(a, p, maps, s);
     case 1282: return launch_attn<128, 2>(a, p, maps, s);
   }
   return set_error(DBSA_ERR_CONFIG, "unsupported attention variant");

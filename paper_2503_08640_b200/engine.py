@@ -36,6 +36,19 @@ PAGE = ops.PAGE
 SEG_FULL, SEG_SELF = nat.SEG_FULL, nat.SEG_SELF
 
 
+def m_tiles(rows_needed: int) -> int:
+    """128-row M tiles per attention work: 2 (two ping-ponged M tiles, Q in
+    smem) or 1 (one M tile, Q in TMEM, double-buffered S).  DBSA_ATTN_TILES
+    forces one kind; the default takes two tiles whenever a slab has more than
+    128 rows."""
+    import os
+
+    forced = os.environ.get("DBSA_ATTN_TILES")
+    if forced in ("1", "2"):
+        return int(forced)
+    return 2 if rows_needed > 128 else 1
+
+
 def _torch():
     import torch
 
@@ -330,7 +343,7 @@ class Stage1Plan:
             acc += e.token_count
         self.n_tok = acc
         longest = max(e.token_count for e in new)
-        self.num_m = 2 if longest * gs > 128 else 1
+        self.num_m = m_tiles(longest * gs)
         slab = (128 * self.num_m) // gs
         if slab < 1:
             raise ConfigError(f"group size {gs} exceeds the 256 rows of one K1 work")
@@ -495,7 +508,7 @@ class NewTokens:
         self.n_new = [len(j.ids) for j in jobs]
         self.tok0 = np.concatenate([[0], np.cumsum(self.n_new)]).astype(np.int64)
         self.n_tok = int(self.tok0[-1])
-        self.num_m = 2 if max(self.n_new) * gs > 128 else 1
+        self.num_m = m_tiles(max(self.n_new) * gs)
         self.slab = (128 * self.num_m) // gs
         if self.slab < 1:
             raise ConfigError(f"group size {gs} exceeds the 256 rows of one K3 work")
@@ -937,7 +950,7 @@ def forward_explicit_context(dm, tokens, context):
     pos = torch.tensor(np.asarray(tokens.positions, np.int32), device=dev)
     pages = ops.to_device(_pages_for([(0, t, self_row)]), dev)
     gs = c.group_size
-    num_m = 2 if t * gs > 128 else 1
+    num_m = m_tiles(t * gs)
     slab = (128 * num_m) // gs
     segs, works = [], []
     for t0 in range(0, t, slab):

@@ -101,7 +101,7 @@ def test_kv_write_pages(hd, H, Hkv):
             assert pool.kp[layer, :, r0:r0 + n, hd:].abs().sum().item() == 0
 
 
-def _stage1_case(hd, H, Hkv, lengths, j=2, layer=0, layers=1):
+def _stage1_case(hd, H, Hkv, lengths, j=2, layer=0, layers=1, num_m=None):
     """Encode every group against sink + prev-j + self (masks.py:80-99) in one launch."""
     dev = "cuda"
     gs = H // Hkv
@@ -109,7 +109,7 @@ def _stage1_case(hd, H, Hkv, lengths, j=2, layer=0, layers=1):
     T = sum(lengths)
     g = torch.Generator().manual_seed(3)
     q = torch.randn(T, H, hd, generator=g).to(torch.bfloat16)
-    num_m = 2 if gs * 16 > 128 else 1
+    num_m = num_m or (2 if gs * 16 > 128 else 1)
     slab_tok = (128 * num_m) // gs
     works, segs = [], []
     for b, n in enumerate(lengths):
@@ -157,9 +157,11 @@ def _stage1_case(hd, H, Hkv, lengths, j=2, layer=0, layers=1):
     return worst
 
 
+@pytest.mark.parametrize("num_m", [1, 2])
 @pytest.mark.parametrize("hd,H,Hkv", [(128, 8, 2), (128, 4, 4), (64, 8, 2), (16, 4, 2), (32, 6, 3), (8, 4, 2)])
-def test_stage1_block_sparse_attention(hd, H, Hkv):
-    worst = _stage1_case(hd, H, Hkv, [150, 64, 97, 200, 33])
+def test_stage1_block_sparse_attention(hd, H, Hkv, num_m):
+    """num_m 1: single-M-tile kernel (Q in TMEM); 2: two ping-ponged M tiles."""
+    worst = _stage1_case(hd, H, Hkv, [150, 64, 97, 200, 33], num_m=num_m)
     assert worst < 2e-2, worst
 
 
@@ -260,8 +262,10 @@ def _stage2_case(hd, H, Hkv, lengths, sel, n_q, labels, splits, theta=10000.0):
 
 @pytest.mark.parametrize("splits", [1, 2, 3])
 @pytest.mark.parametrize("hd,H,Hkv,theta", [(128, 8, 2, 500000.0), (16, 4, 2, 10000.0), (64, 4, 4, 10000.0)])
-def test_stage2_split_kv_attention(hd, H, Hkv, theta, splits):
-    worst = _stage2_case(hd, H, Hkv, [100, 64, 300, 77, 150, 90], sel=[0, 2, 3, 5], n_q=20, labels=[4, 6, 3, 5],
+@pytest.mark.parametrize("n_q,labels", [(20, [4, 6, 3, 5]), (10, [3, 4, 2, 3])])
+def test_stage2_split_kv_attention(hd, H, Hkv, theta, splits, n_q, labels):
+    """(20, ...) runs the two-M-tile kernel at gs 4, (10, ...) the single-M-tile one."""
+    worst = _stage2_case(hd, H, Hkv, [100, 64, 300, 77, 150, 90], sel=[0, 2, 3, 5], n_q=n_q, labels=labels,
                          splits=splits, theta=theta)
     assert worst < 2e-2, worst
 
