@@ -512,7 +512,13 @@ class NewTokens:
         self.slab = (128 * self.num_m) // gs
         if self.slab < 1:
             raise ConfigError(f"group size {gs} exceeds the 256 rows of one K3 work")
-        self.slabs = [[(t0, min(self.slab, n - t0)) for t0 in range(0, n, self.slab)] for n in self.n_new]
+        # balanced slabs: ceil(n / slab) pieces of equal size (e.g. 44 tokens -> 22 + 22
+        # rather than 32 + 12 at one M tile, so no work is mostly padding)
+        self.slabs = []
+        for n in self.n_new:
+            k = -(-n // self.slab)
+            size = -(-n // k)
+            self.slabs.append([(t0, min(size, n - t0)) for t0 in range(0, n, size)])
         self.aux_row0 = np.concatenate([[0], np.cumsum([_round_page(n) for n in self.n_new])]).astype(np.int64)
         self.aux_rows = int(self.aux_row0[-1])
         dev = dm.device
