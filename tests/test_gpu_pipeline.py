@@ -236,3 +236,54 @@ def test_gpu_bm25_bit_exact(name):
     ids = runner.session().select(enc.index.score_matrix_device(terms[: len(meta["queries"])]))
     for qi in range(len(meta["queries"])):
         np.testing.assert_array_equal(ids[qi], a[f"q{qi}_units"])
+
+
+@pytest.mark.parametrize("kind,j", [("full", 2), ("sink-self", 2), ("self", 2), ("sink-prev-self", 0),
+                                    ("sink-prev-self", 3)])
+def test_stage1_patterns_vs_oracle(kind, j):
+    """Every AttentionPattern of the reference (masks.py:15-54) through K1 vs
+    the oracle's sequential f32 stage 1 on the same groups; pair counts exact."""
+    from golden_util import load as gload
+
+    meta, _ = gload("c1")
+    cfg = P.ModelConfig(vocab_size=tokenizer.VOCAB_SIZE, **meta["spec"]["model"])
+    w = P.init_random(cfg, 0)
+    pool, _, _ = O.recall_task(40, 1, 4, 5)
+    task = P.TaskSpec(tuple(P.Demonstration(q, x) for q, x in pool), tuple(O.LABEL_WORDS[:4]))
+    pattern = masks.AttentionPattern(kind, j)
+    mc = P.MethodConfig(block_size=6, ratio=0.5, seed=5, pattern=pattern)
+    enc = P.encode_pool(w, task, mc)
+    oc = O.Cfg(**meta["spec"]["model"])
+    ow = O.init_random(oc, 0)
+    rendered = [pipeline.render_block(task.template, task.pool, m) for m in enc.partition.blocks]
+    kv, attended = O.encode_blocks(oc, ow, [ids for _, ids, _ in rendered], kind, j)
+    assert attended == enc.metrics.attended_tokens[0]
+    bm = masks.build_block_mask(enc.cache.n_blocks, pattern)
+    assert attended == masks.count_allowed_token_pairs(bm, [e.token_count for e in enc.cache.blocks])
+    worst = 0.0
+    for layer in range(cfg.n_layers):
+        for b in range(enc.cache.n_blocks):
+            k, v = enc.cache.segment(layer, b)
+            worst = max(worst, float(np.abs(k - kv[layer][b][0]).max()), float(np.abs(v - kv[layer][b][1]).max()))
+    assert worst < KV_TOL, worst
+
+
+@pytest.mark.parametrize("ordering", ["in-order", "low-to-high", "reverse"])
+@pytest.mark.parametrize("ratio", [0.01, 1.0])
+def test_stage2_orderings_and_extreme_ratios(ordering, ratio):
+    """Anchor-only (ratio -> budget 1: few-shot ICL) and the whole pool, every
+    ordering: K4 ids bit-exact with select + order, labels equal the oracle's."""
+    meta, a, w, task, mc0, enc = _encoded("c1")
+    mc = P.MethodConfig(block_size=16, ratio=ratio, seed=0, ordering=ordering)
+    runner = P.Runner(w, enc.cache, enc.index, task, mc)
+    texts = [q["query"] for q in meta["queries"][:6]]
+    out = runner.infer_batch(texts)
+    st = oracle_pool("c1")
+    for t, (lab, qm) in zip(texts, out):
+        want = retrieval.order(retrieval.select(enc.index, t, ratio), ordering)
+        label, scores, units, n_ctx = O.infer(st["cfg"], st["weights"], st["kv"], st["index"], st["refs"],
+                                              st["labels"], t, ratio, ordering)
+        assert list(want.unit_ids) == units
+        if lab != label:
+            srt = np.sort(scores)
+            assert srt[-1] - srt[-2] < 0.05
