@@ -424,10 +424,63 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = cpu_reference_sample(steps=1, seconds=args.cpu_seconds)
         line["cpu_baseline"] = cb
+    if rank == 0 and world == 1 and not args.no_extras:
+        line["c1_end_to_end"] = c1_end_to_end(dev)
     if rank == 0:
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
+
+
+def c1_end_to_end(dev):
+    """BASELINE.json config C1 (the reference's own tiny model) end to end,
+    both ways on this box: the CPU oracle's full pipeline (a restatement of the
+    reference, pinned to its goldens) vs the GPU API -- stage-1 encode_pool and
+    stage-2 answers for the 32 test queries."""
+    import torch
+
+    import paper_2503_08640_b200 as P
+    from oracle import dbsa_oracle as O
+    from paper_2503_08640_b200 import tokenizer
+
+    spec = dict(d_model=64, n_layers=2, n_heads=4, n_kv_heads=2, head_dim=16, ffn_dim=128)
+    pool, tests, labels = O.recall_task(256, 32, 4, 0)
+    oc = O.Cfg(**spec)
+    ow = O.init_random(oc, 0)
+    t0 = time.perf_counter()
+    part, kv, attended, index, refs, counts = O.encode_pool(oc, ow, pool, 16, 0)
+    cpu_enc = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    cpu_labels = [O.infer(oc, ow, kv, index, refs, labels, q, 0.3)[0] for q, _ in tests]
+    cpu_inf = time.perf_counter() - t0
+    cfg = P.ModelConfig(vocab_size=tokenizer.VOCAB_SIZE, **spec)
+    w = P.init_random(cfg, 0)
+    task = P.TaskSpec(tuple(P.Demonstration(q, a) for q, a in pool), tuple(labels))
+    mc = P.MethodConfig(block_size=16, ratio=0.3, seed=0)
+    P.encode_pool(w, task, mc)  # warm-up
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    enc = P.encode_pool(w, task, mc)
+    torch.cuda.synchronize()
+    gpu_enc = time.perf_counter() - t0
+    runner = P.Runner(w, enc.cache, enc.index, task, mc)
+    runner.infer_batch([q for q, _ in tests])  # warm-up (graph capture)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    out = runner.infer_batch([q for q, _ in tests])
+    torch.cuda.synchronize()
+    gpu_inf = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    single = [runner.infer(q)[0] for q, _ in tests[:8]]
+    gpu_single = (time.perf_counter() - t0) / 8
+    n_tok = sum(counts)
+    return {"config": "C1: CLI init-model defaults, 256 demos in groups of 16 (10,351 tokens), 30%, 32 queries",
+            "cpu_oracle": {"encode_tok_s": n_tok / cpu_enc, "ms_per_query": cpu_inf * 1e3 / len(tests),
+                           "cores": len(os.sched_getaffinity(0))},
+            "gpu": {"encode_tok_s": n_tok / gpu_enc, "ms_per_query_batched": gpu_inf * 1e3 / len(tests),
+                    "ms_per_query_single": gpu_single * 1e3},
+            "labels_identical": [lab for lab, _ in out] == cpu_labels, "single_equals_batched": single ==
+            [lab for lab, _ in out][:8]}
 
 
 # ------------------------------------------------------------------ CPU reference arm
