@@ -77,6 +77,7 @@ struct AttnParams {
   int32_t n_heads, n_kv_heads, head_dim, gs;
   float scale_log2;
   const DbsaAttnWork *works;
+  int32_t n_works;
   const DbsaAttnSeg *segs;
   __nv_bfloat16 *out;
   int64_t out_tok_stride;
@@ -193,6 +194,9 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
     dbsa_attn_kernel(const __grid_constant__ CUtensorMap tm_k0, const __grid_constant__ CUtensorMap tm_v0,
                      const __grid_constant__ CUtensorMap tm_k1, const __grid_constant__ CUtensorMap tm_v1,
                      const AttnParams p) {
+  // Persistent: CTA b runs works b, b + gridDim.x, ...  The K/V rings, TMEM and
+  // every barrier carry over from one work to the next, so the next work's
+  // K/V loads and first QK overlap this work's epilogue.
   using C = AttnCfg<HDP, NUM_M>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -204,15 +208,16 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
   uint64_t *k_empty = k_full + C::KST;        // [KST]
   uint64_t *v_full = k_empty + C::KST;        // [VST]
   uint64_t *v_empty = v_full + C::VST;        // [VST]
-  uint64_t *q_full = v_empty + C::VST;        // [NUM_M]
+  uint64_t *q_full = v_empty + C::VST;        // [NUM_M]  Q(m) staged for the next work
   uint64_t *s_full = q_full + NUM_M;          // [NUM_M]  S(m, j) in TMEM
   uint64_t *p_full = s_full + NUM_M;          // [NUM_M]  P(m, j) in TMEM (S consumed)
-  uint64_t *o_full = p_full + NUM_M;          // [NUM_M]
+  uint64_t *o_full = p_full + NUM_M;          // [NUM_M]  O(m) of a work complete
   uint64_t *q_ready = o_full + NUM_M;         // [NUM_M]  Q(m) re-staged for a new RoPE shift
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(q_ready + NUM_M);
+  uint64_t *o_free = q_ready + NUM_M;         // [NUM_M]  O(m) read by the epilogue (TMEM reusable)
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(o_free + NUM_M);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const DbsaAttnWork w = p.works[blockIdx.x];
+  const int n_works = p.n_works;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::KST; ++s) {
@@ -229,6 +234,7 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
       mbar_init(&p_full[m], 128);
       mbar_init(&o_full[m], 1);
       mbar_init(&q_ready[m], 128);
+      mbar_init(&o_free[m], 128);
     }
     fence_mbar_init();
     tma_prefetch(&tm_k0);
@@ -247,59 +253,61 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
     if (lane == 0) {
       // K(t) is issued one tile ahead of V(t - 1): QK needs K early, P.V needs V late.
       int kj = 0, vj = 0;
-      auto load_v = [&](const DbsaAttnSeg &sg, int row) {
+      int pend_src = 0, pend_layer = 0, pend_kv = 0, pend_row = -1;
+      auto load_v = [&]() {
         const int st = vj % C::VST;
         if (vj >= C::VST) mbar_wait(&v_empty[st], ((vj / C::VST) & 1) ^ 1);
         if (p.dbg & 4) {
           mbar_arrive(&v_full[st]);
         } else {
-          const CUtensorMap *tv = sg.src ? &tm_v1 : &tm_v0;
+          const CUtensorMap *tv = pend_src ? &tm_v1 : &tm_v0;
           mbar_arrive_expect_tx(&v_full[st], C::V_BYTES);
 #pragma unroll
           for (int a = 0; a < 2; ++a)
-            tma_load_4d(sV + st * C::V_BYTES + a * HDP * 128, tv, &v_full[st], row + a * 64, 0, w.kv_head, sg.layer);
+            tma_load_4d(sV + st * C::V_BYTES + a * HDP * 128, tv, &v_full[st], pend_row + a * 64, 0, pend_kv,
+                        pend_layer);
         }
         ++vj;
       };
-      DbsaAttnSeg pend_sg{};
-      int pend_row = -1;
-      for (int si = w.seg_begin; si < w.seg_end; ++si) {
-        const DbsaAttnSeg sg = p.segs[si];
-        const int off = sg.row0 & 63;  // tiles start on 64-row page boundaries
-        const int nt = (off + sg.n_tok + kBN - 1) / kBN;
-        const CUtensorMap *tk = sg.src ? &tm_k1 : &tm_k0;
-        for (int tt = 0; tt < nt; ++tt) {
-          const int row = sg.row0 - off + tt * kBN;
-          const int st = kj % C::KST;
-          if (kj >= C::KST) mbar_wait(&k_empty[st], ((kj / C::KST) & 1) ^ 1);
-          if (p.dbg & 4) {
-            mbar_arrive(&k_full[st]);
-          } else {
-            mbar_arrive_expect_tx(&k_full[st], C::K_BYTES);
+      for (int wi = blockIdx.x; wi < n_works; wi += gridDim.x) {
+        const DbsaAttnWork w = p.works[wi];
+        for (int si = w.seg_begin; si < w.seg_end; ++si) {
+          const DbsaAttnSeg sg = p.segs[si];
+          const int off = sg.row0 & 63;  // tiles start on 64-row page boundaries
+          const int nt = (off + sg.n_tok + kBN - 1) / kBN;
+          const CUtensorMap *tk = sg.src ? &tm_k1 : &tm_k0;
+          for (int tt = 0; tt < nt; ++tt) {
+            const int row = sg.row0 - off + tt * kBN;
+            const int st = kj % C::KST;
+            if (kj >= C::KST) mbar_wait(&k_empty[st], ((kj / C::KST) & 1) ^ 1);
+            if (p.dbg & 4) {
+              mbar_arrive(&k_full[st]);
+            } else {
+              mbar_arrive_expect_tx(&k_full[st], C::K_BYTES);
 #pragma unroll
-            for (int a = 0; a < C::NATOM; ++a)
-              tma_load_4d(sK + st * C::K_BYTES + a * kBN * C::QSW, tk, &k_full[st], a * C::KATOM, row, w.kv_head,
-                          sg.layer);
+              for (int a = 0; a < C::NATOM; ++a)
+                tma_load_4d(sK + st * C::K_BYTES + a * kBN * C::QSW, tk, &k_full[st], a * C::KATOM, row, w.kv_head,
+                            sg.layer);
+            }
+            ++kj;
+            if (pend_row >= 0) load_v();
+            pend_src = sg.src;
+            pend_layer = sg.layer;
+            pend_kv = w.kv_head;
+            pend_row = row;
           }
-          ++kj;
-          if (pend_row >= 0) load_v(pend_sg, pend_row);
-          pend_sg = sg;
-          pend_row = row;
         }
       }
-      if (pend_row >= 0) load_v(pend_sg, pend_row);
+      if (pend_row >= 0) load_v();
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA warp
     constexpr uint32_t idesc_s = umma_idesc_bf16(128, kBN);
     constexpr uint32_t idesc_o = umma_idesc_bf16(128, HDP);
     const uint32_t sQa = smem_u32(sQ), sKa = smem_u32(sK), sVa = smem_u32(sV);
-    int n_tiles = 0;
-    for (int si = w.seg_begin; si < w.seg_end; ++si)
-      n_tiles += ((p.segs[si].row0 & 63) + p.segs[si].n_tok + kBN - 1) / kBN;
     const bool leader = elect_one();
-    auto qk = [&](int m, int j) {  // S(m) = Q(m) K(j)^T, K = head_dim
-      const int st = j % C::KST;
+    auto qk = [&](int m, int jg) {  // S(m) = Q(m) K(jg)^T, K = head_dim
+      const int st = jg % C::KST;
       const uint32_t d = tbase + NUM_M * HDP + m * kBN;
       if (leader) {
 #pragma unroll
@@ -314,17 +322,17 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
       }
       __syncwarp();
     };
-    auto pv = [&](int m, int j) {  // O(m) += P(m, j) V(j), K = kBN keys, P from TMEM
-      const int st = j % C::VST;
+    auto pv = [&](int m, int jg, bool first) {  // O(m) (+)= P(m, jg) V(jg), P from TMEM
+      const int st = jg % C::VST;
       const uint32_t d = tbase + m * HDP;
       const uint32_t pa = tbase + NUM_M * HDP + m * kBN;
       if (leader) {
 #pragma unroll
         for (int kk = 0; kk < kBN / 16; ++kk) {
-          const int a = kk / 4;             // 64-key atom column
-          const int off = (kk % 4) * 32;    // byte offset inside the 128-byte atom row
+          const int a = kk / 4;
+          const int off = (kk % 4) * 32;
           const uint64_t bd = umma_desc_kmajor(sVa + st * C::V_BYTES + a * HDP * 128 + off, 128);
-          if (!(p.dbg & 2)) umma_bf16_ts(d, pa + kk * 8, bd, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+          if (!(p.dbg & 2)) umma_bf16_ts(d, pa + kk * 8, bd, idesc_o, (!first || kk > 0) ? 1u : 0u);
         }
       }
       __syncwarp();
@@ -333,57 +341,72 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
       if (leader) umma_commit(bar);
       __syncwarp();
     };
-    if (n_tiles > 0) {
-      for (int m = 0; m < NUM_M; ++m) mbar_wait(&q_full[m], 0);
+    int jg = 0;        // global tile counter (ring slots and per-tile barrier phases)
+    int n_bound = 0;   // RoPE-shift boundaries seen (q_ready phases)
+    int wk = 0;        // works done by this CTA (q_full / o_full / o_free phases)
+    for (int wi = blockIdx.x; wi < n_works; wi += gridDim.x, ++wk) {
+      const DbsaAttnWork w = p.works[wi];
+      int n_tiles = 0;
+      for (int si = w.seg_begin; si < w.seg_end; ++si)
+        n_tiles += ((p.segs[si].row0 & 63) + p.segs[si].n_tok + kBN - 1) / kBN;
+      for (int m = 0; m < NUM_M; ++m) mbar_wait(&q_full[m], wk & 1);
       tc_fence_after();
-      // segment iterator: tile j is a "shift boundary" when it opens a segment
-      // whose RoPE shift differs from the previous segment's -- QK(m, j) must
-      // then wait for the softmax warps to re-stage Q(m) (q_ready), while
-      // P.V(m, j-1) does not.
-      int it_seg = w.seg_begin, it_tt = 0;
-      int it_nt = ((p.segs[it_seg].row0 & 63) + p.segs[it_seg].n_tok + kBN - 1) / kBN;
-      int n_bound = 0;
-      for (int j = 0; j < n_tiles; ++j) {
-        bool boundary = false;
-        if (it_tt == it_nt) {  // advance to the next segment
-          const int prev_shift = p.segs[it_seg].shift;
-          ++it_seg;
-          it_tt = 0;
-          it_nt = ((p.segs[it_seg].row0 & 63) + p.segs[it_seg].n_tok + kBN - 1) / kBN;
-          boundary = p.segs[it_seg].shift != prev_shift;
+      if (n_tiles > 0) {
+        // segment iterator: tile j is a "shift boundary" when it opens a segment
+        // whose RoPE shift differs from the previous segment's -- QK(m, j) must
+        // then wait for the softmax warps to re-stage Q(m) (q_ready), while
+        // P.V(m, j-1) does not.
+        int it_seg = w.seg_begin, it_tt = 0;
+        int it_nt = ((p.segs[it_seg].row0 & 63) + p.segs[it_seg].n_tok + kBN - 1) / kBN;
+        for (int j = 0; j < n_tiles; ++j) {
+          bool boundary = false;
+          if (it_tt == it_nt) {
+            const int prev_shift = p.segs[it_seg].shift;
+            ++it_seg;
+            it_tt = 0;
+            it_nt = ((p.segs[it_seg].row0 & 63) + p.segs[it_seg].n_tok + kBN - 1) / kBN;
+            boundary = p.segs[it_seg].shift != prev_shift;
+          }
+          ++it_tt;
+          const int t = jg + j;
+          mbar_wait(&k_full[t % C::KST], (t / C::KST) & 1);
+          tc_fence_after();
+          for (int m = 0; m < NUM_M; ++m) {
+            if (j > 0) {
+              // P(m, j-1) ready (and S(m) free): accumulate it, then reuse S(m) for tile j
+              mbar_wait(&p_full[m], (t - 1) & 1);
+              if (m == 0) mbar_wait(&v_full[(t - 1) % C::VST], ((t - 1) / C::VST) & 1);
+              if (j == 1 && wk > 0) mbar_wait(&o_free[m], (wk - 1) & 1);  // previous work's O was read
+              tc_fence_after();
+              pv(m, t - 1, j == 1);
+              if (m == NUM_M - 1) commit(&v_empty[(t - 1) % C::VST]);
+            }
+            if (boundary) {
+              mbar_wait(&q_ready[m], n_bound & 1);
+              tc_fence_after();
+            }
+            qk(m, t);
+          }
+          n_bound += boundary;
+          commit(&k_empty[t % C::KST]);
         }
-        ++it_tt;
-        mbar_wait(&k_full[j % C::KST], (j / C::KST) & 1);
-        tc_fence_after();
+        const int t = jg + n_tiles - 1;
         for (int m = 0; m < NUM_M; ++m) {
-          if (j > 0) {
-            // P(m, j-1) ready (and S(m) free): accumulate it, then reuse S(m) for tile j
-            mbar_wait(&p_full[m], (j - 1) & 1);
-            if (m == 0) mbar_wait(&v_full[(j - 1) % C::VST], ((j - 1) / C::VST) & 1);
-            tc_fence_after();
-            pv(m, j - 1);
-            if (m == NUM_M - 1) commit(&v_empty[(j - 1) % C::VST]);
-          }
-          if (boundary) {
-            mbar_wait(&q_ready[m], n_bound & 1);
-            tc_fence_after();
-          }
-          qk(m, j);
+          mbar_wait(&p_full[m], t & 1);
+          if (m == 0) mbar_wait(&v_full[t % C::VST], (t / C::VST) & 1);
+          if (n_tiles == 1 && wk > 0) mbar_wait(&o_free[m], (wk - 1) & 1);
+          tc_fence_after();
+          pv(m, t, n_tiles == 1);
+          commit(&o_full[m]);
         }
-        n_bound += boundary;
-        commit(&k_empty[j % C::KST]);
+        commit(&v_empty[t % C::VST]);
+        jg += n_tiles;
+      } else {
+        for (int m = 0; m < NUM_M; ++m) {
+          if (wk > 0) mbar_wait(&o_free[m], (wk - 1) & 1);
+          commit(&o_full[m]);
+        }
       }
-      const int j = n_tiles - 1;
-      for (int m = 0; m < NUM_M; ++m) {
-        mbar_wait(&p_full[m], j & 1);
-        if (m == 0) mbar_wait(&v_full[j % C::VST], (j / C::VST) & 1);
-        tc_fence_after();
-        pv(m, j);
-        commit(&o_full[m]);
-      }
-      commit(&v_empty[j % C::VST]);
-    } else {
-      for (int m = 0; m < NUM_M; ++m) commit(&o_full[m]);
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ softmax warpgroups
@@ -391,178 +414,210 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
     const int q4 = warp & 3;
     const int trow = q4 * 32 + lane;  // row inside the M tile == TMEM lane
     const int r = m * 128 + trow;     // row inside the work
-    const int rows = w.n_tok * p.gs;
-    const bool valid = r < rows;
-    const int t = w.q_tok0 + (valid ? r / p.gs : 0);
-    const int head = w.kv_head * p.gs + (valid ? r % p.gs : 0);
-    const int rl = t - w.self_tok0;
-    const int lo = (p.tok_lo && valid) ? p.tok_lo[t] : 0;
     uint8_t *q_tile = sQ + m * C::Q_BYTES;
     const uint32_t lane_base = tbase + ((uint32_t)(q4 * 32) << 16);
     const uint32_t t_s = lane_base + NUM_M * HDP + m * kBN;
     const uint32_t t_o = lane_base + m * HDP;
-
-    int cur_rot = w.seg_end > w.seg_begin ? p.segs[w.seg_begin].shift : 0;
-    load_q_row<HDP>(p, q_tile, trow, valid, t, head, cur_rot);
-    fence_proxy_async_smem();
-    mbar_arrive(&q_full[m]);
-
-    // Online softmax in the log2 domain; the scale is folded into the exp2
-    // FFMA: p = 2^(x * scale_log2 - m_used).
     const float sl2 = p.scale_log2;
-    const bool warp_dead = __all_sync(0xffffffffu, !valid);
-    float m_used = -INFINITY, l_sum = 0.f;
-    int j = 0;
-    for (int si = w.seg_begin; si < w.seg_end; ++si) {
-      const DbsaAttnSeg sg = p.segs[si];
-      const int off = sg.row0 & 63;
-      const int nt = (off + sg.n_tok + kBN - 1) / kBN;
-      const bool is_self = sg.kind == DBSA_SEG_SELF;
-      // visible local keys of this row: [0, vis_hi) minus the band [band_lo, band_hi)
-      int vis_hi = valid ? sg.n_tok : 0;
-      int band_lo = 0, band_hi = 0;
-      if (is_self) {
-        vis_hi = min(vis_hi, rl + 1);
-        band_lo = w.prefix;
-        band_hi = lo;
-      }
-      for (int tt = 0; tt < nt; ++tt, ++j) {
-        const int k0 = tt * kBN - off;  // local key index of tile column 0
-        const int c_lo = max(0, -k0), c_hi = min(kBN, vis_hi - k0);
-        const int b_lo = band_lo - k0, b_hi = band_hi - k0;
-        // invalid rows (beyond the work's rows) count as full: their S is Q=0 . K = 0
-        // and their P only feeds their own (never stored) O rows
-        const bool full = !valid || (c_lo == 0 && c_hi == kBN && (b_hi <= 0 || b_lo >= kBN || b_lo >= b_hi));
-        const bool restage = tt == nt - 1 && si + 1 < w.seg_end && p.segs[si + 1].shift != cur_rot;
-        mbar_wait(&s_full[m], j & 1);
-        tc_fence_after();
-        if (warp_dead || (p.dbg & 1)) {  // no valid row: its P rows only feed its own (discarded) O rows
-          if (restage) {
-            cur_rot = p.segs[si + 1].shift;
-            mbar_arrive(&q_ready[m]);  // nothing to re-stage for invalid rows
-          }
-          tc_fence_before();
-          mbar_arrive(&p_full[m]);
-          continue;
-        }
-        float x[kBN];
-#pragma unroll
-        for (int c = 0; c < kBN; c += 32) tmem_ld32(t_s + c, *reinterpret_cast<float(*)[32]>(&x[c]));
-        tmem_wait_ld();
-        if (!__all_sync(0xffffffffu, full)) {
-#pragma unroll
-          for (int c = 0; c < kBN; ++c) {
-            const bool ok = (c >= c_lo) & (c < c_hi) & ((c < b_lo) | (c >= b_hi));
-            x[c] = ok ? x[c] : -INFINITY;
-          }
-        }
-        float mx[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) mx[i] = fmax3(x[i], x[i + 8], x[i + 16]);
-#pragma unroll
-        for (int c = 24; c + 16 < kBN; c += 16)
-#pragma unroll
-          for (int i = 0; i < 8; ++i) mx[i] = fmax3(mx[i], x[c + i], x[c + 8 + i]);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) mx[i] = fmaxf(mx[i], x[kBN - 8 + i]);
-        const float tmax = fmax3(fmax3(mx[0], mx[1], mx[2]), fmax3(mx[3], mx[4], mx[5]), fmaxf(mx[6], mx[7])) * sl2;
-        const float m_new = fmaxf(m_used, tmax);
-        // Lazy rescale (threshold 2^8).  S(m, j) being complete implies P.V(m, j-1)
-        // retired (issued before QK(m, j) on the in-order tensor pipe), so O(m)
-        // is quiescent here.  tcgen05.ld/st are warp-wide: the decision is warp-uniform.
-        const bool need = (m_used != -INFINITY) && (m_new > m_used + 8.f);
-        float alpha = 1.f;
-        if (__any_sync(0xffffffffu, need)) {
-          if (m_used != -INFINITY) alpha = fast_exp2(m_used - m_new);
-          m_used = m_new;
-#pragma unroll 1
-          for (int c0 = 0; c0 < HDP; c0 += 16) {
-            float o[16];
-            tmem_ld16(t_o + c0, o);
-            tmem_wait_ld();
-#pragma unroll
-            for (int i = 0; i < 16; ++i) o[i] *= alpha;
-            tmem_st16(t_o + c0, o);
-          }
-        } else if (m_used == -INFINITY) {
-          m_used = m_new;  // first finite max: O row holds nothing yet
-        }
-        l_sum *= alpha;
-        const float msub = m_used == -INFINITY ? 0.f : m_used;
-        // exp2 of (x * scale_log2 - m) two lanes at a time (FFMA2 / FADD2); one
-        // pair in four goes through the FMA-pipe exp2 so the MUFU pipe
-        // (16/clk/SM) does not bound the tile.
-        const float2 sl2v = make_float2(sl2, sl2), nmv = make_float2(-msub, -msub);
-        float2 ps[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          uint32_t pk[32];
-#pragma unroll
-          for (int c = 0; c < 64; c += 2) {
-            const float2 a = ffma2(make_float2(x[h * 64 + c], x[h * 64 + c + 1]), sl2v, nmv);
-            const float2 e = ((c >> 1) & 3) == 3 ? exp2_fma2(a) : make_float2(fast_exp2(a.x), fast_exp2(a.y));
-            ps[(c >> 1) & 1] = fadd2(ps[(c >> 1) & 1], e);
-            pk[c >> 1] = pack_bf16(e.x, e.y);
-          }
-          tmem_st32(t_s + h * 32, pk);  // P(j): keys 64h..64h+63 over S columns 32h..32h+31
-        }
-        const float2 pss = fadd2(ps[0], ps[1]);
-        l_sum += pss.x + pss.y;
-        tmem_wait_st();
-        tc_fence_before();
-        mbar_arrive(&p_full[m]);  // P.V(m, j) may start now
-        if (restage) {  // QK(m, j) retired (S read); QK(m, j+1) waits for q_ready(m)
-          cur_rot = p.segs[si + 1].shift;
-          load_q_row<HDP>(p, q_tile, trow, valid, t, head, cur_rot);
-          fence_proxy_async_smem();
-          mbar_arrive(&q_ready[m]);
-        }
-      }
-    }
+    int jg = 0, wk = 0;
 
-    // ------------------------------------------------------------ epilogue
-    mbar_wait(&o_full[m], 0);
-    tc_fence_after();
-    const bool empty = !(l_sum > 0.f);  // no visible key (e.g. a shard without chunks): O = 0, LSE = -inf
-    const float inv_l = empty ? 0.f : 1.f / l_sum;
-    const int hd = p.head_dim;
-#pragma unroll 1
-    for (int c0 = 0; c0 < HDP; c0 += 16) {
-      float o[16];
-      tmem_ld16(t_o + c0, o);
-      tmem_wait_ld();
-      if (empty) {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) o[i] = 0.f;
-      }
-      if (valid && c0 < hd) {
-        if (w.out_mode == 0) {
-          __nv_bfloat16 *dst = p.out + (int64_t)t * p.out_tok_stride + (int64_t)head * hd + c0;
-          if (hd % 16 == 0) {
-            uint4 *d4 = reinterpret_cast<uint4 *>(dst);
-            d4[0] = make_uint4(pack_bf16(o[0] * inv_l, o[1] * inv_l), pack_bf16(o[2] * inv_l, o[3] * inv_l),
-                               pack_bf16(o[4] * inv_l, o[5] * inv_l), pack_bf16(o[6] * inv_l, o[7] * inv_l));
-            d4[1] = make_uint4(pack_bf16(o[8] * inv_l, o[9] * inv_l), pack_bf16(o[10] * inv_l, o[11] * inv_l),
-                               pack_bf16(o[12] * inv_l, o[13] * inv_l), pack_bf16(o[14] * inv_l, o[15] * inv_l));
-          } else {
-            for (int i = 0; i < 16 && c0 + i < hd; ++i) dst[i] = __float2bfloat16(o[i] * inv_l);
+    // per-work row state
+    auto row_of = [&](const DbsaAttnWork &w, bool &valid, int &t, int &head) {
+      const int rows = w.n_tok * p.gs;
+      valid = r < rows;
+      t = w.q_tok0 + (valid ? r / p.gs : 0);
+      head = w.kv_head * p.gs + (valid ? r % p.gs : 0);
+    };
+    if (blockIdx.x < n_works) {  // stage Q of the first work
+      const DbsaAttnWork w0 = p.works[blockIdx.x];
+      bool v0;
+      int t0, h0;
+      row_of(w0, v0, t0, h0);
+      load_q_row<HDP>(p, q_tile, trow, v0, t0, h0, w0.seg_end > w0.seg_begin ? p.segs[w0.seg_begin].shift : 0);
+      fence_proxy_async_smem();
+      mbar_arrive(&q_full[m]);
+    }
+    for (int wi = blockIdx.x; wi < n_works; wi += gridDim.x, ++wk) {
+      const DbsaAttnWork w = p.works[wi];
+      bool valid;
+      int t, head;
+      row_of(w, valid, t, head);
+      const int rl = t - w.self_tok0;
+      const int lo = (p.tok_lo && valid) ? p.tok_lo[t] : 0;
+      int cur_rot = w.seg_end > w.seg_begin ? p.segs[w.seg_begin].shift : 0;
+      // Online softmax in the log2 domain; the scale is folded into the exp2
+      // FFMA: p = 2^(x * scale_log2 - m_used).
+      const bool warp_dead = __all_sync(0xffffffffu, !valid);
+      float m_used = -INFINITY, l_sum = 0.f;
+      int j = 0;
+      for (int si = w.seg_begin; si < w.seg_end; ++si) {
+        const DbsaAttnSeg sg = p.segs[si];
+        const int off = sg.row0 & 63;
+        const int nt = (off + sg.n_tok + kBN - 1) / kBN;
+        const bool is_self = sg.kind == DBSA_SEG_SELF;
+        // visible local keys of this row: [0, vis_hi) minus the band [band_lo, band_hi)
+        int vis_hi = valid ? sg.n_tok : 0;
+        int band_lo = 0, band_hi = 0;
+        if (is_self) {
+          vis_hi = min(vis_hi, rl + 1);
+          band_lo = w.prefix;
+          band_hi = lo;
+        }
+        for (int tt = 0; tt < nt; ++tt, ++j) {
+          const int k0 = tt * kBN - off;  // local key index of tile column 0
+          const int c_lo = max(0, -k0), c_hi = min(kBN, vis_hi - k0);
+          const int b_lo = band_lo - k0, b_hi = band_hi - k0;
+          // invalid rows (beyond the work's rows) count as full: their S is Q=0 . K = 0
+          // and their P only feeds their own (never stored) O rows
+          const bool full = !valid || (c_lo == 0 && c_hi == kBN && (b_hi <= 0 || b_lo >= kBN || b_lo >= b_hi));
+          const bool restage = tt == nt - 1 && si + 1 < w.seg_end && p.segs[si + 1].shift != cur_rot;
+          mbar_wait(&s_full[m], (jg + j) & 1);
+          tc_fence_after();
+          if (warp_dead || (p.dbg & 1)) {  // no valid row: its P rows only feed its own (discarded) O rows
+            if (restage) {
+              cur_rot = p.segs[si + 1].shift;
+              mbar_arrive(&q_ready[m]);  // nothing to re-stage for invalid rows
+            }
+            tc_fence_before();
+            mbar_arrive(&p_full[m]);
+            continue;
           }
-        } else {
-          float *dst = p.part_o + (w.part_row0 + r) * (int64_t)hd + c0;
-          if (hd % 16 == 0) {
-            float4 *d4 = reinterpret_cast<float4 *>(dst);
+          float x[kBN];
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
-              d4[i] = make_float4(o[4 * i] * inv_l, o[4 * i + 1] * inv_l, o[4 * i + 2] * inv_l, o[4 * i + 3] * inv_l);
-          } else {
-            for (int i = 0; i < 16 && c0 + i < hd; ++i) dst[i] = o[i] * inv_l;
+          for (int c = 0; c < kBN; c += 32) tmem_ld32(t_s + c, *reinterpret_cast<float(*)[32]>(&x[c]));
+          tmem_wait_ld();
+          if (!__all_sync(0xffffffffu, full)) {
+#pragma unroll
+            for (int c = 0; c < kBN; ++c) {
+              const bool ok = (c >= c_lo) & (c < c_hi) & ((c < b_lo) | (c >= b_hi));
+              x[c] = ok ? x[c] : -INFINITY;
+            }
+          }
+          float mx[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) mx[i] = fmax3(x[i], x[i + 8], x[i + 16]);
+#pragma unroll
+          for (int c = 24; c + 16 < kBN; c += 16)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) mx[i] = fmax3(mx[i], x[c + i], x[c + 8 + i]);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) mx[i] = fmaxf(mx[i], x[kBN - 8 + i]);
+          const float tmax =
+              fmax3(fmax3(mx[0], mx[1], mx[2]), fmax3(mx[3], mx[4], mx[5]), fmaxf(mx[6], mx[7])) * sl2;
+          const float m_new = fmaxf(m_used, tmax);
+          // Lazy rescale (threshold 2^8).  S(m, j) being complete implies P.V(m, j-1)
+          // retired (issued before QK(m, j) on the in-order tensor pipe), so O(m)
+          // is quiescent here.  tcgen05.ld/st are warp-wide: the decision is warp-uniform.
+          const bool need = (m_used != -INFINITY) && (m_new > m_used + 8.f);
+          float alpha = 1.f;
+          if (__any_sync(0xffffffffu, need)) {
+            if (m_used != -INFINITY) alpha = fast_exp2(m_used - m_new);
+            m_used = m_new;
+#pragma unroll 1
+            for (int c0 = 0; c0 < HDP; c0 += 16) {
+              float o[16];
+              tmem_ld16(t_o + c0, o);
+              tmem_wait_ld();
+#pragma unroll
+              for (int i = 0; i < 16; ++i) o[i] *= alpha;
+              tmem_st16(t_o + c0, o);
+            }
+          } else if (m_used == -INFINITY) {
+            m_used = m_new;  // first finite max: O row holds nothing yet
+          }
+          l_sum *= alpha;
+          const float msub = m_used == -INFINITY ? 0.f : m_used;
+          // exp2 of (x * scale_log2 - m) two lanes at a time (FFMA2 / FADD2); one
+          // pair in four goes through the FMA-pipe exp2 so the MUFU pipe
+          // (16/clk/SM) does not bound the tile.
+          const float2 sl2v = make_float2(sl2, sl2), nmv = make_float2(-msub, -msub);
+          float2 ps[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            uint32_t pk[32];
+#pragma unroll
+            for (int c = 0; c < 64; c += 2) {
+              const float2 a = ffma2(make_float2(x[h * 64 + c], x[h * 64 + c + 1]), sl2v, nmv);
+              const float2 e = ((c >> 1) & 3) == 3 ? exp2_fma2(a) : make_float2(fast_exp2(a.x), fast_exp2(a.y));
+              ps[(c >> 1) & 1] = fadd2(ps[(c >> 1) & 1], e);
+              pk[c >> 1] = pack_bf16(e.x, e.y);
+            }
+            tmem_st32(t_s + h * 32, pk);  // P(j): keys 64h..64h+63 over S columns 32h..32h+31
+          }
+          const float2 pss = fadd2(ps[0], ps[1]);
+          l_sum += pss.x + pss.y;
+          tmem_wait_st();
+          tc_fence_before();
+          mbar_arrive(&p_full[m]);  // P.V(m, j) may start now
+          if (restage) {  // QK(m, j) retired (S read); QK(m, j+1) waits for q_ready(m)
+            cur_rot = p.segs[si + 1].shift;
+            load_q_row<HDP>(p, q_tile, trow, valid, t, head, cur_rot);
+            fence_proxy_async_smem();
+            mbar_arrive(&q_ready[m]);
           }
         }
       }
-    }
-    if (valid && w.out_mode == 1) {
-      // natural-log LSE of the scaled scores: (m + log2 l) * ln 2
-      p.part_lse[w.part_row0 + r] = l_sum > 0.f ? (m_used + log2f(l_sum)) * 0.69314718055994531f : -INFINITY;
+      jg += j;
+      // The last QK of this work has retired (its S was read): stage the next
+      // work's Q now, so its first QK overlaps this epilogue.
+      const int wn = wi + gridDim.x;
+      if (wn < n_works) {
+        const DbsaAttnWork w2 = p.works[wn];
+        bool v2;
+        int t2, h2;
+        row_of(w2, v2, t2, h2);
+        load_q_row<HDP>(p, q_tile, trow, v2, t2, h2, w2.seg_end > w2.seg_begin ? p.segs[w2.seg_begin].shift : 0);
+        fence_proxy_async_smem();
+        mbar_arrive(&q_full[m]);
+      }
+
+      // ---------------------------------------------------------- epilogue
+      mbar_wait(&o_full[m], wk & 1);
+      tc_fence_after();
+      const bool empty = !(l_sum > 0.f);  // no visible key (e.g. a shard without chunks): O = 0, LSE = -inf
+      const float inv_l = empty ? 0.f : 1.f / l_sum;
+      const int hd = p.head_dim;
+#pragma unroll 1
+      for (int c0 = 0; c0 < HDP; c0 += 16) {
+        float o[16];
+        tmem_ld16(t_o + c0, o);
+        tmem_wait_ld();
+        if (empty) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) o[i] = 0.f;
+        }
+        if (valid && c0 < hd) {
+          if (w.out_mode == 0) {
+            __nv_bfloat16 *dst = p.out + (int64_t)t * p.out_tok_stride + (int64_t)head * hd + c0;
+            if (hd % 16 == 0) {
+              uint4 *d4 = reinterpret_cast<uint4 *>(dst);
+              d4[0] = make_uint4(pack_bf16(o[0] * inv_l, o[1] * inv_l), pack_bf16(o[2] * inv_l, o[3] * inv_l),
+                                 pack_bf16(o[4] * inv_l, o[5] * inv_l), pack_bf16(o[6] * inv_l, o[7] * inv_l));
+              d4[1] = make_uint4(pack_bf16(o[8] * inv_l, o[9] * inv_l), pack_bf16(o[10] * inv_l, o[11] * inv_l),
+                                 pack_bf16(o[12] * inv_l, o[13] * inv_l), pack_bf16(o[14] * inv_l, o[15] * inv_l));
+            } else {
+              for (int i = 0; i < 16 && c0 + i < hd; ++i) dst[i] = __float2bfloat16(o[i] * inv_l);
+            }
+          } else {
+            float *dst = p.part_o + (w.part_row0 + r) * (int64_t)hd + c0;
+            if (hd % 16 == 0) {
+              float4 *d4 = reinterpret_cast<float4 *>(dst);
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                d4[i] =
+                    make_float4(o[4 * i] * inv_l, o[4 * i + 1] * inv_l, o[4 * i + 2] * inv_l, o[4 * i + 3] * inv_l);
+            } else {
+              for (int i = 0; i < 16 && c0 + i < hd; ++i) dst[i] = o[i] * inv_l;
+            }
+          }
+        }
+      }
+      if (valid && w.out_mode == 1) {
+        // natural-log LSE of the scaled scores: (m + log2 l) * ln 2
+        p.part_lse[w.part_row0 + r] = l_sum > 0.f ? (m_used + log2f(l_sum)) * 0.69314718055994531f : -INFINITY;
+      }
+      tc_fence_before();
+      mbar_arrive(&o_free[m]);  // O(m) may be overwritten by the next work's first P.V
     }
   }
 
@@ -571,7 +626,6 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
   tc_fence_after();
   if (warp == 2) tmem_dealloc(tbase, C::TMEM_COLS);
 }
-
 
 // ============================================================================
 // Single-M-tile variant (num_m == 1): one 128-row M tile per CTA, Q held in
@@ -1070,6 +1124,17 @@ static int launch_attn1(const DbsaAttnArgs &a, const AttnParams &p, const CUtens
   return DBSA_OK;
 }
 
+static int num_sms() {
+  static thread_local int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
 template <int HDP, int NUM_M>
 static int launch_attn(const DbsaAttnArgs &a, const AttnParams &p, const CUtensorMap *maps, cudaStream_t s) {
   using C = AttnCfg<HDP, NUM_M>;
@@ -1080,7 +1145,9 @@ static int launch_attn(const DbsaAttnArgs &a, const AttnParams &p, const CUtenso
     if (e != cudaSuccess) return set_error(DBSA_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
     attr_set = true;
   }
-  kern<<<a.n_works, C::THREADS, C::SMEM, s>>>(maps[0], maps[1], maps[2], maps[3], p);
+  // persistent: one CTA per SM (1 CTA fits per SM), striding over the works
+  const int grid = a.n_works < num_sms() ? a.n_works : num_sms();
+  kern<<<grid, C::THREADS, C::SMEM, s>>>(maps[0], maps[1], maps[2], maps[3], p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(DBSA_ERR_CUDA, "attention launch: %s", cudaGetErrorString(e));
   return DBSA_OK;
@@ -1127,6 +1194,7 @@ extern "C" int dbsa_attention(const DbsaAttnArgs *args, void *stream) {
   p.gs = a.n_heads / a.n_kv_heads;
   p.scale_log2 = a.scale * 1.4426950408889634f;
   p.works = a.works;
+  p.n_works = a.n_works;
   p.segs = a.segs;
   p.out = reinterpret_cast<__nv_bfloat16 *>(a.out);
   p.out_tok_stride = a.out_tok_stride;
