@@ -267,7 +267,9 @@ def run_ours(args):
 
     # the step's forward + scoring replays one captured CUDA graph (engine.GraphedStage2);
     # each step copies its own work / token tables into the graph's buffers first
-    graph = engine.GraphedStage2(dm, cache.store, steps[0][3], steps[0][4], len(sess.label_ids))
+    cap = (max(getattr(st[4].sched, "n_real_works", 0) for st in steps),
+           max(getattr(st[4].sched, "n_real_segs", 0) for st in steps))
+    graph = engine.GraphedStage2(dm, cache.store, steps[0][3], steps[0][4], len(sess.label_ids), capacity=cap)
     scorers = [engine.LabelScorer(dm, st[4], st[3], len(sess.label_ids)) for st in steps]
 
     def device_step(st, i):
@@ -582,8 +584,12 @@ def main():
     ap.add_argument("--no-extras", action="store_true", help="skip the batch-1 latency and dense-comparator probes")
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--ratio", type=float, default=0.30)
+    ap.add_argument("--schedule", default=None, choices=["chunk", "query"],
+                    help="stage-2 K3 schedule (default: chunk-major for batches, split-KV per query for one query)")
     args = ap.parse_args()
     select_config(args.config, args.ratio)
+    if args.schedule:
+        os.environ["DBSA_STAGE2_SCHEDULE"] = args.schedule
     if args.impl == "reference":
         run_reference(args)
     else:

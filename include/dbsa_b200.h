@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define DBSA_ABI_VERSION 3
+#define DBSA_ABI_VERSION 4
 #define DBSA_PAGE_TOKENS 64
 
 /* Error codes -> reference exceptions (errors.py:4-29). */
@@ -56,6 +56,22 @@ extern "C" {
 #define DBSA_SEG_FULL 0 /* context chunk: every key visible to every row */
 #define DBSA_SEG_SELF 1 /* the rows' own tokens: causal, optionally a tree */
 
+/* Output modes of a work. */
+#define DBSA_OUT_BF16 0    /* normalized bf16 rows into out */
+#define DBSA_OUT_PARTIAL 1 /* fp32 partial O + LSE at part_row0 + row */
+#define DBSA_OUT_MAPPED 2  /* rows gathered through the row map (chunk-major stage 2): fp32 partial O + LSE
+                              at part_row0 + map.part_tok * gs + (row % gs) */
+
+/* Row map entry of a DBSA_OUT_MAPPED work: work-local token i is map entry
+ * q_tok0 + i.  Lets one work stack the rows of MANY queries against one
+ * selected chunk (each query's delta differs, so the rope row is per entry). */
+typedef struct DbsaRowMap {
+  int32_t tok;      /* token index into q */
+  int32_t rope_row; /* rope_table row of this token for the work's chunk: tok_pos - delta */
+  int32_t part_tok; /* partial slot (in tokens) */
+  int32_t pad;
+} DbsaRowMap;
+
 /* One unit of attention work = one CTA: up to 128*num_m query rows of one kv
  * head (token-major GQA packing: row r = token (r / gs), head (r % gs)),
  * attending to the segment list [seg_begin, seg_end). */
@@ -67,7 +83,8 @@ typedef struct DbsaAttnWork {
   int32_t seg_begin;
   int32_t seg_end;
   int32_t prefix;   /* SELF keys with local index < prefix are visible to all rows */
-  int32_t out_mode; /* 0: normalized bf16 into out; 1: fp32 partial + lse */
+  int32_t out_mode; /* DBSA_OUT_BF16 / DBSA_OUT_PARTIAL / DBSA_OUT_MAPPED (FULL segments only,
+                       every shift 0: the rope row comes from the map) */
   int64_t part_row0; /* partial row base (out_mode 1) */
 } DbsaAttnWork;
 
@@ -115,8 +132,10 @@ typedef struct DbsaAttnArgs {
   const DbsaAttnSeg *segs; /* device */
   void *out; /* bf16, element (t, head, d) at out[t*out_tok_stride + head*head_dim + d] */
   int64_t out_tok_stride;
-  float *part_o;   /* fp32 [rows][head_dim] (out_mode 1) */
-  float *part_lse; /* fp32 [rows], natural-log LSE (out_mode 1) */
+  void *part_o;    /* [rows][head_dim] normalised partial O (out_mode 1 / 2): fp32, or bf16 if part_bf16 */
+  float *part_lse; /* fp32 [rows], natural-log LSE (out_mode 1 / 2) */
+  const DbsaRowMap *row_map; /* device; required when any work is DBSA_OUT_MAPPED, else may be NULL */
+  int32_t part_bf16;         /* partial O element type: 0 fp32, 1 bf16 */
 } DbsaAttnArgs;
 int dbsa_attention(const DbsaAttnArgs *args, void *stream);
 
@@ -131,7 +150,8 @@ typedef struct DbsaMergeGroup {
   int32_t kv_head;
 } DbsaMergeGroup;
 typedef struct DbsaMergeArgs {
-  const float *part_o, *part_lse;
+  const void *part_o; /* fp32, or bf16 if part_bf16 */
+  const float *part_lse;
   const DbsaMergeGroup *groups; /* device */
   int32_t n_groups;
   int32_t max_rows;
@@ -140,6 +160,7 @@ typedef struct DbsaMergeArgs {
   int64_t out_tok_stride;
   int64_t split_stride; /* rows between split s and s+1 of a group; 0 = the group's `rows`
                            (a gathered [world][R] partial buffer uses R: the C5 shard merge) */
+  int32_t part_bf16;
 } DbsaMergeArgs;
 int dbsa_lse_merge(const DbsaMergeArgs *args, void *stream);
 

@@ -31,7 +31,8 @@ EXPORTED_SYMBOLS = (
     "dbsa_last_error",
 )
 
-ABI_VERSION = 3
+ABI_VERSION = 4
+OUT_BF16, OUT_PARTIAL, OUT_MAPPED = 0, 1, 2
 PAGE_TOKENS = 64
 SEG_FULL = 0
 SEG_SELF = 1
@@ -64,7 +65,12 @@ class AttnArgs(ctypes.Structure):
         ("scale", _f32), ("num_m", _i32),
         ("works", _vp), ("n_works", _i32), ("segs", _vp),
         ("out", _vp), ("out_tok_stride", _i64), ("part_o", _vp), ("part_lse", _vp),
+        ("row_map", _vp), ("part_bf16", _i32),
     ]
+
+
+class RowMap(ctypes.Structure):
+    _fields_ = [("tok", _i32), ("rope_row", _i32), ("part_tok", _i32), ("pad", _i32)]
 
 
 class MergeGroup(ctypes.Structure):
@@ -75,7 +81,7 @@ class MergeArgs(ctypes.Structure):
     _fields_ = [
         ("part_o", _vp), ("part_lse", _vp), ("groups", _vp), ("n_groups", _i32), ("max_rows", _i32),
         ("n_heads", _i32), ("n_kv_heads", _i32), ("head_dim", _i32), ("out", _vp), ("out_tok_stride", _i64),
-        ("split_stride", _i64),
+        ("split_stride", _i64), ("part_bf16", _i32),
     ]
 
 

@@ -81,9 +81,12 @@ struct AttnParams {
   const DbsaAttnSeg *segs;
   __nv_bfloat16 *out;
   int64_t out_tok_stride;
-  float *part_o;
+  void *part_o;  // fp32, or bf16 if part_bf16
   float *part_lse;
-  int dbg;  // profiling switches (DBSA_DEBUG_MODE): 1 = skip softmax math, 2 = skip MMAs, 4 = skip TMA loads
+  const DbsaRowMap *row_map;
+  int part_bf16;  // out_mode DBSA_OUT_MAPPED works: q_tok0 indexes this map
+  int dbg;  // profiling switches (DBSA_DEBUG_MODE): 1 = skip softmax math, 2 = skip MMAs, 4 = skip TMA loads,
+            // 8 = skip epilogue stores, 16 = skip Q staging (two-tile kernel)
 };
 
 // 2^x for a pair on the FMA/ALU pipes (FA4's MUFU offload): round to the
@@ -117,7 +120,7 @@ __device__ __forceinline__ float fast_exp2(float x) {
 // use so one row costs a few memory round trips, not one per element.
 template <int HDP>
 __device__ __forceinline__ void load_q_row(const AttnParams &p, uint8_t *q_tile, int row, bool valid,
-                                           int t, int head, int shift) {
+                                           int t, int head, int rope_row) {
   constexpr int QSW = AttnCfg<HDP, 1>::QSW;
   const int hd = p.head_dim, half = hd >> 1;
   auto put = [&](int c, const float (&o)[8]) {
@@ -132,7 +135,7 @@ __device__ __forceinline__ void load_q_row(const AttnParams &p, uint8_t *q_tile,
     return;
   }
   const __nv_bfloat16 *src = p.q + (int64_t)t * p.q_tok_stride + (int64_t)head * hd;
-  const float2 *rp = p.rope + (int64_t)(p.tok_pos[t] - shift) * half;
+  const float2 *rp = p.rope + (int64_t)rope_row * half;
   if (HDP >= 32 && hd == HDP && (p.q_tok_stride & 7) == 0) {
     // fast path: full-width head, every 8-element chunk lies in one half, 16-byte
     // aligned rows.  Two passes, each issuing all of its loads before any use.
@@ -186,6 +189,170 @@ __device__ __forceinline__ void load_q_row(const AttnParams &p, uint8_t *q_tile,
       o[j] = val;
     }
     put(c, o);
+  }
+}
+
+// Where row r of work w comes from and where its result goes.  Rows are
+// token-major GQA packing: work-local token r / gs, head r % gs of the work's
+// kv head.  Plain works read tokens q_tok0.. and rotate at tok_pos - shift of
+// the current segment; DBSA_OUT_MAPPED works (chunk-major stage 2: rows of many
+// queries against ONE chunk) take token, rope row and partial slot from the
+// row map, so each query row carries its own re-positioning delta.
+struct RowRef {
+  bool valid;
+  int t, head, rope_row;
+  int64_t part_row;
+};
+__device__ __forceinline__ RowRef row_ref(const AttnParams &p, const DbsaAttnWork &w, int r) {
+  RowRef x;
+  x.valid = r < w.n_tok * p.gs;
+  const int i = x.valid ? r / p.gs : 0, hl = x.valid ? r % p.gs : 0;
+  x.head = w.kv_head * p.gs + hl;
+  if (w.out_mode == DBSA_OUT_MAPPED) {
+    const DbsaRowMap e = p.row_map[w.q_tok0 + i];
+    x.t = e.tok;
+    x.rope_row = e.rope_row;
+    x.part_row = w.part_row0 + (int64_t)e.part_tok * p.gs + hl;
+  } else {
+    x.t = w.q_tok0 + i;
+    x.rope_row = p.tok_pos[x.t] - (w.seg_end > w.seg_begin ? p.segs[w.seg_begin].shift : 0);
+    x.part_row = w.part_row0 + r;
+  }
+  return x;
+}
+
+// Epilogue of one row (thread = TMEM lane = row): the whole O row from TMEM
+// in one round trip (HDP / 32 loads, one wait), normalised by 1/l, then
+// either bf16 into out or an fp32 partial + natural-log LSE.  Warp-collective
+// (tcgen05.ld): every lane calls it, invalid rows store nothing.
+template <int HDP>
+__device__ __forceinline__ void epilogue_row(const AttnParams &p, uint32_t t_o, bool valid, int t, int head,
+                                             int out_mode, int64_t part_row, float l_sum, float m_used) {
+  float o[HDP];
+  if constexpr (HDP >= 32) {
+#pragma unroll
+    for (int c = 0; c < HDP; c += 32) tmem_ld32(t_o + c, *reinterpret_cast<float(*)[32]>(&o[c]));
+  } else {
+    tmem_ld16(t_o, *reinterpret_cast<float(*)[16]>(&o[0]));
+  }
+  tmem_wait_ld();
+  if (!valid || (p.dbg & 8)) return;
+  const bool empty = !(l_sum > 0.f);  // no visible key (e.g. a shard without chunks): O = 0, LSE = -inf
+  const float inv_l = empty ? 0.f : 1.f / l_sum;
+  const int hd = p.head_dim;
+  if (out_mode == DBSA_OUT_BF16) {
+    __nv_bfloat16 *dst = p.out + (int64_t)t * p.out_tok_stride + (int64_t)head * hd;
+#pragma unroll
+    for (int c = 0; c < HDP; c += 8) {
+      if (c + 8 <= hd && (hd & 7) == 0) {
+        *reinterpret_cast<uint4 *>(dst + c) =
+            make_uint4(pack_bf16(o[c] * inv_l, o[c + 1] * inv_l), pack_bf16(o[c + 2] * inv_l, o[c + 3] * inv_l),
+                       pack_bf16(o[c + 4] * inv_l, o[c + 5] * inv_l), pack_bf16(o[c + 6] * inv_l, o[c + 7] * inv_l));
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          if (c + i < hd) dst[c + i] = __float2bfloat16(o[c + i] * inv_l);
+      }
+    }
+  } else if (p.part_bf16) {
+    __nv_bfloat16 *dst = reinterpret_cast<__nv_bfloat16 *>(p.part_o) + part_row * (int64_t)hd;
+#pragma unroll
+    for (int c = 0; c < HDP; c += 8) {
+      if (c + 8 <= hd && (hd & 7) == 0) {
+        *reinterpret_cast<uint4 *>(dst + c) =
+            make_uint4(pack_bf16(o[c] * inv_l, o[c + 1] * inv_l), pack_bf16(o[c + 2] * inv_l, o[c + 3] * inv_l),
+                       pack_bf16(o[c + 4] * inv_l, o[c + 5] * inv_l), pack_bf16(o[c + 6] * inv_l, o[c + 7] * inv_l));
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          if (c + i < hd) dst[c + i] = __float2bfloat16(o[c + i] * inv_l);
+      }
+    }
+    p.part_lse[part_row] = empty ? -INFINITY : (m_used + log2f(l_sum)) * 0.69314718055994531f;
+  } else {
+    float *dst = reinterpret_cast<float *>(p.part_o) + part_row * (int64_t)hd;
+#pragma unroll
+    for (int c = 0; c < HDP; c += 4) {
+      if (c + 4 <= hd && (hd & 3) == 0) {
+        *reinterpret_cast<float4 *>(dst + c) =
+            make_float4(o[c] * inv_l, o[c + 1] * inv_l, o[c + 2] * inv_l, o[c + 3] * inv_l);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (c + i < hd) dst[c + i] = o[c + i] * inv_l;
+      }
+    }
+    // natural-log LSE of the scaled scores: (m + log2 l) * ln 2
+    p.part_lse[part_row] = empty ? -INFINITY : (m_used + log2f(l_sum)) * 0.69314718055994531f;
+  }
+}
+
+// Stage the 128-row Q tile m of work w cooperatively: a row's 16-byte chunk
+// pairs (c, c + HDP/16) -- the two rotary halves -- go to HDP/16 consecutive
+// lanes, so one warp instruction reads whole 128-byte lines of q and of the
+// rope table for 32 / (HDP/16) rows instead of one 16-byte piece of 32
+// different rows (the thread-per-row form costs ~32 L1 wavefronts per
+// instruction).  restage: rope row tok_pos - shift (a plain work's next
+// segment); otherwise the row's own (row_ref) rope row.  Full-width heads only
+// (hd == HDP, 16-byte aligned rows); the caller falls back to load_q_row.
+template <int HDP>
+__device__ __forceinline__ void stage_q_coop(const AttnParams &p, const DbsaAttnWork &w, int m, uint8_t *q_tile,
+                                             int q4, int lane, bool restage, int shift) {
+  constexpr int QSW = AttnCfg<HDP, 1>::QSW;
+  constexpr int NCH = HDP / 16;  // chunk pairs per row == lanes per row
+  constexpr int RPI = 32 / NCH;  // rows per warp instruction
+  constexpr int NIT = 32 / RPI;  // iterations for the warp's 32 rows
+  const int c = lane % NCH, rsub = lane / NCH, half = HDP / 2;
+  // phase A: every iteration's (token, head, rope row) first, so the row-map /
+  // tok_pos round trip is paid once, not once per iteration
+  int tok[NIT], head[NIT], rrow[NIT];
+#pragma unroll
+  for (int it = 0; it < NIT; ++it) {
+    const RowRef x = row_ref(p, w, m * 128 + q4 * 32 + it * RPI + rsub);
+    tok[it] = x.valid ? x.t : -1;
+    head[it] = x.head;
+    rrow[it] = x.rope_row;
+  }
+  if (restage) {
+#pragma unroll
+    for (int it = 0; it < NIT; ++it)
+      if (tok[it] >= 0) rrow[it] = p.tok_pos[tok[it]] - shift;
+  }
+  // phase B: q chunk pair + its (cos, sin), rotate, swizzled 16-byte stores
+#pragma unroll
+  for (int it = 0; it < NIT; ++it) {
+    const int row = q4 * 32 + it * RPI + rsub;
+    float a[8], b[8];
+    if (tok[it] >= 0) {
+      const __nv_bfloat16 *src = p.q + (int64_t)tok[it] * p.q_tok_stride + (int64_t)head[it] * HDP + c * 8;
+      const float4 *rp = reinterpret_cast<const float4 *>(p.rope + (int64_t)rrow[it] * half + c * 8);
+      const uint4 lo4 = *reinterpret_cast<const uint4 *>(src);
+      const uint4 hi4 = *reinterpret_cast<const uint4 *>(src + half);
+      float4 cs4[4];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) cs4[v] = rp[v];
+      const __nv_bfloat16 *lo = reinterpret_cast<const __nv_bfloat16 *>(&lo4);
+      const __nv_bfloat16 *hi = reinterpret_cast<const __nv_bfloat16 *>(&hi4);
+      const float *cs = reinterpret_cast<const float *>(cs4);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float cc = cs[2 * j], sn = cs[2 * j + 1];
+        const float xl = __bfloat162float(lo[j]), yh = __bfloat162float(hi[j]);
+        a[j] = xl * cc - yh * sn;
+        b[j] = xl * sn + yh * cc;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) a[j] = b[j] = 0.f;
+    }
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      const float(&o)[8] = hh ? b : a;
+      const int ch = hh * NCH + c;
+      const int atom = ch / (QSW / 16), cc = ch % (QSW / 16);
+      uint4 *d = reinterpret_cast<uint4 *>(q_tile + atom * 128 * QSW + swz_offset(row, cc, QSW));
+      *d = make_uint4(pack_bf16(o[0], o[1]), pack_bf16(o[2], o[3]), pack_bf16(o[4], o[5]), pack_bf16(o[6], o[7]));
+    }
   }
 }
 
@@ -247,7 +414,11 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
-
+  // The control warpgroup hands registers to the two softmax warpgroups; each
+  // role's code sits inside the branch of its setmaxnreg so ptxas allocates
+  // it under that budget.
+  if (warp < 4) {
+  if constexpr (NUM_M == 2) regs_dec<C::REG_CTRL>();
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
@@ -408,7 +579,9 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
         }
       }
     }
-  } else if (warp >= 4) {
+  }
+  } else {
+    if constexpr (NUM_M == 2) regs_inc<C::REG_SOFTMAX>();
     // ------------------------------------------------------------ softmax warpgroups
     const int m = (warp - 4) >> 2;
     const int q4 = warp & 3;
@@ -421,27 +594,26 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
     const float sl2 = p.scale_log2;
     int jg = 0, wk = 0;
 
-    // per-work row state
-    auto row_of = [&](const DbsaAttnWork &w, bool &valid, int &t, int &head) {
-      const int rows = w.n_tok * p.gs;
-      valid = r < rows;
-      t = w.q_tok0 + (valid ? r / p.gs : 0);
-      head = w.kv_head * p.gs + (valid ? r % p.gs : 0);
+    const bool coop = HDP >= 16 && p.head_dim == HDP && (p.q_tok_stride & 7) == 0;
+    auto stage_q = [&](const DbsaAttnWork &wq, bool restage, int shift) {
+      if (p.dbg & 16) return;  // profiling: keep whatever Q the tile holds
+      if (coop) {
+        stage_q_coop<HDP>(p, wq, m, q_tile, q4, lane, restage, shift);
+      } else {
+        const RowRef xq = row_ref(p, wq, r);
+        load_q_row<HDP>(p, q_tile, trow, xq.valid, xq.t, xq.head, restage ? p.tok_pos[xq.t] - shift : xq.rope_row);
+      }
     };
     if (blockIdx.x < n_works) {  // stage Q of the first work
-      const DbsaAttnWork w0 = p.works[blockIdx.x];
-      bool v0;
-      int t0, h0;
-      row_of(w0, v0, t0, h0);
-      load_q_row<HDP>(p, q_tile, trow, v0, t0, h0, w0.seg_end > w0.seg_begin ? p.segs[w0.seg_begin].shift : 0);
+      stage_q(p.works[blockIdx.x], false, 0);
       fence_proxy_async_smem();
       mbar_arrive(&q_full[m]);
     }
     for (int wi = blockIdx.x; wi < n_works; wi += gridDim.x, ++wk) {
       const DbsaAttnWork w = p.works[wi];
-      bool valid;
-      int t, head;
-      row_of(w, valid, t, head);
+      const RowRef xr = row_ref(p, w, r);
+      const bool valid = xr.valid;
+      const int t = xr.t, head = xr.head;
       const int rl = t - w.self_tok0;
       const int lo = (p.tok_lo && valid) ? p.tok_lo[t] : 0;
       int cur_rot = w.seg_end > w.seg_begin ? p.segs[w.seg_begin].shift : 0;
@@ -551,7 +723,7 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
           mbar_arrive(&p_full[m]);  // P.V(m, j) may start now
           if (restage) {  // QK(m, j) retired (S read); QK(m, j+1) waits for q_ready(m)
             cur_rot = p.segs[si + 1].shift;
-            load_q_row<HDP>(p, q_tile, trow, valid, t, head, cur_rot);
+            stage_q(w, true, cur_rot);
             fence_proxy_async_smem();
             mbar_arrive(&q_ready[m]);
           }
@@ -559,14 +731,14 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
       }
       jg += j;
       // The last QK of this work has retired (its S was read): stage the next
-      // work's Q now, so its first QK overlaps this epilogue.
+      // work's Q now, so its first QK overlaps this epilogue.  A work without
+      // key tiles read no S, so nothing yet proves the MMA warp consumed this
+      // work's q_full phase: wait for its o_full first, or the next arrival
+      // could complete a second q_full phase before the first was observed.
+      if (j == 0) mbar_wait(&o_full[m], wk & 1);
       const int wn = wi + gridDim.x;
       if (wn < n_works) {
-        const DbsaAttnWork w2 = p.works[wn];
-        bool v2;
-        int t2, h2;
-        row_of(w2, v2, t2, h2);
-        load_q_row<HDP>(p, q_tile, trow, v2, t2, h2, w2.seg_end > w2.seg_begin ? p.segs[w2.seg_begin].shift : 0);
+        stage_q(p.works[wn], false, 0);
         fence_proxy_async_smem();
         mbar_arrive(&q_full[m]);
       }
@@ -574,48 +746,7 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
       // ---------------------------------------------------------- epilogue
       mbar_wait(&o_full[m], wk & 1);
       tc_fence_after();
-      const bool empty = !(l_sum > 0.f);  // no visible key (e.g. a shard without chunks): O = 0, LSE = -inf
-      const float inv_l = empty ? 0.f : 1.f / l_sum;
-      const int hd = p.head_dim;
-#pragma unroll 1
-      for (int c0 = 0; c0 < HDP; c0 += 16) {
-        float o[16];
-        tmem_ld16(t_o + c0, o);
-        tmem_wait_ld();
-        if (empty) {
-#pragma unroll
-          for (int i = 0; i < 16; ++i) o[i] = 0.f;
-        }
-        if (valid && c0 < hd) {
-          if (w.out_mode == 0) {
-            __nv_bfloat16 *dst = p.out + (int64_t)t * p.out_tok_stride + (int64_t)head * hd + c0;
-            if (hd % 16 == 0) {
-              uint4 *d4 = reinterpret_cast<uint4 *>(dst);
-              d4[0] = make_uint4(pack_bf16(o[0] * inv_l, o[1] * inv_l), pack_bf16(o[2] * inv_l, o[3] * inv_l),
-                                 pack_bf16(o[4] * inv_l, o[5] * inv_l), pack_bf16(o[6] * inv_l, o[7] * inv_l));
-              d4[1] = make_uint4(pack_bf16(o[8] * inv_l, o[9] * inv_l), pack_bf16(o[10] * inv_l, o[11] * inv_l),
-                                 pack_bf16(o[12] * inv_l, o[13] * inv_l), pack_bf16(o[14] * inv_l, o[15] * inv_l));
-            } else {
-              for (int i = 0; i < 16 && c0 + i < hd; ++i) dst[i] = __float2bfloat16(o[i] * inv_l);
-            }
-          } else {
-            float *dst = p.part_o + (w.part_row0 + r) * (int64_t)hd + c0;
-            if (hd % 16 == 0) {
-              float4 *d4 = reinterpret_cast<float4 *>(dst);
-#pragma unroll
-              for (int i = 0; i < 4; ++i)
-                d4[i] =
-                    make_float4(o[4 * i] * inv_l, o[4 * i + 1] * inv_l, o[4 * i + 2] * inv_l, o[4 * i + 3] * inv_l);
-            } else {
-              for (int i = 0; i < 16 && c0 + i < hd; ++i) dst[i] = o[i] * inv_l;
-            }
-          }
-        }
-      }
-      if (valid && w.out_mode == 1) {
-        // natural-log LSE of the scaled scores: (m + log2 l) * ln 2
-        p.part_lse[w.part_row0 + r] = l_sum > 0.f ? (m_used + log2f(l_sum)) * 0.69314718055994531f : -INFINITY;
-      }
+      epilogue_row<HDP>(p, t_o, valid, t, head, w.out_mode, xr.part_row, l_sum, m_used);
       tc_fence_before();
       mbar_arrive(&o_free[m]);  // O(m) may be overwritten by the next work's first P.V
     }
@@ -660,7 +791,7 @@ struct Attn1Cfg {
 // A-operand layout of the TS MMA).
 template <int HDP>
 __device__ __forceinline__ void q_row_to_tmem(const AttnParams &p, uint32_t tq, bool valid, int t, int head,
-                                              int shift) {
+                                              int rope_row) {
   const int hd = p.head_dim, half = hd >> 1;
   uint32_t pk[HDP / 2];
   if (!valid) {
@@ -668,7 +799,7 @@ __device__ __forceinline__ void q_row_to_tmem(const AttnParams &p, uint32_t tq, 
     for (int i = 0; i < HDP / 2; ++i) pk[i] = 0u;
   } else {
     const __nv_bfloat16 *src = p.q + (int64_t)t * p.q_tok_stride + (int64_t)head * hd;
-    const float2 *rp = p.rope + (int64_t)(p.tok_pos[t] - shift) * half;
+    const float2 *rp = p.rope + (int64_t)rope_row * half;
     if (HDP >= 32 && hd == HDP && (p.q_tok_stride & 7) == 0) {
       constexpr int NCH = HDP / 16;  // 8-pair chunks per half of the head
 #pragma unroll
@@ -909,10 +1040,9 @@ __global__ void __launch_bounds__(256, 1)
     // ------------------------------------------------------------ softmax warpgroup
     const int q4 = warp & 3;
     const int trow = q4 * 32 + lane;
-    const int rows = w.n_tok * p.gs;
-    const bool valid = trow < rows;
-    const int t = w.q_tok0 + (valid ? trow / p.gs : 0);
-    const int head = w.kv_head * p.gs + (valid ? trow % p.gs : 0);
+    const RowRef xr = row_ref(p, w, trow);
+    const bool valid = xr.valid;
+    const int t = xr.t, head = xr.head;
     const int rl = t - w.self_tok0;
     const int lo = (p.tok_lo && valid) ? p.tok_lo[t] : 0;
     const uint32_t lane_base = tbase + ((uint32_t)(q4 * 32) << 16);
@@ -920,7 +1050,7 @@ __global__ void __launch_bounds__(256, 1)
     const uint32_t t_q = lane_base + C::T_Q;
 
     int cur_rot = w.seg_end > w.seg_begin ? p.segs[w.seg_begin].shift : 0;
-    q_row_to_tmem<HDP>(p, t_q, valid, t, head, cur_rot);
+    q_row_to_tmem<HDP>(p, t_q, valid, t, head, xr.rope_row);
     tc_fence_before();
     mbar_arrive(q_full);
 
@@ -953,7 +1083,7 @@ __global__ void __launch_bounds__(256, 1)
           // QK(j) retired (S(j) ready), QK(j+1) waits for q_full: re-stage Q now so
           // the next tile's QK overlaps this tile's softmax
           cur_rot = p.segs[si + 1].shift;
-          q_row_to_tmem<HDP>(p, t_q, valid, t, head, cur_rot);
+          q_row_to_tmem<HDP>(p, t_q, valid, t, head, p.tok_pos[t] - cur_rot);
           tc_fence_before();
           mbar_arrive(q_full);
         }
@@ -1032,45 +1162,7 @@ __global__ void __launch_bounds__(256, 1)
     // ------------------------------------------------------------ epilogue
     mbar_wait(o_full, 0);
     tc_fence_after();
-    const bool empty = !(l_sum > 0.f);
-    const float inv_l = empty ? 0.f : 1.f / l_sum;
-    const int hd = p.head_dim;
-#pragma unroll 1
-    for (int c0 = 0; c0 < HDP; c0 += 16) {
-      float o[16];
-      tmem_ld16(t_o + c0, o);
-      tmem_wait_ld();
-      if (empty) {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) o[i] = 0.f;
-      }
-      if (valid && c0 < hd) {
-        if (w.out_mode == 0) {
-          __nv_bfloat16 *dst = p.out + (int64_t)t * p.out_tok_stride + (int64_t)head * hd + c0;
-          if (hd % 16 == 0) {
-            uint4 *d4 = reinterpret_cast<uint4 *>(dst);
-            d4[0] = make_uint4(pack_bf16(o[0] * inv_l, o[1] * inv_l), pack_bf16(o[2] * inv_l, o[3] * inv_l),
-                               pack_bf16(o[4] * inv_l, o[5] * inv_l), pack_bf16(o[6] * inv_l, o[7] * inv_l));
-            d4[1] = make_uint4(pack_bf16(o[8] * inv_l, o[9] * inv_l), pack_bf16(o[10] * inv_l, o[11] * inv_l),
-                               pack_bf16(o[12] * inv_l, o[13] * inv_l), pack_bf16(o[14] * inv_l, o[15] * inv_l));
-          } else {
-            for (int i = 0; i < 16 && c0 + i < hd; ++i) dst[i] = __float2bfloat16(o[i] * inv_l);
-          }
-        } else {
-          float *dst = p.part_o + (w.part_row0 + trow) * (int64_t)hd + c0;
-          if (hd % 16 == 0) {
-            float4 *d4 = reinterpret_cast<float4 *>(dst);
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-              d4[i] = make_float4(o[4 * i] * inv_l, o[4 * i + 1] * inv_l, o[4 * i + 2] * inv_l, o[4 * i + 3] * inv_l);
-          } else {
-            for (int i = 0; i < 16 && c0 + i < hd; ++i) dst[i] = o[i] * inv_l;
-          }
-        }
-      }
-    }
-    if (valid && w.out_mode == 1)
-      p.part_lse[w.part_row0 + trow] = l_sum > 0.f ? (m_used + log2f(l_sum)) * 0.69314718055994531f : -INFINITY;
+    epilogue_row<HDP>(p, t_o, valid, t, head, w.out_mode, xr.part_row, l_sum, m_used);
   }
 
   tc_fence_before();
@@ -1200,6 +1292,8 @@ extern "C" int dbsa_attention(const DbsaAttnArgs *args, void *stream) {
   p.out_tok_stride = a.out_tok_stride;
   p.part_o = a.part_o;
   p.part_lse = a.part_lse;
+  p.row_map = a.row_map;
+  p.part_bf16 = a.part_bf16;
   {
     const char *e = getenv("DBSA_DEBUG_MODE");
     p.dbg = e ? atoi(e) : 0;

@@ -24,6 +24,7 @@ __device__ __forceinline__ float warp_sum(float v) {
 
 // One warp per (group, row): lse = log sum_s exp(lse_s); O = sum_s exp(lse_s - lse) O_s.
 // This is the split form of the single softmax of kernels._softmax64 (kernels.py:52-56).
+template <bool BF16>
 __global__ void lse_merge_kernel(DbsaMergeArgs a) {
   const DbsaMergeGroup g = a.groups[blockIdx.y];
   const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -49,16 +50,33 @@ __global__ void lse_merge_kernel(DbsaMergeArgs a) {
       const float l = a.part_lse[g.part_row0 + (int64_t)s * sstride + r];
       if (l == -INFINITY) continue;
       const float wgt = __expf(l - mx) * inv;
-      const float *src = a.part_o + (g.part_row0 + (int64_t)s * sstride + r) * hd;
-      if ((hd & 3) == 0 && d0 + lane * 4 + 3 < hd) {
-        const float4 v = *reinterpret_cast<const float4 *>(src + d0 + lane * 4);
-        acc[0] += wgt * v.x;
-        acc[1] += wgt * v.y;
-        acc[2] += wgt * v.z;
-        acc[3] += wgt * v.w;
+      const int64_t off = (g.part_row0 + (int64_t)s * sstride + r) * hd;
+      if constexpr (BF16) {
+        const __nv_bfloat16 *src = reinterpret_cast<const __nv_bfloat16 *>(a.part_o) + off;
+        if ((hd & 3) == 0 && d0 + lane * 4 + 3 < hd) {
+          const uint2 v = *reinterpret_cast<const uint2 *>(src + d0 + lane * 4);
+          const __nv_bfloat162 v0 = *reinterpret_cast<const __nv_bfloat162 *>(&v.x);
+          const __nv_bfloat162 v1 = *reinterpret_cast<const __nv_bfloat162 *>(&v.y);
+          acc[0] += wgt * __low2float(v0);
+          acc[1] += wgt * __high2float(v0);
+          acc[2] += wgt * __low2float(v1);
+          acc[3] += wgt * __high2float(v1);
+        } else {
+          for (int i = 0; i < 4; ++i)
+            if (d0 + lane * 4 + i < hd) acc[i] += wgt * __bfloat162float(src[d0 + lane * 4 + i]);
+        }
       } else {
-        for (int i = 0; i < 4; ++i)
-          if (d0 + lane * 4 + i < hd) acc[i] += wgt * src[d0 + lane * 4 + i];
+        const float *src = reinterpret_cast<const float *>(a.part_o) + off;
+        if ((hd & 3) == 0 && d0 + lane * 4 + 3 < hd) {
+          const float4 v = *reinterpret_cast<const float4 *>(src + d0 + lane * 4);
+          acc[0] += wgt * v.x;
+          acc[1] += wgt * v.y;
+          acc[2] += wgt * v.z;
+          acc[3] += wgt * v.w;
+        } else {
+          for (int i = 0; i < 4; ++i)
+            if (d0 + lane * 4 + i < hd) acc[i] += wgt * src[d0 + lane * 4 + i];
+        }
       }
     }
     for (int i = 0; i < 4; ++i)
@@ -135,7 +153,10 @@ extern "C" int dbsa_lse_merge(const DbsaMergeArgs *args, void *stream) {
   const DbsaMergeArgs &a = *args;
   if (a.n_groups <= 0 || a.max_rows <= 0) return DBSA_OK;
   dim3 grid((a.max_rows + 3) / 4, a.n_groups);
-  lse_merge_kernel<<<grid, 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(a);
+  if (a.part_bf16)
+    lse_merge_kernel<true><<<grid, 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(a);
+  else
+    lse_merge_kernel<false><<<grid, 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(a);
   return check_launch("lse_merge");
 }
 

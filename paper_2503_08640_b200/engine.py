@@ -528,6 +528,7 @@ class NewTokens:
         if int(pos.max()) >= c.max_seq_len:
             raise ValidationError(f"position {int(pos.max())} exceeds max_seq_len {c.max_seq_len}")
         self.max_pos = int(pos.max())
+        self.pos_host = pos
         self.pos = torch.from_numpy(pos).to(dev, non_blocking=True)
         self.lo = torch.from_numpy(lo).to(dev, non_blocking=True)
         self.ids = torch.from_numpy(ids).to(dev, non_blocking=True)
@@ -652,13 +653,175 @@ class AttnSchedule:
                       part_lse=self.part_lse if part_lse is None else part_lse)
 
 
-class Stage2Plan:
-    """Single-device tables for a batch of QueryJobs: NewTokens + a split-KV
-    AttnSchedule over the jobs' chunk tables."""
+class ChunkMajorSchedule:
+    """Chunk-major K3 for a BATCH of queries: one work stacks the rows of many
+    queries against ONE selected chunk (DBSA_OUT_MAPPED works through a row
+    map), so a chunk's K/V tiles are streamed once per 128*num_m rows instead
+    of once per query, and the MMA M tiles are full instead of holding one
+    query's gs * n_new rows (176 of 256 at C3).  Every (query, chunk) pair and
+    every query's own tokens (SELF, per-query works) produce an fp32 partial +
+    LSE; K3m merges the S_q = n_chunks + 1 partials of each query row -- the
+    single softmax over the concatenated key set of kernels.py:52-56.
 
-    def __init__(self, dm, jobs, target_ctas: int | None = None, order: str = "query"):
+    Partial layout, per kv head: [query][split s][token][gs] rows (split s of
+    query q = its s-th chunk, the last split = SELF), so a query's merge group
+    is (base, rows = n * gs, n_splits = S_q) with the default split stride.
+    The RoPE re-positioning delta of (query, chunk) is folded into each map
+    entry's rope row (tok_pos - delta)."""
+
+    def __init__(self, dm, jobs, nt: NewTokens, chunk_tables=None, num_m: int = 2):
+        torch = _torch()
+        c = dm.config
+        gs, hkv, hd = c.group_size, c.n_kv_heads, c.head_dim
+        tables = chunk_tables if chunk_tables is not None else [j.chunks for j in jobs]
+        slab = (128 * num_m) // gs
+        if slab < 1:
+            raise ConfigError(f"group size {gs} exceeds the {128 * num_m} rows of one K3 work")
+        self.num_m = num_m
+        pos = nt.pos_host.astype(np.int64)
+        n_new = np.asarray(nt.n_new, np.int64)
+        tabs = [np.asarray(t, dtype=np.int64).reshape(-1, 3) for t in tables]
+        n_split = np.array([len(t) + 1 for t in tabs], np.int64)
+        tokbase = np.concatenate([[0], np.cumsum(n_split * n_new)])
+        tot = int(tokbase[-1])  # partial tokens per kv head
+        kv_rows = tot * gs
+        # (query, chunk) pairs, grouped by chunk (pool row, length)
+        qi = np.repeat(np.arange(len(jobs)), n_split - 1)
+        ch = np.concatenate(tabs) if len(qi) else np.zeros((0, 3), np.int64)
+        sidx = np.concatenate([np.arange(len(t)) for t in tabs]) if len(qi) else np.zeros(0, np.int64)
+        key = ch[:, 0] * (1 << 24) + ch[:, 1] if len(qi) else np.zeros(0, np.int64)
+        order = np.lexsort((qi, key))
+        segs, works, entries = [], [], []
+        n_map = 0
+        if len(order):
+            keys_sorted = key[order]
+            starts = np.flatnonzero(np.r_[True, keys_sorted[1:] != keys_sorted[:-1]])
+            ends = np.r_[starts[1:], len(order)]
+            for a, b in zip(starts, ends):
+                pairs = order[a:b]
+                row, cnt = int(ch[pairs[0], 0]), int(ch[pairs[0], 1])
+                # map entries of every (query, token) row against this chunk
+                q_of = qi[pairs]
+                nn = n_new[q_of]
+                rep = np.repeat(np.arange(len(pairs)), nn)
+                tok_local = np.arange(int(nn.sum())) - np.repeat(np.cumsum(nn) - nn, nn)
+                q_rep = q_of[rep]
+                tok = nt.tok0[q_rep] + tok_local
+                rope_row = pos[tok] - ch[pairs, 2][rep]
+                part = tokbase[q_rep] + sidx[pairs][rep] * n_new[q_rep] + tok_local
+                e = np.stack([tok, rope_row, part, np.zeros_like(tok)], axis=1)
+                entries.append(e)
+                n_e = len(e)
+                k = -(-n_e // slab)
+                size = -(-n_e // k)
+                sb = len(segs)
+                segs.append((0, 0, row, cnt, SEG_FULL, 0))
+                for kv in range(hkv):
+                    for t0 in range(0, n_e, size):
+                        works.append((n_map + t0, min(size, n_e - t0), 0, kv, sb, sb + 1, 0, nat.OUT_MAPPED,
+                                      kv * kv_rows))
+                n_map += n_e
+        merges = []
+        for q, j in enumerate(jobs):
+            n, s_last = int(n_new[q]), int(n_split[q]) - 1
+            q0 = int(nt.tok0[q])
+            k = -(-n // slab)
+            size = -(-n // k)
+            for t0 in range(0, n, size):
+                ntk = min(size, n - t0)
+                sb = len(segs)
+                segs.append((1, 0, int(nt.aux_row0[q]), t0 + ntk, SEG_SELF, 0))
+                for kv in range(hkv):
+                    works.append((q0 + t0, ntk, q0, kv, sb, sb + 1, j.prefix, nat.OUT_PARTIAL,
+                                  kv * kv_rows + (int(tokbase[q]) + s_last * n + t0) * gs))
+            for kv in range(hkv):
+                merges.append((kv * kv_rows + int(tokbase[q]) * gs, n * gs, s_last + 1, q0, kv))
+        emap = np.concatenate(entries) if entries else np.zeros((1, 4), np.int64)
+        self.kv_tokens = int(sum(int(t[:, 1].sum()) for t in tabs))
+        self.n_works, self.n_segs, self.n_merge = len(works), len(segs), len(merges)
+        dev = dm.device
+        self.row_map = ops.to_device(np.ascontiguousarray(emap.astype(np.int32)).view(ops.ROWMAP_DTYPE).reshape(-1),
+                                     dev)
+        self.works = ops.to_device(_work_array(works), dev)
+        self.segs = ops.to_device(_per_layer_segs(_seg_array(segs), c.n_layers), dev)
+        self.merges = ops.to_device(_merge_array(merges), dev) if merges else None
+        self.max_rows = max((m[1] for m in merges), default=0)
+        self.rope = dm.rope_for(max(nt.max_pos, int(emap[:, 1].max())) + 1)
+        self.part_rows = kv_rows * hkv
+        # bf16 partials: a normalised partial row is a convex combination of V rows,
+        # so one bf16 rounding (2^-9 relative) before the merge adds at most the
+        # error of the final bf16 output; it halves the partial traffic
+        self.part_o = torch.empty((max(self.part_rows, 1), hd), dtype=torch.bfloat16, device=dev)
+        self.part_lse = torch.empty((max(self.part_rows, 1),), dtype=torch.float32, device=dev)
+
+        self.n_real_works, self.n_real_segs = self.n_works, self.n_segs
+
+    def pad_to(self, works_cap: int, segs_cap: int) -> None:
+        """Grow the device tables to fixed capacities (a captured graph's launch
+        shape): extra works are empty (no segment, no row) and cost a CTA a
+        few barrier round trips; extra segments are never referenced."""
+        torch = _torch()
+        L = self.segs.numel() // (self.n_segs * ops.SEG_DTYPE.itemsize) if self.n_segs else 0
+        if works_cap < self.n_real_works or segs_cap < self.n_real_segs:
+            raise ValueError("capacity below the schedule's size")
+        w = torch.zeros(works_cap * ops.WORK_DTYPE.itemsize, dtype=torch.uint8, device=self.works.device)
+        w[: self.works.numel()].copy_(self.works)
+        s = torch.zeros((L, segs_cap * ops.SEG_DTYPE.itemsize), dtype=torch.uint8, device=self.segs.device)
+        s[:, : self.n_segs * ops.SEG_DTYPE.itemsize].copy_(self.segs.view(L, -1))
+        self.works, self.segs = w, s.view(-1)
+        self.n_works, self.n_segs = works_cap, segs_cap
+
+    def copy_tables_from(self, other: "ChunkMajorSchedule") -> None:
+        """Load another batch's tables into these (padded) buffers in place."""
+        if other.n_real_works > self.n_works or other.n_real_segs > self.n_segs:
+            raise ValueError("schedule exceeds the captured capacity")
+        nw = other.n_real_works * ops.WORK_DTYPE.itemsize
+        self.works[:nw].copy_(other.works[:nw], non_blocking=True)
+        self.works[nw:].zero_()
+        L = self.segs.numel() // (self.n_segs * ops.SEG_DTYPE.itemsize)
+        ns = other.n_real_segs * ops.SEG_DTYPE.itemsize
+        self.segs.view(L, -1)[:, :ns].copy_(other.segs.view(L, -1)[:, :ns], non_blocking=True)
+        self.row_map.copy_(other.row_map, non_blocking=True)
+        self.merges.copy_(other.merges, non_blocking=True)
+
+    def segs_ptr(self, layer: int) -> int:
+        return self.segs.data_ptr() + layer * self.n_segs * ops.SEG_DTYPE.itemsize
+
+    def launch(self, dm, nt: NewTokens, layer, qkv, out, pool, part_o=None, part_lse=None):
+        c = dm.config
+        qw, kw = c.n_heads * c.head_dim, c.n_kv_heads * c.head_dim
+        if self.n_works == 0:
+            return
+        ops.attention(q=qkv, q_tok_stride=qw + 2 * kw, tok_pos=nt.pos, tok_lo=nt.lo, rope=self.rope,
+                      pool=pool, aux=nt.aux(), n_heads=c.n_heads, n_kv_heads=c.n_kv_heads, head_dim=c.head_dim,
+                      works_dev=self.works, n_works=self.n_works, segs_dev=self.segs_ptr(layer), num_m=self.num_m,
+                      out=out, out_tok_stride=qw, part_o=self.part_o if part_o is None else part_o,
+                      part_lse=self.part_lse if part_lse is None else part_lse, row_map=self.row_map)
+
+
+def stage2_schedule_kind(n_jobs: int) -> str:
+    """'chunk' (chunk-major, rows of many queries per work) for batches, 'query'
+    (split-KV per query) for a single query or when DBSA_STAGE2_SCHEDULE forces it."""
+    import os
+
+    forced = os.environ.get("DBSA_STAGE2_SCHEDULE")
+    if forced in ("chunk", "query"):
+        return forced
+    return "chunk" if n_jobs >= 8 else "query"
+
+
+class Stage2Plan:
+    """Single-device tables for a batch of QueryJobs: NewTokens + a K3
+    schedule over the jobs' chunk tables (chunk-major for batches, split-KV
+    per query otherwise; see stage2_schedule_kind)."""
+
+    def __init__(self, dm, jobs, target_ctas: int | None = None, order: str = "query", schedule: str | None = None):
         self.new = NewTokens(dm, jobs)
-        self.sched = AttnSchedule(dm, jobs, self.new, target_ctas=target_ctas, order=order)
+        self.schedule = schedule or stage2_schedule_kind(len(jobs))
+        if self.schedule == "chunk":
+            self.sched = ChunkMajorSchedule(dm, jobs, self.new)
+        else:
+            self.sched = AttnSchedule(dm, jobs, self.new, target_ctas=target_ctas, order=order)
         for name in ("tok0", "n_tok", "num_m", "pos", "lo", "ids", "pages", "n_pages", "k_aux", "v_aux", "aux_rows"):
             setattr(self, name, getattr(self.new, name))
         for name in ("works", "n_works", "n_segs", "n_merge", "merges", "max_rows", "rope", "part_o", "part_lse",
@@ -816,11 +979,20 @@ class GraphedStage2:
     otherwise be host-bound.
     """
 
-    def __init__(self, dm, store, jobs, plan, n_labels):
+    def __init__(self, dm, store, jobs, plan, n_labels, capacity=None):
+        """capacity: optional (works, segments) lower bound for a chunk-major
+        template (e.g. the largest tables of a set of batches to replay)."""
         torch = _torch()
         self.dm, self.store, self.plan = dm, store, plan
         self.scorer = LabelScorer(dm, plan, jobs, n_labels)
         self.key = plan_key(plan, self.scorer)
+        if isinstance(plan.sched, ChunkMajorSchedule):
+            # the chunk-major table sizes vary with how a batch's selections
+            # overlap: capture at a padded capacity, replay any batch that fits
+            sc = plan.sched
+            nw, ns = max(sc.n_real_works, (capacity or (0, 0))[0]), max(sc.n_real_segs, (capacity or (0, 0))[1])
+            sc.pad_to(-(-(nw * 17 // 16 + 64) // 64) * 64, -(-(ns * 17 // 16 + 16) // 16) * 16)
+            plan.works, plan.n_works, plan.segs, plan.n_segs = sc.works, sc.n_works, sc.segs, sc.n_segs
         self._run()  # warm-up: workspace allocation, cuBLAS handles, kernel attributes
         torch.cuda.current_stream(dm.device).synchronize()
         self.graph = torch.cuda.CUDAGraph()
@@ -838,13 +1010,18 @@ class GraphedStage2:
         if plan_key(plan, scorer) != self.key:
             raise ValueError("plan shape differs from the captured graph")
         t, n = self.plan, plan
-        for dst, src in ((t.new.pos, n.new.pos), (t.new.lo, n.new.lo), (t.new.ids, n.new.ids),
-                         (t.new.pages, n.new.pages), (t.sched.works, n.sched.works), (t.sched.segs, n.sched.segs),
-                         (self.scorer.rows, scorer.rows), (self.scorer.targets, scorer.targets),
-                         (self.scorer.owner, scorer.owner)):
-            dst.copy_(src, non_blocking=True)
-        if t.sched.merges is not None:
-            t.sched.merges.copy_(n.sched.merges, non_blocking=True)
+        if n is not t:
+            pairs = [(t.new.pos, n.new.pos), (t.new.lo, n.new.lo), (t.new.ids, n.new.ids), (t.new.pages, n.new.pages),
+                     (self.scorer.rows, scorer.rows), (self.scorer.targets, scorer.targets),
+                     (self.scorer.owner, scorer.owner)]
+            if isinstance(t.sched, ChunkMajorSchedule):
+                t.sched.copy_tables_from(n.sched)
+            else:
+                pairs += [(t.sched.works, n.sched.works), (t.sched.segs, n.sched.segs)]
+                if t.sched.merges is not None:
+                    pairs.append((t.sched.merges, n.sched.merges))
+            for dst, src in pairs:
+                dst.copy_(src, non_blocking=True)
         if n.sched.rope is not t.sched.rope:
             raise ValueError("rope table was re-allocated; recapture")
         self.graph.replay()
@@ -853,8 +1030,24 @@ class GraphedStage2:
 
 
 def plan_key(plan, scorer):
-    return (plan.new.n_tok, tuple(plan.new.n_new), plan.new.n_pages, plan.sched.n_works, plan.sched.n_segs,
-            plan.sched.n_merge, plan.sched.part_rows, int(scorer.rows.numel()), scorer.n_out, plan.new.num_m)
+    """Launch shape of a stage-2 batch: plans with equal keys can replay one
+    captured graph.  Chunk-major table sizes are capacity-checked at replay
+    instead (GraphedStage2 pads them)."""
+    sc = plan.sched
+    if isinstance(sc, ChunkMajorSchedule):
+        tables = ("chunk", sc.row_map.numel(), sc.num_m)
+    else:
+        tables = ("query", sc.n_works, sc.n_segs)
+    return (plan.new.n_tok, tuple(plan.new.n_new), plan.new.n_pages, tables, sc.n_merge, sc.part_rows,
+            int(scorer.rows.numel()), scorer.n_out, plan.new.num_m)
+
+
+def fits_graph(graph, plan) -> bool:
+    """Whether `plan`'s chunk-major tables fit `graph`'s captured capacity."""
+    sc, t = plan.sched, graph.plan.sched
+    if not isinstance(sc, ChunkMajorSchedule):
+        return True
+    return sc.n_real_works <= t.n_works and sc.n_real_segs <= t.n_segs
 
 
 def _final_logits(dm, h_rows):

@@ -36,6 +36,7 @@ WORK_DTYPE = np.dtype(
 SEG_DTYPE = np.dtype(
     [("src", "<i4"), ("layer", "<i4"), ("row0", "<i4"), ("n_tok", "<i4"),
      ("kind", "<i4"), ("shift", "<i4"), ("pad0", "<i4"), ("pad1", "<i4")], align=True)
+ROWMAP_DTYPE = np.dtype([("tok", "<i4"), ("rope_row", "<i4"), ("part_tok", "<i4"), ("pad", "<i4")], align=True)
 PAGE_DTYPE = np.dtype([("tok0", "<i4"), ("n_tok", "<i4"), ("row0", "<i4"), ("pad", "<i4")], align=True)
 MERGE_DTYPE = np.dtype(
     [("part_row0", "<i8"), ("rows", "<i4"), ("n_splits", "<i4"), ("q_tok0", "<i4"), ("kv_head", "<i4")],
@@ -43,6 +44,7 @@ MERGE_DTYPE = np.dtype(
 
 assert WORK_DTYPE.itemsize == ctypes.sizeof(nat.AttnWork)
 assert SEG_DTYPE.itemsize == ctypes.sizeof(nat.AttnSeg)
+assert ROWMAP_DTYPE.itemsize == ctypes.sizeof(nat.RowMap)
 assert PAGE_DTYPE.itemsize == ctypes.sizeof(nat.Page)
 assert MERGE_DTYPE.itemsize == ctypes.sizeof(nat.MergeGroup)
 
@@ -109,8 +111,10 @@ def kv_read(k_planes, v_planes, rows, layers, layer, tok_pos, rope, pages_dev, n
 
 
 def attention(*, q, q_tok_stride, tok_pos, tok_lo, rope, pool, aux, n_heads, n_kv_heads, head_dim,
-              works_dev, n_works, segs_dev, num_m, out, out_tok_stride, part_o=None, part_lse=None):
-    """Launch K1/K3.  `pool` / `aux` are (k_planes, v_planes, rows, layers)."""
+              works_dev, n_works, segs_dev, num_m, out, out_tok_stride, part_o=None, part_lse=None,
+              row_map=None):
+    """Launch K1/K3.  `pool` / `aux` are (k_planes, v_planes, rows, layers); `row_map`
+    (ROWMAP_DTYPE, device) backs DBSA_OUT_MAPPED works."""
     kp, vp, prow, pl = pool
     ka, va, arow, al = aux if aux is not None else (None, None, 0, 0)
     a = nat.AttnArgs(
@@ -121,7 +125,8 @@ def attention(*, q, q_tok_stride, tok_pos, tok_lo, rope, pool, aux, n_heads, n_k
         n_heads=n_heads, n_kv_heads=n_kv_heads, head_dim=head_dim, hd_pad=hd_pad(head_dim),
         scale=float(1.0 / math.sqrt(head_dim)), num_m=num_m, works=_p(works_dev),
         n_works=n_works, segs=_p(segs_dev), out=out.data_ptr(), out_tok_stride=out_tok_stride,
-        part_o=nat.ptr(part_o), part_lse=nat.ptr(part_lse))
+        part_o=nat.ptr(part_o), part_lse=nat.ptr(part_lse), row_map=nat.ptr(row_map),
+        part_bf16=int(part_o is not None and part_o.element_size() == 2))
     nat.check(nat.load_library().dbsa_attention(ctypes.byref(a), nat.stream_handle()))
     _launched()
 
@@ -131,7 +136,7 @@ def lse_merge(part_o, part_lse, groups_dev, n_groups, max_rows, n_heads, n_kv_he
     a = nat.MergeArgs(part_o=part_o.data_ptr(), part_lse=part_lse.data_ptr(), groups=groups_dev.data_ptr(),
                       n_groups=n_groups, max_rows=max_rows, n_heads=n_heads, n_kv_heads=n_kv_heads,
                       head_dim=head_dim, out=out.data_ptr(), out_tok_stride=out_tok_stride,
-                      split_stride=split_stride)
+                      split_stride=split_stride, part_bf16=int(part_o.element_size() == 2))
     nat.check(nat.load_library().dbsa_lse_merge(ctypes.byref(a), nat.stream_handle()))
     _launched()
 

@@ -285,7 +285,7 @@ class Stage2Session:
         scorer = engine.LabelScorer(self.dm, plan, jobs, len(self.label_ids))
         key = engine.plan_key(plan, scorer)
         graphs = self.__dict__.setdefault("_graphs", {})
-        if key not in graphs:
+        if key not in graphs or not engine.fits_graph(graphs[key], plan):
             graphs[key] = engine.GraphedStage2(self.dm, self.cache.store, jobs, plan, len(self.label_ids))
         s, best = graphs[key].replay(plan, scorer)
         return ids, s, best

@@ -295,3 +295,110 @@ def test_topk_bit_exact(n_units, ordering):
         got = ops.topk_select(dev_scores, budget, ordering).cpu().numpy()
         for q in range(scores.shape[0]):
             assert list(got[q]) == _py_select(list(scores[q]), budget, ordering)
+
+
+class _DM:
+    """The attributes a stage-2 plan reads (config, device, rope tables)."""
+
+    def __init__(self, cfg, dev):
+        self.config, self.device = cfg, dev
+        self.rope = ops.rope_table(cfg.max_seq_len, cfg.head_dim, cfg.rope_theta, dev)
+
+    def rope_for(self, rows):
+        if rows > self.rope.shape[0]:
+            self.rope = ops.rope_table(rows, self.config.head_dim, self.config.rope_theta, self.device)
+        return self.rope
+
+
+@pytest.mark.parametrize("schedule", ["chunk", "query", "chunk-padded"])
+@pytest.mark.parametrize("hd,H,Hkv", [(128, 8, 2), (64, 4, 4), (32, 8, 1)])
+def test_stage2_batch_schedules_vs_float64(schedule, hd, H, Hkv):
+    """A batch of label jobs over overlapping chunk tables (whole groups and
+    example-granularity sub-spans, assorted orders) through one layer of K3 +
+    K3m, chunk-major (DBSA_OUT_MAPPED row-map works) and split-KV per query,
+    against float64 attention over the assembled context (kvstore.py:188-221,
+    model.py:381-392, kernels.py:73-100)."""
+    import paper_2503_08640_b200 as P
+    from paper_2503_08640_b200 import engine
+
+    dev = torch.device("cuda", 0)
+    theta = 10000.0
+    cfg = P.ModelConfig(d_model=H * hd, n_layers=1, n_heads=H, n_kv_heads=Hkv, head_dim=hd, ffn_dim=64,
+                        vocab_size=300, rope_theta=theta, max_seq_len=8192)
+    dm = _DM(cfg, dev)
+    lengths = [130, 64, 300, 77, 150, 90, 200, 41]
+    cache = P.SegmentedKVCache(cfg, dev, capacity_tokens=sum(lengths))
+    blocks = cache._reserve(lengths, [b"\0" * 32] * len(lengths), [()] * len(lengths))
+    g = torch.Generator(device=dev).manual_seed(3)
+    cache.store.k.normal_(generator=g)
+    cache.store.v.normal_(generator=g)
+    st = cache.store
+    rows0 = np.array([b.row0 for b in blocks])
+    pos0 = np.array([b.pos_start for b in blocks])
+    rng = np.random.default_rng(7)
+    # units: whole groups plus a few sub-spans (example granularity)
+    units = [(b, 0, n) for b, n in enumerate(lengths)] + [(2, 10, 70), (2, 200, 300), (6, 5, 133), (4, 0, 64)]
+    jobs = []
+    for qi in range(11):
+        k = int(rng.integers(1, 6))
+        pick = [0] + rng.choice(np.arange(1, len(units)), k - 1, replace=False).tolist()
+        if qi % 3 == 1:
+            pick = [0] + pick[1:][::-1]
+        ln = np.array([units[u][2] - units[u][1] for u in pick])
+        new_start = np.cumsum(ln) - ln
+        tab = np.array([(rows0[units[u][0]] + units[u][1], ln[i], new_start[i] - (pos0[units[u][0]] + units[u][1]))
+                        for i, u in enumerate(pick)])
+        q_ids = rng.integers(3, 200, int(rng.integers(5, 30))).tolist()
+        labels = [rng.integers(3, 200, int(rng.integers(2, 6))).tolist() for _ in range(3)]
+        jobs.append((engine.label_job(tab, int(ln.sum()), q_ids, labels), pick, ln))
+    plan = engine.Stage2Plan(dm, [j for j, _, _ in jobs], schedule=schedule.split("-")[0])
+    if schedule == "chunk-padded":  # graph capacity padding: trailing empty works / unused segments
+        plan.sched.pad_to(plan.sched.n_works + 300, plan.sched.n_segs + 20)
+    nt = plan.new
+    qw, kw = H * hd, Hkv * hd
+    qkv = (torch.randn(nt.n_tok, qw + 2 * kw, generator=g, device=dev) * 0.5).to(torch.bfloat16)
+    ops.kv_write(qkv[:, qw:], qkv[:, qw + kw:], qw + 2 * kw, nt.pos, dm.rope, nt.pages, nt.n_pages, nt.k_aux,
+                 nt.v_aux, nt.aux_rows, 1, 0, Hkv, hd)
+    out = torch.zeros(nt.n_tok, qw, dtype=torch.bfloat16, device=dev)
+    plan.sched.launch(dm, nt, 0, qkv, out, st.planes())
+    if plan.sched.n_merge:
+        ops.lse_merge(plan.sched.part_o, plan.sched.part_lse, plan.sched.merges, plan.sched.n_merge,
+                      plan.sched.max_rows, H, Hkv, hd, out, qw)
+    torch.cuda.synchronize()
+    got = out.float().cpu().numpy().reshape(nt.n_tok, H, hd)
+    Kp = st.k[0].float().cpu().numpy()  # [Hkv][rows][hdp], rotated at original positions
+    Vp = st.v[0].float().cpu().numpy()  # [Hkv][hdp][rows]
+    qn = qkv[:, :qw].float().cpu().numpy().reshape(nt.n_tok, H, hd).astype(np.float64)
+    kn = qkv[:, qw:qw + kw].float().cpu().numpy().reshape(nt.n_tok, Hkv, hd).astype(np.float64)
+    vn = qkv[:, qw + kw:].float().cpu().numpy().reshape(nt.n_tok, Hkv, hd).astype(np.float64)
+    gs = H // Hkv
+    worst = 0.0
+    for qi, (job, pick, ln) in enumerate(jobs):
+        t0, n = int(nt.tok0[qi]), nt.n_new[qi]
+        pos = nt.pos_host[t0:t0 + n].astype(np.int64)
+        ch = np.asarray(job.chunks).reshape(-1, 3)
+        for kv in range(Hkv):
+            kself = _rope64(kn[t0:t0 + n, kv:kv + 1], pos, theta)[:, 0]
+            for h in range(gs):
+                head = kv * gs + h
+                q = qn[t0:t0 + n, head:head + 1]
+                scores, vals = [], []
+                for row, cnt, delta in ch:
+                    qr = _rope64(q, pos - delta, theta)[:, 0]  # R(p - delta) q . R(p_orig) k
+                    scores.append(qr @ Kp[kv, row:row + cnt, :hd].astype(np.float64).T)
+                    vals.append(Vp[kv, :hd, row:row + cnt].astype(np.float64).T)
+                qs = _rope64(q, pos, theta)[:, 0]
+                s_self = qs @ kself.T
+                lo = np.asarray(job.lo)
+                vis = np.zeros((n, n), bool)
+                for r in range(n):
+                    for kk in range(r + 1):
+                        vis[r, kk] = kk < job.prefix or kk >= lo[r]
+                s_self = np.where(vis, s_self, -np.inf)
+                s = np.concatenate(scores + [s_self], axis=1) / math.sqrt(hd)
+                v = np.concatenate(vals + [vn[t0:t0 + n, kv]], axis=0)
+                m = s.max(axis=1, keepdims=True)
+                e = np.exp(s - m)
+                want = (e / e.sum(axis=1, keepdims=True)) @ v
+                worst = max(worst, float(np.abs(got[t0:t0 + n, head] - want).max()))
+    assert worst < 2e-2, worst

@@ -21,6 +21,8 @@ ap.add_argument("--hkv", type=int, default=8)
 ap.add_argument("--heads", type=int, default=32)
 ap.add_argument("--target", type=int, default=0)
 ap.add_argument("--order", default="query")
+ap.add_argument("--schedule", default=None, help="chunk | query (default: by batch size)")
+ap.add_argument("--chunk-m", type=int, default=2, help="M tiles per chunk-major work")
 args = ap.parse_args()
 
 dev = torch.device("cuda", 0)
@@ -83,15 +85,16 @@ if args.stage in ("2", "both"):
     q = [rng.integers(3, 1000, 32).tolist() for _ in range(B)]
     tabs, n_ctx = sess.chunks_for(ids)
     jobs = [engine.label_job(tabs[i], int(n_ctx[i]), q[i], sess.label_ids) for i in range(B)]
-    plan = engine.Stage2Plan(dm, jobs, args.target or None, args.order)
+    plan = engine.Stage2Plan(dm, jobs, args.target or None, args.order, schedule=args.schedule)
+    if plan.schedule == "chunk" and args.chunk_m != 2:
+        plan.sched = engine.ChunkMajorSchedule(dm, jobs, plan.new, num_m=args.chunk_m)
+        for name in ("works", "n_works", "n_merge", "merges", "max_rows", "part_o", "part_lse"):
+            setattr(plan, name, getattr(plan.sched, name))
     qkv = torch.randn(plan.n_tok, stride, device=dev).to(torch.bfloat16)
     out = torch.empty(plan.n_tok, qw, dtype=torch.bfloat16, device=dev)
     aux = (plan.k_aux, plan.v_aux, plan.aux_rows, 1)
     def k3():
-        ops.attention(q=qkv, q_tok_stride=stride, tok_pos=plan.pos, tok_lo=plan.lo, rope=plan.rope,
-                      pool=st.planes(), aux=aux, n_heads=cfg.n_heads, n_kv_heads=cfg.n_kv_heads, head_dim=128,
-                      works_dev=plan.works, n_works=plan.n_works, segs_dev=plan.segs_ptr(0), num_m=plan.num_m,
-                      out=out, out_tok_stride=qw, part_o=plan.part_o, part_lse=plan.part_lse)
+        plan.sched.launch(dm, plan.new, 0, qkv, out, st.planes())
     def k3m():
         if plan.n_merge:
             ops.lse_merge(plan.part_o, plan.part_lse, plan.merges, plan.n_merge, plan.max_rows, cfg.n_heads,
@@ -99,5 +102,5 @@ if args.stage in ("2", "both"):
     ms = timeit(k3, args.reps)
     mm = timeit(k3m, args.reps)
     by = plan.kv_tokens * 2 * cfg.n_kv_heads * 128 * 2 + 2 * plan.n_tok * qw * 2
-    print(f"K3: B={B} {plan.n_works} works num_m={plan.num_m}, {ms:.3f} ms, {by/ms/1e6:.1f} GB/s "
+    print(f"K3 [{plan.schedule}]: B={B} {plan.n_works} works num_m={plan.sched.num_m if hasattr(plan.sched, 'num_m') else plan.num_m}, {ms:.3f} ms, {by/ms/1e6:.1f} GB/s "
           f"({by/ms/1e6/hbm*100:.1f}% of {hbm}); merge {mm:.3f} ms ({plan.n_merge} groups)", flush=True)
