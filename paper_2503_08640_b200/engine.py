@@ -672,88 +672,27 @@ class ChunkMajorSchedule:
     def __init__(self, dm, jobs, nt: NewTokens, chunk_tables=None, num_m: int = 2):
         torch = _torch()
         c = dm.config
-        gs, hkv, hd = c.group_size, c.n_kv_heads, c.head_dim
+        hd = c.head_dim
         tables = chunk_tables if chunk_tables is not None else [j.chunks for j in jobs]
-        slab = (128 * num_m) // gs
-        if slab < 1:
-            raise ConfigError(f"group size {gs} exceeds the {128 * num_m} rows of one K3 work")
         self.num_m = num_m
-        pos = nt.pos_host.astype(np.int64)
-        n_new = np.asarray(nt.n_new, np.int64)
-        tabs = [np.asarray(t, dtype=np.int64).reshape(-1, 3) for t in tables]
-        n_split = np.array([len(t) + 1 for t in tabs], np.int64)
-        tokbase = np.concatenate([[0], np.cumsum(n_split * n_new)])
-        tot = int(tokbase[-1])  # partial tokens per kv head
-        kv_rows = tot * gs
-        # (query, chunk) pairs, grouped by chunk (pool row, length)
-        qi = np.repeat(np.arange(len(jobs)), n_split - 1)
-        ch = np.concatenate(tabs) if len(qi) else np.zeros((0, 3), np.int64)
-        sidx = np.concatenate([np.arange(len(t)) for t in tabs]) if len(qi) else np.zeros(0, np.int64)
-        key = ch[:, 0] * (1 << 24) + ch[:, 1] if len(qi) else np.zeros(0, np.int64)
-        order = np.lexsort((qi, key))
-        segs, works, entries = [], [], []
-        n_map = 0
-        if len(order):
-            keys_sorted = key[order]
-            starts = np.flatnonzero(np.r_[True, keys_sorted[1:] != keys_sorted[:-1]])
-            ends = np.r_[starts[1:], len(order)]
-            for a, b in zip(starts, ends):
-                pairs = order[a:b]
-                row, cnt = int(ch[pairs[0], 0]), int(ch[pairs[0], 1])
-                # map entries of every (query, token) row against this chunk
-                q_of = qi[pairs]
-                nn = n_new[q_of]
-                rep = np.repeat(np.arange(len(pairs)), nn)
-                tok_local = np.arange(int(nn.sum())) - np.repeat(np.cumsum(nn) - nn, nn)
-                q_rep = q_of[rep]
-                tok = nt.tok0[q_rep] + tok_local
-                rope_row = pos[tok] - ch[pairs, 2][rep]
-                part = tokbase[q_rep] + sidx[pairs][rep] * n_new[q_rep] + tok_local
-                e = np.stack([tok, rope_row, part, np.zeros_like(tok)], axis=1)
-                entries.append(e)
-                n_e = len(e)
-                k = -(-n_e // slab)
-                size = -(-n_e // k)
-                sb = len(segs)
-                segs.append((0, 0, row, cnt, SEG_FULL, 0))
-                for kv in range(hkv):
-                    for t0 in range(0, n_e, size):
-                        works.append((n_map + t0, min(size, n_e - t0), 0, kv, sb, sb + 1, 0, nat.OUT_MAPPED,
-                                      kv * kv_rows))
-                n_map += n_e
-        merges = []
-        for q, j in enumerate(jobs):
-            n, s_last = int(n_new[q]), int(n_split[q]) - 1
-            q0 = int(nt.tok0[q])
-            k = -(-n // slab)
-            size = -(-n // k)
-            for t0 in range(0, n, size):
-                ntk = min(size, n - t0)
-                sb = len(segs)
-                segs.append((1, 0, int(nt.aux_row0[q]), t0 + ntk, SEG_SELF, 0))
-                for kv in range(hkv):
-                    works.append((q0 + t0, ntk, q0, kv, sb, sb + 1, j.prefix, nat.OUT_PARTIAL,
-                                  kv * kv_rows + (int(tokbase[q]) + s_last * n + t0) * gs))
-            for kv in range(hkv):
-                merges.append((kv * kv_rows + int(tokbase[q]) * gs, n * gs, s_last + 1, q0, kv))
-        emap = np.concatenate(entries) if entries else np.zeros((1, 4), np.int64)
-        self.kv_tokens = int(sum(int(t[:, 1].sum()) for t in tabs))
+        t = chunk_major_tables(tables, nt.n_new, nt.pos_host, nt.aux_row0, [j.prefix for j in jobs], c.group_size,
+                               c.n_kv_heads, num_m)
+        emap, works, segs, merges = t["row_map"], t["works"], t["segs"], t["merges"]
+        self.kv_tokens = t["kv_tokens"]
         self.n_works, self.n_segs, self.n_merge = len(works), len(segs), len(merges)
         dev = dm.device
-        self.row_map = ops.to_device(np.ascontiguousarray(emap.astype(np.int32)).view(ops.ROWMAP_DTYPE).reshape(-1),
-                                     dev)
-        self.works = ops.to_device(_work_array(works), dev)
-        self.segs = ops.to_device(_per_layer_segs(_seg_array(segs), c.n_layers), dev)
-        self.merges = ops.to_device(_merge_array(merges), dev) if merges else None
-        self.max_rows = max((m[1] for m in merges), default=0)
+        self.row_map = ops.to_device(emap.view(ops.ROWMAP_DTYPE).reshape(-1), dev)
+        self.works = ops.to_device(works, dev)
+        self.segs = ops.to_device(_per_layer_segs(segs, c.n_layers), dev)
+        self.merges = ops.to_device(merges, dev) if len(merges) else None
+        self.max_rows = t["max_rows"]
         self.rope = dm.rope_for(max(nt.max_pos, int(emap[:, 1].max())) + 1)
-        self.part_rows = kv_rows * hkv
+        self.part_rows = t["part_rows"]
         # bf16 partials: a normalised partial row is a convex combination of V rows,
         # so one bf16 rounding (2^-9 relative) before the merge adds at most the
         # error of the final bf16 output; it halves the partial traffic
         self.part_o = torch.empty((max(self.part_rows, 1), hd), dtype=torch.bfloat16, device=dev)
         self.part_lse = torch.empty((max(self.part_rows, 1),), dtype=torch.float32, device=dev)
-
         self.n_real_works, self.n_real_segs = self.n_works, self.n_segs
 
     def pad_to(self, works_cap: int, segs_cap: int) -> None:
@@ -797,6 +736,109 @@ class ChunkMajorSchedule:
                       works_dev=self.works, n_works=self.n_works, segs_dev=self.segs_ptr(layer), num_m=self.num_m,
                       out=out, out_tok_stride=qw, part_o=self.part_o if part_o is None else part_o,
                       part_lse=self.part_lse if part_lse is None else part_lse, row_map=self.row_map)
+
+
+def chunk_major_tables(tables, n_new, pos_host, aux_row0, prefixes, gs: int, hkv: int, num_m: int = 2) -> dict:
+    """Host tables of a chunk-major K3 launch (ChunkMajorSchedule), vectorised
+    numpy: the row map, works (chunk works kv-major then balanced row slices,
+    then each query's SELF works), segments (one FULL per distinct chunk, one
+    SELF per query slab) and the K3m merge groups."""
+    slab = (128 * num_m) // gs
+    if slab < 1:
+        raise ConfigError(f"group size {gs} exceeds the {128 * num_m} rows of one K3 work")
+    n_jobs = len(n_new)
+    pos = np.asarray(pos_host, np.int64)
+    n_new = np.asarray(n_new, np.int64)
+    tok0 = np.concatenate([[0], np.cumsum(n_new)[:-1]]).astype(np.int64)
+    tabs = [np.asarray(t, dtype=np.int64).reshape(-1, 3) for t in tables]
+    n_ch = np.array([len(t) for t in tabs], np.int64)
+    n_split = n_ch + 1
+    tokbase = np.concatenate([[0], np.cumsum(n_split * n_new)])
+    kv_rows = int(tokbase[-1]) * gs  # partial rows per kv head
+    # ---- (query, chunk) pairs grouped by chunk (pool row, length), queries ascending
+    qi = np.repeat(np.arange(n_jobs), n_ch)
+    ch = np.concatenate(tabs) if len(qi) else np.zeros((0, 3), np.int64)
+    sidx = np.arange(len(qi)) - np.repeat(np.cumsum(n_ch) - n_ch, n_ch)
+    order = np.lexsort((qi, ch[:, 1], ch[:, 0]))
+    qi, ch, sidx = qi[order], ch[order], sidx[order]
+    # ---- row-map entries: every (pair, token) in pair order
+    ne = n_new[qi]
+    pair_e0 = np.cumsum(ne) - ne
+    rep = np.repeat(np.arange(len(qi)), ne)
+    local = np.arange(int(ne.sum())) - pair_e0[rep]
+    q_rep = qi[rep]
+    tok = tok0[q_rep] + local
+    emap = np.zeros((max(len(tok), 1), 4), np.int32)
+    if len(tok):
+        emap[: len(tok), 0] = tok
+        emap[: len(tok), 1] = pos[tok] - ch[rep, 2]
+        emap[: len(tok), 2] = tokbase[q_rep] + sidx[rep] * n_new[q_rep] + local
+    # ---- one FULL segment + works per distinct chunk: kv-major, then balanced slices
+    if len(qi):
+        newkey = np.r_[True, (ch[1:, 0] != ch[:-1, 0]) | (ch[1:, 1] != ch[:-1, 1])]
+        kstart = np.flatnonzero(newkey)
+        e_cnt = np.add.reduceat(ne, kstart)
+        e0 = pair_e0[kstart]
+        k = -(-e_cnt // slab)
+        size = -(-e_cnt // k)
+        n_keys = len(kstart)
+        blk = hkv * k  # works per chunk
+        kw = np.repeat(np.arange(n_keys), blk)
+        within = np.arange(int(blk.sum())) - np.repeat(np.cumsum(blk) - blk, blk)
+        kv = within // k[kw]
+        sl = within % k[kw]
+        t0 = sl * size[kw]
+        cw = np.zeros(len(kw), dtype=ops.WORK_DTYPE)
+        cw["q_tok0"] = e0[kw] + t0
+        cw["n_tok"] = np.minimum(size[kw], e_cnt[kw] - t0)
+        cw["kv_head"] = kv
+        cw["seg_begin"] = kw
+        cw["seg_end"] = kw + 1
+        cw["out_mode"] = nat.OUT_MAPPED
+        cw["part_row0"] = kv.astype(np.int64) * kv_rows
+        cseg = np.zeros(n_keys, dtype=ops.SEG_DTYPE)
+        cseg["row0"] = ch[kstart, 0]
+        cseg["n_tok"] = ch[kstart, 1]
+        cseg["kind"] = SEG_FULL
+    else:
+        cw = np.zeros(0, dtype=ops.WORK_DTYPE)
+        cseg = np.zeros(0, dtype=ops.SEG_DTYPE)
+        n_keys = 0
+    # ---- SELF works (each query's own tokens, causal tree) into its last split
+    ks = -(-n_new // slab)
+    ssize = -(-n_new // ks)
+    sq = np.repeat(np.arange(n_jobs), ks)
+    st0 = (np.arange(int(ks.sum())) - np.repeat(np.cumsum(ks) - ks, ks)) * ssize[sq]
+    sn = np.minimum(ssize[sq], n_new[sq] - st0)
+    sseg = np.zeros(len(sq), dtype=ops.SEG_DTYPE)
+    sseg["src"] = 1
+    sseg["row0"] = np.asarray(aux_row0, np.int64)[sq]
+    sseg["n_tok"] = st0 + sn
+    sseg["kind"] = SEG_SELF
+    prefix = np.asarray(prefixes, np.int64)
+    sw = np.zeros((len(sq), hkv), dtype=ops.WORK_DTYPE)
+    kvs = np.arange(hkv)[None, :]
+    sw["q_tok0"] = (tok0[sq] + st0)[:, None]
+    sw["n_tok"] = sn[:, None]
+    sw["self_tok0"] = tok0[sq][:, None]
+    sw["kv_head"] = kvs
+    sw["seg_begin"] = (n_keys + np.arange(len(sq)))[:, None]
+    sw["seg_end"] = sw["seg_begin"] + 1
+    sw["prefix"] = prefix[sq][:, None]
+    sw["out_mode"] = nat.OUT_PARTIAL
+    sw["part_row0"] = kvs * kv_rows + ((tokbase[sq] + n_ch[sq] * n_new[sq] + st0) * gs)[:, None]
+    works = np.concatenate([cw, sw.reshape(-1)])
+    segs = np.concatenate([cseg, sseg])
+    mg = np.zeros((n_jobs, hkv), dtype=ops.MERGE_DTYPE)
+    mg["part_row0"] = kvs * kv_rows + (tokbase[:-1] * gs)[:, None]
+    mg["rows"] = (n_new * gs)[:, None]
+    mg["n_splits"] = n_split[:, None]
+    mg["q_tok0"] = tok0[:, None]
+    mg["kv_head"] = kvs
+    merges = mg.reshape(-1)
+    return {"row_map": emap, "works": works, "segs": segs, "merges": merges,
+            "kv_tokens": int(ch[:, 1].sum()) if len(qi) else 0,
+            "max_rows": int((n_new * gs).max()) if n_jobs else 0, "part_rows": kv_rows * hkv}
 
 
 def stage2_schedule_kind(n_jobs: int) -> str:

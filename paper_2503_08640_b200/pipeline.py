@@ -290,6 +290,48 @@ class Stage2Session:
         s, best = graphs[key].replay(plan, scorer)
         return ids, s, best
 
+    def answer_stream(self, batches):
+        """Pipelined answer() over an iterable of (scores, query_ids_list)
+        batches; yields (ids, scores [B, n_labels], argmax [B]) as HOST arrays,
+        in order.  Batch i+1's K4 selection runs on a side stream while batch
+        i's forward replays on the current stream, so its ids come back, and
+        its chunk tables are planned on the host, while the GPU is busy; each
+        batch's results are copied out to pinned memory right behind its
+        replay (the captured graph reuses its output buffers)."""
+        import torch
+
+        main = torch.cuda.current_stream(self.dm.device)
+        side = torch.cuda.Stream(self.dm.device)
+        pending = None
+        for scores, q_ids in batches:
+            with torch.cuda.stream(side):
+                if not isinstance(scores, torch.Tensor):
+                    scores = torch.from_numpy(np.ascontiguousarray(scores))
+                ids_dev = engine.ops.topk_select(scores.to(self.dm.device, non_blocking=True), self.budget,
+                                                 self.ordering)
+                ids = ids_dev.cpu().numpy().astype(np.int64)  # waits for the side stream only
+            jobs, plan = self.plan(ids, q_ids)
+            scorer = engine.LabelScorer(self.dm, plan, jobs, len(self.label_ids))
+            key = engine.plan_key(plan, scorer)
+            graphs = self.__dict__.setdefault("_graphs", {})
+            if key not in graphs or not engine.fits_graph(graphs[key], plan):
+                main.synchronize()
+                graphs[key] = engine.GraphedStage2(self.dm, self.cache.store, jobs, plan, len(self.label_ids))
+            s_dev, best_dev = graphs[key].replay(plan, scorer)
+            s_host = torch.empty(s_dev.shape, dtype=s_dev.dtype, pin_memory=True)
+            b_host = torch.empty(best_dev.shape, dtype=best_dev.dtype, pin_memory=True)
+            s_host.copy_(s_dev, non_blocking=True)
+            b_host.copy_(best_dev, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(main)
+            if pending is not None:
+                pending[0].synchronize()
+                yield pending[1:]
+            pending = (ev, ids, s_host.numpy(), b_host.numpy())
+        if pending is not None:
+            pending[0].synchronize()
+            yield pending[1:]
+
 
 class Runner:
     """Inference session over (weights, cache, index) (pipeline.py:322-446).

@@ -129,6 +129,16 @@ def test_stage2_batched_k4_path_matches_reference(name):
     assert [lab for lab, _ in out] == single
     for qi, (lab, qm) in enumerate(out):
         assert qm.attended_pairs == meta["queries"][qi]["attended_pairs"]
+    # the pipelined batch entry point: same ids and labels, batch by batch
+    q_ids = [tokenizer.encode(task.template.render_query(t)) for t in texts]
+    half = len(texts) // 2
+    batches = [(scores[:half], q_ids[:half]), (scores[half:], q_ids[half:])]
+    got = list(sess.answer_stream(batches))
+    for (ids_b, s_b, best_b), (sc_b, q_b) in zip(got, batches):
+        ids1, s1, best1 = sess.answer(sc_b, q_b)
+        np.testing.assert_array_equal(ids_b, ids1)
+        np.testing.assert_array_equal(best_b, best1.cpu().numpy())
+        np.testing.assert_allclose(s_b, s1.cpu().numpy(), atol=1e-5)
 
 
 def test_forward_query_logits_c1():
