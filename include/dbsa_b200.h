@@ -231,6 +231,10 @@ int dbsa_bm25_scores(const int32_t *term_ids, int64_t n_queries, int32_t max_ter
  * kernels.py:103-123): RMSNorm fp32 -> bf16, and silu(gate) * up. */
 int dbsa_rmsnorm(const float *x, const float *weight, void *out, int64_t rows, int64_t dim,
                  float eps, void *stream);
+/* Residual add fused with the next norm (model.py:352-359): x += delta (fp32,
+ * in place), then out = bf16 RMSNorm(x) * weight. */
+int dbsa_add_rmsnorm(float *x, const float *delta, const float *weight, void *out, int64_t rows, int64_t dim,
+                     float eps, void *stream);
 int dbsa_silu_mul(const void *gate_up, void *out, int64_t rows, int64_t ffn, void *stream);
 
 /* Label scoring gather (model.py:414-417,441-443): for each scored row r,

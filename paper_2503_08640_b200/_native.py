@@ -24,6 +24,7 @@ EXPORTED_SYMBOLS = (
     "dbsa_rope_table",
     "dbsa_topk_select",
     "dbsa_rmsnorm",
+    "dbsa_add_rmsnorm",
     "dbsa_silu_mul",
     "dbsa_label_logprob",
     "dbsa_bm25_scores",
@@ -144,6 +145,7 @@ def load_library(path: Path | str | None = None) -> ctypes.CDLL:
         lib.dbsa_rope_table.argtypes = [_vp, _i64, _vp, _i32, _i64, _vp]
         lib.dbsa_topk_select.argtypes = [_vp, _i64, _i64, _i64, _i32, _vp, _vp]
         lib.dbsa_rmsnorm.argtypes = [_vp, _vp, _vp, _i64, _i64, _f32, _vp]
+        lib.dbsa_add_rmsnorm.argtypes = [_vp, _vp, _vp, _vp, _i64, _i64, _f32, _vp]
         lib.dbsa_silu_mul.argtypes = [_vp, _vp, _i64, _i64, _vp]
         lib.dbsa_label_logprob.argtypes = [_vp, _i64, _i64, _vp, _vp, _vp]
         lib.dbsa_bm25_scores.argtypes = [_vp, _i64, _i32, _vp, _vp, _vp, _i64, ctypes.c_double, _vp, _vp]

@@ -24,6 +24,29 @@ __device__ __forceinline__ float warp_sum(float v) {
 
 // One warp per (group, row): lse = log sum_s exp(lse_s); O = sum_s exp(lse_s - lse) O_s.
 // This is the split form of the single softmax of kernels._softmax64 (kernels.py:52-56).
+// Lanes first own splits (max, sum, per-split weights), then own 4 head dims
+// each: the weights are broadcast by shuffle and 8 splits' partial rows are
+// loaded before they are accumulated, so the loads of a row are in flight together.
+template <bool BF16>
+__device__ __forceinline__ void load4(const void *base, int64_t off, float (&v)[4]) {
+  if constexpr (BF16) {
+    const uint2 u = *reinterpret_cast<const uint2 *>(reinterpret_cast<const __nv_bfloat16 *>(base) + off);
+    const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162 *>(&u.x);
+    const __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162 *>(&u.y);
+    v[0] = __low2float(a), v[1] = __high2float(a), v[2] = __low2float(b), v[3] = __high2float(b);
+  } else {
+    const float4 f = *reinterpret_cast<const float4 *>(reinterpret_cast<const float *>(base) + off);
+    v[0] = f.x, v[1] = f.y, v[2] = f.z, v[3] = f.w;
+  }
+}
+template <bool BF16>
+__device__ __forceinline__ float load1(const void *base, int64_t off) {
+  if constexpr (BF16)
+    return __bfloat162float(reinterpret_cast<const __nv_bfloat16 *>(base)[off]);
+  else
+    return reinterpret_cast<const float *>(base)[off];
+}
+
 template <bool BF16>
 __global__ void lse_merge_kernel(DbsaMergeArgs a) {
   const DbsaMergeGroup g = a.groups[blockIdx.y];
@@ -32,64 +55,141 @@ __global__ void lse_merge_kernel(DbsaMergeArgs a) {
   if (r >= g.rows) return;
   const int hd = a.head_dim, gs = a.n_heads / a.n_kv_heads;
   const int64_t sstride = a.split_stride > 0 ? a.split_stride : g.rows;
-  float mx = -INFINITY;
-  for (int s = lane; s < g.n_splits; s += 32) mx = fmaxf(mx, a.part_lse[g.part_row0 + (int64_t)s * sstride + r]);
+  const int64_t row0 = g.part_row0 + r;
+  // one read of each split's LSE: lane s holds split s (a second pass only past 32 splits)
+  const float l_own = lane < g.n_splits ? a.part_lse[row0 + (int64_t)lane * sstride] : -INFINITY;
+  float mx = l_own;
+  for (int s = lane + 32; s < g.n_splits; s += 32) mx = fmaxf(mx, a.part_lse[row0 + (int64_t)s * sstride]);
   mx = warp_max(mx);
-  float tot = 0.f;
-  for (int s = lane; s < g.n_splits; s += 32) {
-    const float l = a.part_lse[g.part_row0 + (int64_t)s * sstride + r];
+  float tot = l_own == -INFINITY ? 0.f : __expf(l_own - mx);
+  for (int s = lane + 32; s < g.n_splits; s += 32) {
+    const float l = a.part_lse[row0 + (int64_t)s * sstride];
     tot += l == -INFINITY ? 0.f : __expf(l - mx);
   }
   tot = warp_sum(tot);
   const float inv = tot > 0.f ? 1.f / tot : 0.f;
   const int t = g.q_tok0 + r / gs, head = g.kv_head * gs + r % gs;
   __nv_bfloat16 *dst = reinterpret_cast<__nv_bfloat16 *>(a.out) + (int64_t)t * a.out_tok_stride + (int64_t)head * hd;
-  for (int d0 = 0; d0 < hd; d0 += 32 * 4) {
+  const bool vec = (hd & 3) == 0;
+  for (int d0 = 0; d0 < hd; d0 += 128) {
+    const int d = d0 + lane * 4;
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int s = 0; s < g.n_splits; ++s) {
-      const float l = a.part_lse[g.part_row0 + (int64_t)s * sstride + r];
-      if (l == -INFINITY) continue;
-      const float wgt = __expf(l - mx) * inv;
-      const int64_t off = (g.part_row0 + (int64_t)s * sstride + r) * hd;
-      if constexpr (BF16) {
-        const __nv_bfloat16 *src = reinterpret_cast<const __nv_bfloat16 *>(a.part_o) + off;
-        if ((hd & 3) == 0 && d0 + lane * 4 + 3 < hd) {
-          const uint2 v = *reinterpret_cast<const uint2 *>(src + d0 + lane * 4);
-          const __nv_bfloat162 v0 = *reinterpret_cast<const __nv_bfloat162 *>(&v.x);
-          const __nv_bfloat162 v1 = *reinterpret_cast<const __nv_bfloat162 *>(&v.y);
-          acc[0] += wgt * __low2float(v0);
-          acc[1] += wgt * __high2float(v0);
-          acc[2] += wgt * __low2float(v1);
-          acc[3] += wgt * __high2float(v1);
-        } else {
-          for (int i = 0; i < 4; ++i)
-            if (d0 + lane * 4 + i < hd) acc[i] += wgt * __bfloat162float(src[d0 + lane * 4 + i]);
+    for (int s0 = 0; s0 < g.n_splits; s0 += 32) {
+      const int cnt = min(32, g.n_splits - s0);
+      float wl = 0.f;
+      if (lane < cnt) {
+        const float l = s0 == 0 ? l_own : a.part_lse[row0 + (int64_t)(s0 + lane) * sstride];
+        wl = l == -INFINITY ? 0.f : __expf(l - mx) * inv;
+      }
+      int k = 0;
+      if (vec) {  // warp-uniform: lanes past the head read column 0 and drop it
+        const int dl = d + 3 < hd ? d : 0;
+        for (; k + 8 <= cnt; k += 8) {
+          float v[8][4];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) load4<BF16>(a.part_o, (row0 + (int64_t)(s0 + k + u) * sstride) * hd + dl, v[u]);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const float wu = __shfl_sync(0xffffffffu, wl, k + u);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) acc[i] += wu * v[u][i];
+          }
+        }
+        for (; k < cnt; ++k) {
+          float v[4];
+          load4<BF16>(a.part_o, (row0 + (int64_t)(s0 + k) * sstride) * hd + dl, v);
+          const float wu = __shfl_sync(0xffffffffu, wl, k);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) acc[i] += wu * v[i];
         }
       } else {
-        const float *src = reinterpret_cast<const float *>(a.part_o) + off;
-        if ((hd & 3) == 0 && d0 + lane * 4 + 3 < hd) {
-          const float4 v = *reinterpret_cast<const float4 *>(src + d0 + lane * 4);
-          acc[0] += wgt * v.x;
-          acc[1] += wgt * v.y;
-          acc[2] += wgt * v.z;
-          acc[3] += wgt * v.w;
-        } else {
+        for (; k < cnt; ++k) {
+          const float wu = __shfl_sync(0xffffffffu, wl, k);
+          const int64_t off = (row0 + (int64_t)(s0 + k) * sstride) * hd + d;
           for (int i = 0; i < 4; ++i)
-            if (d0 + lane * 4 + i < hd) acc[i] += wgt * src[d0 + lane * 4 + i];
+            if (d + i < hd) acc[i] += wu * load1<BF16>(a.part_o, off + i);
         }
       }
     }
-    for (int i = 0; i < 4; ++i)
-      if (d0 + lane * 4 + i < hd) dst[d0 + lane * 4 + i] = __float2bfloat16(acc[i]);
+    if (vec && d + 3 < hd) {
+      __nv_bfloat162 lo = __floats2bfloat162_rn(acc[0], acc[1]), hi = __floats2bfloat162_rn(acc[2], acc[3]);
+      uint2 u;
+      u.x = *reinterpret_cast<uint32_t *>(&lo);
+      u.y = *reinterpret_cast<uint32_t *>(&hi);
+      *reinterpret_cast<uint2 *>(dst + d) = u;
+    } else {
+      for (int i = 0; i < 4; ++i)
+        if (d + i < hd) dst[d + i] = __float2bfloat16(acc[i]);
+    }
   }
 }
 
 // x fp32 [rows, dim] -> bf16 x * rsqrt(mean(x^2) + eps) * w (kernels.rms_norm, kernels.py:103-112).
-__global__ void rmsnorm_kernel(const float *x, const float *w, __nv_bfloat16 *out, int64_t dim, float eps) {
+// ADD: first x += delta in place -- the residual add of model.py:352-359 fused
+// with the norm that reads the same row.  float4 path: each thread keeps its
+// VPT float4 of the row in registers between the sum and the scale pass.
+template <bool ADD, int VPT>
+__global__ void rmsnorm4_kernel(float *x, const float *delta, const float *w, __nv_bfloat16 *out, int64_t dim,
+                                float eps) {
   const int64_t row = blockIdx.x;
-  const float *xr = x + row * dim;
+  float4 *xr = reinterpret_cast<float4 *>(x + row * dim);
+  const int n4 = (int)(dim >> 2);
+  float4 v[VPT];
   float ss = 0.f;
-  for (int64_t i = threadIdx.x; i < dim; i += blockDim.x) ss += xr[i] * xr[i];
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) {
+    const int i = threadIdx.x + k * blockDim.x;
+    if (i < n4) {
+      v[k] = xr[i];
+      if constexpr (ADD) {
+        const float4 d = reinterpret_cast<const float4 *>(delta + row * dim)[i];
+        v[k].x += d.x, v[k].y += d.y, v[k].z += d.z, v[k].w += d.w;
+        xr[i] = v[k];
+      }
+      ss += v[k].x * v[k].x + v[k].y * v[k].y + v[k].z * v[k].z + v[k].w * v[k].w;
+    }
+  }
+  __shared__ float red[32];
+  ss = warp_sum(ss);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    t = warp_sum(t);
+    if (threadIdx.x == 0) red[0] = t;
+  }
+  __syncthreads();
+  const float inv = rsqrtf(red[0] / (float)dim + eps);
+  uint2 *orow = reinterpret_cast<uint2 *>(out + row * dim);
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) {
+    const int i = threadIdx.x + k * blockDim.x;
+    if (i < n4) {
+      const float4 ww = reinterpret_cast<const float4 *>(w)[i];
+      __nv_bfloat162 lo = __floats2bfloat162_rn(v[k].x * inv * ww.x, v[k].y * inv * ww.y);
+      __nv_bfloat162 hi = __floats2bfloat162_rn(v[k].z * inv * ww.z, v[k].w * inv * ww.w);
+      uint2 u;
+      u.x = *reinterpret_cast<uint32_t *>(&lo);
+      u.y = *reinterpret_cast<uint32_t *>(&hi);
+      orow[i] = u;
+    }
+  }
+}
+
+template <bool ADD>
+__global__ void rmsnorm_kernel(float *x, const float *delta, const float *w, __nv_bfloat16 *out, int64_t dim,
+                               float eps) {
+  const int64_t row = blockIdx.x;
+  float *xr = x + row * dim;
+  float ss = 0.f;
+  for (int64_t i = threadIdx.x; i < dim; i += blockDim.x) {
+    float v = xr[i];
+    if constexpr (ADD) {
+      v += delta[row * dim + i];
+      xr[i] = v;
+    }
+    ss += v * v;
+  }
   __shared__ float red[32];
   ss = warp_sum(ss);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
@@ -104,14 +204,55 @@ __global__ void rmsnorm_kernel(const float *x, const float *w, __nv_bfloat16 *ou
   for (int64_t i = threadIdx.x; i < dim; i += blockDim.x) out[row * dim + i] = __float2bfloat16(xr[i] * inv * w[i]);
 }
 
+template <bool ADD>
+static int launch_rmsnorm(float *x, const float *delta, const float *weight, void *out, int64_t rows, int64_t dim,
+                          float eps, cudaStream_t st) {
+  if (rows <= 0) return DBSA_OK;
+  __nv_bfloat16 *o = reinterpret_cast<__nv_bfloat16 *>(out);
+  const bool al = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(weight) |
+                    reinterpret_cast<uintptr_t>(out) | (ADD ? reinterpret_cast<uintptr_t>(delta) : 0)) & 15) == 0;
+  if (dim % 4 == 0 && al && dim <= 4 * 256 * 8) {
+    const int n4 = (int)(dim / 4);
+    if (n4 <= 256 * 4)
+      rmsnorm4_kernel<ADD, 4><<<(unsigned)rows, 256, 0, st>>>(x, delta, weight, o, dim, eps);
+    else
+      rmsnorm4_kernel<ADD, 8><<<(unsigned)rows, 256, 0, st>>>(x, delta, weight, o, dim, eps);
+  } else {
+    const int threads = dim >= 1024 ? 256 : (dim >= 256 ? 128 : 64);
+    rmsnorm_kernel<ADD><<<(unsigned)rows, threads, 0, st>>>(x, delta, weight, o, dim, eps);
+  }
+  return check_launch("rmsnorm");
+}
+
 // gate_up bf16 [rows, 2*ffn] (gate | up) -> silu(gate) * up (kernels.silu_gate, kernels.py:115-123).
+__device__ __forceinline__ float silu_f(float g) { return g / (1.f + __expf(-g)); }
 __global__ void silu_mul_kernel(const __nv_bfloat16 *gu, __nv_bfloat16 *out, int64_t rows, int64_t ffn) {
   const int64_t n = rows * ffn;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n; idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = idx / ffn, c = idx % ffn;
     const float g = __bfloat162float(gu[r * 2 * ffn + c]);
     const float u = __bfloat162float(gu[r * 2 * ffn + ffn + c]);
-    out[idx] = __float2bfloat16(g / (1.f + __expf(-g)) * u);
+    out[idx] = __float2bfloat16(silu_f(g) * u);
+  }
+}
+// 8 columns per thread (16-byte loads of gate and up), one CTA row-strip per y.
+__global__ void silu_mul8_kernel(const uint4 *gu, uint4 *out, int64_t rows, int64_t ffn8) {
+  for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
+    const uint4 *gr = gu + r * 2 * ffn8;
+    uint4 *orow = out + r * ffn8;
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < ffn8; c += (int64_t)gridDim.x * blockDim.x) {
+      const uint4 g4 = gr[c], u4 = gr[ffn8 + c];
+      const __nv_bfloat162 *g2 = reinterpret_cast<const __nv_bfloat162 *>(&g4);
+      const __nv_bfloat162 *u2 = reinterpret_cast<const __nv_bfloat162 *>(&u4);
+      uint4 o4;
+      __nv_bfloat162 *o2 = reinterpret_cast<__nv_bfloat162 *>(&o4);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 g = __bfloat1622float2(g2[i]), u = __bfloat1622float2(u2[i]);
+        o2[i] = __floats2bfloat162_rn(silu_f(g.x) * u.x, silu_f(g.y) * u.y);
+      }
+      orow[c] = o4;
+    }
   }
 }
 
@@ -162,21 +303,31 @@ extern "C" int dbsa_lse_merge(const DbsaMergeArgs *args, void *stream) {
 
 extern "C" int dbsa_rmsnorm(const float *x, const float *weight, void *out, int64_t rows, int64_t dim, float eps,
                             void *stream) {
-  using namespace dbsa;
-  if (rows <= 0) return DBSA_OK;
-  const int threads = dim >= 1024 ? 256 : (dim >= 256 ? 128 : 64);
-  rmsnorm_kernel<<<(unsigned)rows, threads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      x, weight, reinterpret_cast<__nv_bfloat16 *>(out), dim, eps);
-  return check_launch("rmsnorm");
+  return dbsa::launch_rmsnorm<false>(const_cast<float *>(x), nullptr, weight, out, rows, dim, eps,
+                                     reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int dbsa_add_rmsnorm(float *x, const float *delta, const float *weight, void *out, int64_t rows, int64_t dim,
+                                float eps, void *stream) {
+  return dbsa::launch_rmsnorm<true>(x, delta, weight, out, rows, dim, eps, reinterpret_cast<cudaStream_t>(stream));
 }
 
 extern "C" int dbsa_silu_mul(const void *gate_up, void *out, int64_t rows, int64_t ffn, void *stream) {
   using namespace dbsa;
   if (rows <= 0) return DBSA_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (ffn % 8 == 0 && (reinterpret_cast<uintptr_t>(gate_up) & 15) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+    const int64_t ffn8 = ffn / 8;
+    const int bx = (int)((ffn8 + 255) / 256);
+    const int by = (int)(rows < 65535 ? rows : 65535);
+    silu_mul8_kernel<<<dim3(bx, by), 256, 0, st>>>(reinterpret_cast<const uint4 *>(gate_up),
+                                                     reinterpret_cast<uint4 *>(out), rows, ffn8);
+    return check_launch("silu_mul");
+  }
   const int64_t n = rows * ffn;
   const int blocks = (int)((n + 255) / 256 < 148 * 32 ? (n + 255) / 256 : 148 * 32);
-  silu_mul_kernel<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      reinterpret_cast<const __nv_bfloat16 *>(gate_up), reinterpret_cast<__nv_bfloat16 *>(out), rows, ffn);
+  silu_mul_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16 *>(gate_up),
+                                          reinterpret_cast<__nv_bfloat16 *>(out), rows, ffn);
   return check_launch("silu_mul");
 }
 

@@ -297,20 +297,23 @@ def _decoder_gen(dm, ids_dev, attend, write_kv, n_layers=None):
     L = c.n_layers if n_layers is None else n_layers
     for layer in range(L):
         lw = dm.layers[layer]
-        ops.rmsnorm(h, lw["attn_norm"], c.norm_eps, out=s.x)
+        if layer == 0:
+            ops.rmsnorm(h, lw["attn_norm"], c.norm_eps, out=s.x)
+        else:  # the previous layer's FFN residual add, fused with this norm
+            ops.add_rmsnorm(h, s.proj, lw["attn_norm"], c.norm_eps, s.x)
         torch.mm(s.x, lw["wqkv"], out=s.qkv)
         write_kv(layer, s.qkv)
         yield layer
         attend(layer, s.qkv, s.att)
         mm_f32(s.att, lw["wo"], s.proj)
-        h.add_(s.proj)
-        ops.rmsnorm(h, lw["ffn_norm"], c.norm_eps, out=s.x)
+        ops.add_rmsnorm(h, s.proj, lw["ffn_norm"], c.norm_eps, s.x)
         for a in range(0, n, s.ffn_chunk):
             b = min(n, a + s.ffn_chunk)
             gu, act = s.gu[: b - a], s.act[: b - a]
             torch.mm(s.x[a:b], lw["wgu"], out=gu)
             ops.silu_mul(gu, c.ffn_dim, out=act)
             mm_f32(act, lw["wdown"], s.proj[a:b])
+    if L:
         h.add_(s.proj)
     return h
 

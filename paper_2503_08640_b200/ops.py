@@ -166,6 +166,14 @@ def rmsnorm(x, weight, eps: float, out=None):
     return out
 
 
+def add_rmsnorm(x, delta, weight, eps: float, out):
+    """x += delta (fp32, in place); out = bf16 RMSNorm(x) * weight."""
+    nat.check(nat.load_library().dbsa_add_rmsnorm(x.data_ptr(), delta.data_ptr(), weight.data_ptr(), out.data_ptr(),
+                                                  x.shape[0], x.shape[1], float(eps), nat.stream_handle()))
+    _launched()
+    return out
+
+
 def silu_mul(gate_up, ffn: int, out=None):
     import torch
 
