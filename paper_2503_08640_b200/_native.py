@@ -9,12 +9,15 @@ reference exception hierarchy (errors.py:4-29 of the reference package).
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
 from . import errors
 
 LIB_PATH = Path(__file__).resolve().parent / "libdbsa_sm100a.so"
+if os.environ.get("DBSA_LIB"):  # kernel A/B experiments (tools/build_variant.py): an alternative build
+    LIB_PATH = Path(os.environ["DBSA_LIB"])
 
 EXPORTED_SYMBOLS = (
     "dbsa_attention",

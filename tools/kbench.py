@@ -23,6 +23,7 @@ ap.add_argument("--target", type=int, default=0)
 ap.add_argument("--order", default="query")
 ap.add_argument("--schedule", default=None, help="chunk | query (default: by batch size)")
 ap.add_argument("--chunk-m", type=int, default=2, help="M tiles per chunk-major work")
+ap.add_argument("--dense", action="store_true", help="one contiguous T' chunk per query")
 args = ap.parse_args()
 
 dev = torch.device("cuda", 0)
@@ -84,6 +85,9 @@ if args.stage in ("2", "both"):
                     for _ in range(B)])
     q = [rng.integers(3, 1000, 32).tolist() for _ in range(B)]
     tabs, n_ctx = sess.chunks_for(ids)
+    if args.dense:  # one contiguous run of T' pool rows per query (the dense comparator)
+        Tp = int(n_ctx[0])
+        tabs = np.array([[[0, Tp, 0]]] * B, np.int64)
     jobs = [engine.label_job(tabs[i], int(n_ctx[i]), q[i], sess.label_ids) for i in range(B)]
     plan = engine.Stage2Plan(dm, jobs, args.target or None, args.order, schedule=args.schedule)
     if plan.schedule == "chunk" and args.chunk_m != 2:
