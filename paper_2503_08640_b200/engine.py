@@ -532,9 +532,9 @@ class NewTokens:
             raise ValidationError(f"position {int(pos.max())} exceeds max_seq_len {c.max_seq_len}")
         self.max_pos = int(pos.max())
         self.pos_host = pos
-        self.pos = torch.from_numpy(pos).to(dev, non_blocking=True)
-        self.lo = torch.from_numpy(lo).to(dev, non_blocking=True)
-        self.ids = torch.from_numpy(ids).to(dev, non_blocking=True)
+        self.pos = ops.h2d(pos, dev)
+        self.lo = ops.h2d(lo, dev)
+        self.ids = ops.h2d(ids, dev)
         self.pages = ops.to_device(_pages_for([(int(self.tok0[i]), self.n_new[i], int(self.aux_row0[i]))
                                                for i in range(len(jobs))]), dev)
         self.n_pages = int(sum(-(-n // PAGE) for n in self.n_new))
@@ -691,12 +691,33 @@ class ChunkMajorSchedule:
         self.max_rows = t["max_rows"]
         self.rope = dm.rope_for(max(nt.max_pos, int(emap[:, 1].max())) + 1)
         self.part_rows = t["part_rows"]
+        self._hd, self._part = hd, None
+        self.n_real_works, self.n_real_segs = self.n_works, self.n_segs
+
+    def _partials(self):
         # bf16 partials: a normalised partial row is a convex combination of V rows,
         # so one bf16 rounding (2^-9 relative) before the merge adds at most the
-        # error of the final bf16 output; it halves the partial traffic
-        self.part_o = torch.empty((max(self.part_rows, 1), hd), dtype=torch.bfloat16, device=dev)
-        self.part_lse = torch.empty((max(self.part_rows, 1),), dtype=torch.float32, device=dev)
-        self.n_real_works, self.n_real_segs = self.n_works, self.n_segs
+        # error of the final bf16 output; it halves the partial traffic.  Allocated
+        # on first use: a plan that only feeds a captured graph never needs its own.
+        if self._part is None:
+            torch = _torch()
+            n = max(self.part_rows, 1)
+            dev = self.works.device
+            self._part = (torch.empty((n, self._hd), dtype=torch.bfloat16, device=dev),
+                          torch.empty((n,), dtype=torch.float32, device=dev))
+        return self._part
+
+    @property
+    def part_o(self):
+        return self._partials()[0]
+
+    @part_o.setter
+    def part_o(self, v):
+        self._part = (v, self._partials()[1])
+
+    @property
+    def part_lse(self):
+        return self._partials()[1]
 
     def pad_to(self, works_cap: int, segs_cap: int) -> None:
         """Grow the device tables to fixed capacities (a captured graph's launch
@@ -869,9 +890,16 @@ class Stage2Plan:
             self.sched = AttnSchedule(dm, jobs, self.new, target_ctas=target_ctas, order=order)
         for name in ("tok0", "n_tok", "num_m", "pos", "lo", "ids", "pages", "n_pages", "k_aux", "v_aux", "aux_rows"):
             setattr(self, name, getattr(self.new, name))
-        for name in ("works", "n_works", "n_segs", "n_merge", "merges", "max_rows", "rope", "part_o", "part_lse",
-                     "kv_tokens"):
+        for name in ("works", "n_works", "n_segs", "n_merge", "merges", "max_rows", "rope", "kv_tokens"):
             setattr(self, name, getattr(self.sched, name))
+
+    @property
+    def part_o(self):
+        return self.sched.part_o
+
+    @property
+    def part_lse(self):
+        return self.sched.part_lse
 
     def segs_ptr(self, layer: int) -> int:
         return self.sched.segs_ptr(layer)
@@ -1123,9 +1151,9 @@ class LabelScorer:
                     prev = base + off + k
                 off += len(lab) - 1
         dev = dm.device
-        self.rows = torch.tensor(rows, dtype=torch.int64, device=dev)
-        self.targets = torch.tensor(targets, dtype=torch.int32, device=dev)
-        self.owner = torch.tensor(owner, dtype=torch.int64, device=dev)
+        self.rows = ops.h2d(np.asarray(rows, np.int64), dev)
+        self.targets = ops.h2d(np.asarray(targets, np.int32), dev)
+        self.owner = ops.h2d(np.asarray(owner, np.int64), dev)
         self.n_out = len(jobs) * n_labels
         self.n_labels = n_labels
 

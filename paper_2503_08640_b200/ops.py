@@ -73,6 +73,15 @@ def to_device(arr: np.ndarray, device):
     return t.pin_memory().to(device, non_blocking=True)
 
 
+def h2d(arr: np.ndarray, device):
+    """Typed host array -> device tensor through pinned memory: the copy is
+    stream-ordered and asynchronous (a pageable source would block the host
+    until the stream's earlier work finished)."""
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(arr)).pin_memory().to(device, non_blocking=True)
+
+
 def rope_table(rows: int, head_dim: int, theta: float, device, pos0: int = 0):
     """float32 [rows, hd/2, 2] table of (cos, sin)(pos * inv_freq) built on device in float64."""
     import torch

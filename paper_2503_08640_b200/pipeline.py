@@ -306,7 +306,7 @@ class Stage2Session:
         for scores, q_ids in batches:
             with torch.cuda.stream(side):
                 if not isinstance(scores, torch.Tensor):
-                    scores = torch.from_numpy(np.ascontiguousarray(scores))
+                    scores = torch.from_numpy(np.ascontiguousarray(scores)).pin_memory()
                 ids_dev = engine.ops.topk_select(scores.to(self.dm.device, non_blocking=True), self.budget,
                                                  self.ordering)
                 ids = ids_dev.cpu().numpy().astype(np.int64)  # waits for the side stream only

@@ -92,7 +92,7 @@ if args.stage in ("2", "both"):
     plan = engine.Stage2Plan(dm, jobs, args.target or None, args.order, schedule=args.schedule)
     if plan.schedule == "chunk" and args.chunk_m != 2:
         plan.sched = engine.ChunkMajorSchedule(dm, jobs, plan.new, num_m=args.chunk_m)
-        for name in ("works", "n_works", "n_merge", "merges", "max_rows", "part_o", "part_lse"):
+        for name in ("works", "n_works", "n_merge", "merges", "max_rows"):
             setattr(plan, name, getattr(plan.sched, name))
     qkv = torch.randn(plan.n_tok, stride, device=dev).to(torch.bfloat16)
     out = torch.empty(plan.n_tok, qw, dtype=torch.bfloat16, device=dev)

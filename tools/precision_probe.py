@@ -21,7 +21,7 @@ for name in ("c1", "g128", "m64ex"):
         plan = engine.Stage2Plan(sess.dm, jobs, schedule=sched)
         if dt is not None:
             plan.sched.part_o = plan.sched.part_o.to(dt)
-            plan.part_o = plan.sched.part_o
+
         s, best = sess.run(jobs, plan)
         s = s.double().cpu().numpy()
         print(f"{name} {sched:5s} {str(dt):14s} max|d score| {np.abs(s - ref).max():.4f} mean {np.abs(s - ref).mean():.5f}")
