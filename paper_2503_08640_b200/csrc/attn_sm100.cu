@@ -44,6 +44,21 @@ namespace dbsa {
 
 constexpr int kBN = 128;  // keys per tile
 
+// Profiling build only (-DDBSA_STAMPS, tools/build_variant.py + tools/stamps.py):
+// per-tile clock stamps of CTA 0 for the first 256 key tiles of the two-tile
+// kernel, read back with dbsa_debug_stamps.
+#ifdef DBSA_STAMPS
+__device__ long long g_stamps[256 * 12];
+#define STAMP(slot, j)                                                         \
+  do {                                                                         \
+    if (blockIdx.x == 0 && (j) < 256) g_stamps[(j) * 12 + (slot)] = clock64(); \
+  } while (0)
+#else
+#define STAMP(slot, j) \
+  do {               \
+  } while (0)
+#endif
+
 template <int HDP, int NUM_M>
 struct AttnCfg {
   static constexpr int QSW = HDP >= 64 ? 128 : HDP * 2;  // swizzle width of Q / K rows (bytes)
@@ -546,6 +561,7 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
             if (j > 0) {
               // P(m, j-1) ready (and S(m) free): accumulate it, then reuse S(m) for tile j
               mbar_wait(&p_full[m], (t - 1) & 1);
+              if (lane == 0) STAMP(10 + m, t - 1);
               if (m == 0) mbar_wait(&v_full[(t - 1) % C::VST], ((t - 1) / C::VST) & 1);
               if (j == 1 && wk > 0) mbar_wait(&o_free[m], (wk - 1) & 1);  // previous work's O was read
               tc_fence_after();
@@ -643,8 +659,10 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
           // and their P only feeds their own (never stored) O rows
           const bool full = !valid || (c_lo == 0 && c_hi == kBN && (b_hi <= 0 || b_lo >= kBN || b_lo >= b_hi));
           const bool restage = tt == nt - 1 && si + 1 < w.seg_end && p.segs[si + 1].shift != cur_rot;
+          if (trow == 0) STAMP(m * 5 + 0, jg + j);
           mbar_wait(&s_full[m], (jg + j) & 1);
           tc_fence_after();
+          if (trow == 0) STAMP(m * 5 + 1, jg + j);
           if (warp_dead || (p.dbg & 1)) {  // no valid row: its P rows only feed its own (discarded) O rows
             if (restage) {
               cur_rot = p.segs[si + 1].shift;
@@ -658,6 +676,7 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
 #pragma unroll
           for (int c = 0; c < kBN; c += 32) tmem_ld32(t_s + c, *reinterpret_cast<float(*)[32]>(&x[c]));
           tmem_wait_ld();
+          if (trow == 0) STAMP(m * 5 + 2, jg + j);
           if (!__all_sync(0xffffffffu, full)) {
 #pragma unroll
             for (int c = 0; c < kBN; ++c) {
@@ -677,6 +696,7 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
           const float tmax =
               fmax3(fmax3(mx[0], mx[1], mx[2]), fmax3(mx[3], mx[4], mx[5]), fmaxf(mx[6], mx[7])) * sl2;
           const float m_new = fmaxf(m_used, tmax);
+          if (trow == 0) STAMP(m * 5 + 3, jg + j);
           // Lazy rescale (threshold 2^8).  S(m, j) being complete implies P.V(m, j-1)
           // retired (issued before QK(m, j) on the in-order tensor pipe), so O(m)
           // is quiescent here.  tcgen05.ld/st are warp-wide: the decision is warp-uniform.
@@ -721,6 +741,7 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
           tmem_wait_st();
           tc_fence_before();
           mbar_arrive(&p_full[m]);  // P.V(m, j) may start now
+          if (trow == 0) STAMP(m * 5 + 4, jg + j);
           if (restage) {  // QK(m, j) retired (S read); QK(m, j+1) waits for q_ready(m)
             cur_rot = p.segs[si + 1].shift;
             stage_q(w, true, cur_rot);
@@ -1246,6 +1267,14 @@ static int launch_attn(const DbsaAttnArgs &a, const AttnParams &p, const CUtenso
 }
 
 }  // namespace dbsa
+
+#ifdef DBSA_STAMPS
+extern "C" int dbsa_debug_stamps(long long *host, int n) {
+  return cudaMemcpyFromSymbol(host, dbsa::g_stamps, sizeof(long long) * (n < 256 * 12 ? n : 256 * 12)) == cudaSuccess
+             ? 0
+             : DBSA_ERR_CUDA;
+}
+#endif
 
 extern "C" int dbsa_attention(const DbsaAttnArgs *args, void *stream) {
   using namespace dbsa;
