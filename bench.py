@@ -246,8 +246,12 @@ def run_ours(args):
               "ms": s1_ms, "pool_tokens": N_GROUPS * GROUP_TOK, "attended_pairs": pairs, "mode": s1_mode,
               "roofline": {"kernel": "dbsa_attn_kernel (K1)", "bound": "tensor",
                            "achieved": k1_flops / (k1_ms / 1e3) / 1e12 if k1_ms else None,
-                           "peak": tf_burst, "unit": "TFLOP/s",
-                           "frac": (k1_flops / (k1_ms / 1e3) / 1e12) / tf_burst if k1_ms else None,
+                           # K1 is timed in situ, inside the long stage-1 step (32 layers of
+                           # GEMMs around it): the sustained bf16 figure is its denominator
+                           "peak": tf_sus, "peak_kind": "sustained (timed inside the stage-1 step)",
+                           "peak_burst": tf_burst, "unit": "TFLOP/s",
+                           "frac": (k1_flops / (k1_ms / 1e3) / 1e12) / tf_sus if k1_ms else None,
+                           "frac_of_burst": (k1_flops / (k1_ms / 1e3) / 1e12) / tf_burst if k1_ms else None,
                            "traffic": traffic_for("k1", "c2"), "launch_ms": k1_ms,
                            "flops_per_launch": k1_flops,
                            "share_of_step": (k1_ms * cfg.n_layers) / s1_times[-1] if k1_ms else None,
