@@ -47,7 +47,7 @@ __device__ __forceinline__ float load1(const void *base, int64_t off) {
     return reinterpret_cast<const float *>(base)[off];
 }
 
-template <bool BF16>
+template <bool BF16, bool LATENCY>
 __global__ void lse_merge_kernel(DbsaMergeArgs a) {
   const DbsaMergeGroup g = a.groups[blockIdx.y];
   const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -56,6 +56,43 @@ __global__ void lse_merge_kernel(DbsaMergeArgs a) {
   const int hd = a.head_dim, gs = a.n_heads / a.n_kv_heads;
   const int64_t sstride = a.split_stride > 0 ? a.split_stride : g.rows;
   const int64_t row0 = g.part_row0 + r;
+  constexpr int kFast = 24;
+  if (LATENCY && hd <= 128 && (hd & 3) == 0 && g.n_splits <= kFast) {
+    // latency path (few rows, e.g. one query): every split's partial row is
+    // loaded before the LSE reduction (the loads do not depend on it), so the
+    // row costs ~two memory round trips; large merges keep the lean path below
+    // (its lower register count keeps more rows in flight)
+    const int dl = lane * 4 + 3 < hd ? lane * 4 : 0;
+    float v[kFast][4];
+#pragma unroll
+    for (int s = 0; s < kFast; ++s)
+      if (s < g.n_splits) load4<BF16>(a.part_o, (row0 + (int64_t)s * sstride) * hd + dl, v[s]);
+    const float l = lane < g.n_splits ? a.part_lse[row0 + (int64_t)lane * sstride] : -INFINITY;
+    const float mx = warp_max(l);
+    const float e = l == -INFINITY ? 0.f : __expf(l - mx);
+    const float tot = warp_sum(e);
+    const float wl = tot > 0.f ? e / tot : 0.f;
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int s = 0; s < kFast; ++s) {
+      const float ws = __shfl_sync(0xffffffffu, wl, s);
+      if (s < g.n_splits) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[i] += ws * v[s][i];
+      }
+    }
+    if (lane * 4 + 3 < hd) {
+      const int t = g.q_tok0 + r / gs, head = g.kv_head * gs + r % gs;
+      __nv_bfloat16 *dst =
+          reinterpret_cast<__nv_bfloat16 *>(a.out) + (int64_t)t * a.out_tok_stride + (int64_t)head * hd + lane * 4;
+      __nv_bfloat162 lo = __floats2bfloat162_rn(acc[0], acc[1]), hi = __floats2bfloat162_rn(acc[2], acc[3]);
+      uint2 u;
+      u.x = *reinterpret_cast<uint32_t *>(&lo);
+      u.y = *reinterpret_cast<uint32_t *>(&hi);
+      *reinterpret_cast<uint2 *>(dst) = u;
+    }
+    return;
+  }
   // one read of each split's LSE: lane s holds split s (a second pass only past 32 splits)
   const float l_own = lane < g.n_splits ? a.part_lse[row0 + (int64_t)lane * sstride] : -INFINITY;
   float mx = l_own;
@@ -294,10 +331,19 @@ extern "C" int dbsa_lse_merge(const DbsaMergeArgs *args, void *stream) {
   const DbsaMergeArgs &a = *args;
   if (a.n_groups <= 0 || a.max_rows <= 0) return DBSA_OK;
   dim3 grid((a.max_rows + 3) / 4, a.n_groups);
-  if (a.part_bf16)
-    lse_merge_kernel<true><<<grid, 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(a);
-  else
-    lse_merge_kernel<false><<<grid, 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(a);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const bool small = (int64_t)a.n_groups * a.max_rows <= 16384;
+  if (a.part_bf16) {
+    if (small)
+      lse_merge_kernel<true, true><<<grid, 128, 0, st>>>(a);
+    else
+      lse_merge_kernel<true, false><<<grid, 128, 0, st>>>(a);
+  } else {
+    if (small)
+      lse_merge_kernel<false, true><<<grid, 128, 0, st>>>(a);
+    else
+      lse_merge_kernel<false, false><<<grid, 128, 0, st>>>(a);
+  }
   return check_launch("lse_merge");
 }
 
