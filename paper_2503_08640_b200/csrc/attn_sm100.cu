@@ -49,6 +49,11 @@ constexpr int kBN = 128;  // keys per tile
 // kernel, read back with dbsa_debug_stamps.
 #ifdef DBSA_STAMPS
 __device__ long long g_stamps[256 * 12];
+__device__ long long g_wstamps[256 * 12];  // per work of CTA 0: m*4 + {softmax done, Q staged, O full, epilogue done}
+#define WSTAMP(slot, w)                                                       \
+  do {                                                                        \
+    if (blockIdx.x == 0 && (w) < 256) g_wstamps[(w) * 12 + (slot)] = clock64(); \
+  } while (0)
 #define STAMP(slot, j)                                                         \
   do {                                                                         \
     if (blockIdx.x == 0 && (j) < 256) g_stamps[(j) * 12 + (slot)] = clock64(); \
@@ -56,6 +61,9 @@ __device__ long long g_stamps[256 * 12];
 #else
 #define STAMP(slot, j) \
   do {               \
+  } while (0)
+#define WSTAMP(slot, w) \
+  do {                \
   } while (0)
 #endif
 
@@ -678,10 +686,15 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
           tmem_wait_ld();
           if (trow == 0) STAMP(m * 5 + 2, jg + j);
           if (!__all_sync(0xffffffffu, full)) {
+            if (is_self) {
 #pragma unroll
-            for (int c = 0; c < kBN; ++c) {
-              const bool ok = (c >= c_lo) & (c < c_hi) & ((c < b_lo) | (c >= b_hi));
-              x[c] = ok ? x[c] : -INFINITY;
+              for (int c = 0; c < kBN; ++c) {
+                const bool ok = (c >= c_lo) & (c < c_hi) & ((c < b_lo) | (c >= b_hi));
+                x[c] = ok ? x[c] : -INFINITY;
+              }
+            } else {  // a context chunk's first / last tile: one column range
+#pragma unroll
+              for (int c = 0; c < kBN; ++c) x[c] = (c >= c_lo) & (c < c_hi) ? x[c] : -INFINITY;
             }
           }
           float mx[8];
@@ -757,19 +770,23 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
       // work's q_full phase: wait for its o_full first, or the next arrival
       // could complete a second q_full phase before the first was observed.
       if (j == 0) mbar_wait(&o_full[m], wk & 1);
+      if (trow == 0) WSTAMP(m * 4 + 0, wk);
       const int wn = wi + gridDim.x;
       if (wn < n_works) {
         stage_q(p.works[wn], false, 0);
         fence_proxy_async_smem();
         mbar_arrive(&q_full[m]);
       }
+      if (trow == 0) WSTAMP(m * 4 + 1, wk);
 
       // ---------------------------------------------------------- epilogue
       mbar_wait(&o_full[m], wk & 1);
       tc_fence_after();
+      if (trow == 0) WSTAMP(m * 4 + 2, wk);
       epilogue_row<HDP>(p, t_o, valid, t, head, w.out_mode, xr.part_row, l_sum, m_used);
       tc_fence_before();
       mbar_arrive(&o_free[m]);  // O(m) may be overwritten by the next work's first P.V
+      if (trow == 0) WSTAMP(m * 4 + 3, wk);
     }
   }
 
@@ -1271,6 +1288,11 @@ static int launch_attn(const DbsaAttnArgs &a, const AttnParams &p, const CUtenso
 #ifdef DBSA_STAMPS
 extern "C" int dbsa_debug_stamps(long long *host, int n) {
   return cudaMemcpyFromSymbol(host, dbsa::g_stamps, sizeof(long long) * (n < 256 * 12 ? n : 256 * 12)) == cudaSuccess
+             ? 0
+             : DBSA_ERR_CUDA;
+}
+extern "C" int dbsa_debug_wstamps(long long *host, int n) {
+  return cudaMemcpyFromSymbol(host, dbsa::g_wstamps, sizeof(long long) * (n < 256 * 12 ? n : 256 * 12)) == cudaSuccess
              ? 0
              : DBSA_ERR_CUDA;
 }

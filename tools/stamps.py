@@ -23,3 +23,18 @@ for m in (0, 1):
 print("MMA sees P(m0) after arrive:", d(4, 10), "  P(m1):", d(9, 11))
 print("m0 arrive -> m0 next S ready:", np.median(a[1:, 1] - a[:-1, 4]))
 print("period (m0 S ready -> next):", np.median(np.diff(a[:, 1])))
+if os.environ.get("RAW"):
+    b = np.array(buf, dtype=np.int64).reshape(256, 12)
+    t0 = b[0, 0]
+    for j in range(int(os.environ["RAW"])):
+        print(j, " ".join(f"{(x - t0) if x else -1:7d}" for x in b[j]))
+wb = (ctypes.c_longlong * (256 * 12))()
+if hasattr(lib, "dbsa_debug_wstamps") and lib.dbsa_debug_wstamps(wb, 256 * 12) == 0:
+    w = np.array(wb, dtype=np.int64).reshape(256, 12)
+    w = w[(w[:, 0] > 0) & (w[:, 3] > 0)]
+    if len(w) > 4:
+        w = w[2:-1]
+        for m in (0, 1):
+            b = m * 4
+            print(f"work boundary m{m}: stage next Q {np.median(w[:, b+1]-w[:, b]):7.0f}  wait O {np.median(w[:, b+2]-w[:, b+1]):7.0f}"
+                  f"  epilogue {np.median(w[:, b+3]-w[:, b+2]):7.0f}  work period {np.median(np.diff(w[:, b])):7.0f}  (works {len(w)})")
