@@ -271,9 +271,8 @@ def run_ours(args):
 
     # the step's forward + scoring replays one captured CUDA graph (engine.GraphedStage2);
     # each step copies its own work / token tables into the graph's buffers first
-    cap = (max(getattr(st[4].sched, "n_real_works", 0) for st in steps),
-           max(getattr(st[4].sched, "n_real_segs", 0) for st in steps))
-    graph = engine.GraphedStage2(dm, cache.store, steps[0][3], steps[0][4], len(sess.label_ids), capacity=cap)
+    graph = engine.GraphedStage2(dm, cache.store, steps[0][3], steps[0][4], len(sess.label_ids),
+                                 capacity=sess._capacity(steps[0][3]))
     scorers = [engine.LabelScorer(dm, st[4], st[3], len(sess.label_ids)) for st in steps]
 
     def device_step(st, i):
@@ -399,9 +398,32 @@ def run_ours(args):
             return a_.elapsed_time(b_) / reps
 
         t_sel, t_dense = time_k3(plan0c), time_k3(plan_d)
+
+        # the north-star form: the whole stage-2 step (graph replay, all layers,
+        # label scoring) of the same queries over the selected chunks vs over one
+        # dense contiguous run of the same T' pool rows
+        def time_step(jobs_x, plan_x, reps=5):
+            g = engine.GraphedStage2(dm, cache.store, jobs_x, plan_x, len(sess.label_ids))
+            sc_x = engine.LabelScorer(dm, plan_x, jobs_x, len(sess.label_ids))
+            g.replay(plan_x, sc_x)
+            torch.cuda.synchronize()
+            a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_.record()
+            for _ in range(reps):
+                g.replay(plan_x, sc_x)
+            b_.record()
+            torch.cuda.synchronize()
+            return a_.elapsed_time(b_) / reps / len(jobs_x)
+
+        jobs_s, plan_s = sess.plan(sess.select(st0[1]), st0[0])
+        plan_dd = engine.Stage2Plan(dm, dense_jobs)
+        s_sel, s_dense = time_step(jobs_s, plan_s), time_step(dense_jobs, plan_dd)
         extra["dense_comparator"] = {"k3_selected_chunks_ms": t_sel, "k3_dense_contiguous_ms": t_dense,
                                      "ratio": t_sel / t_dense,
-                                     "note": f"same {B} queries, T'={Tp}: {sess.budget} chunks vs one contiguous run"}
+                                     "step_selected_ms_per_query": s_sel, "step_dense_ms_per_query": s_dense,
+                                     "step_ratio": s_sel / s_dense,
+                                     "note": f"same {B} queries, T'={Tp}: {sess.budget} chunks vs one contiguous run; "
+                                             "ratio = K3 per launch, step_ratio = the whole stage-2 step per query"}
 
     # roofline of K3 (dominant stage-2 kernel): algorithmic bytes per launch =
     # selected KV (2 * Hkv * hd * 2 B per token, one layer) + Q in + O out.

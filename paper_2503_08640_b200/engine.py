@@ -1063,8 +1063,11 @@ class GraphedStage2:
             # the chunk-major table sizes vary with how a batch's selections
             # overlap: capture at a padded capacity, replay any batch that fits
             sc = plan.sched
-            nw, ns = max(sc.n_real_works, (capacity or (0, 0))[0]), max(sc.n_real_segs, (capacity or (0, 0))[1])
-            sc.pad_to(-(-(nw * 17 // 16 + 64) // 64) * 64, -(-(ns * 17 // 16 + 16) // 16) * 16)
+            if capacity is None:  # headroom for batches whose selections overlap less
+                nw, ns = sc.n_real_works * 17 // 16 + 64, sc.n_real_segs * 17 // 16 + 16
+            else:
+                nw, ns = max(sc.n_real_works, capacity[0]), max(sc.n_real_segs, capacity[1])
+            sc.pad_to(-(-nw // 64) * 64, -(-ns // 16) * 16)
             plan.works, plan.n_works, plan.segs, plan.n_segs = sc.works, sc.n_works, sc.segs, sc.n_segs
         self._run()  # warm-up: workspace allocation, cuBLAS handles, kernel attributes
         torch.cuda.current_stream(dm.device).synchronize()

@@ -273,6 +273,21 @@ class Stage2Session:
         scorer = engine.LabelScorer(self.dm, plan, jobs, len(self.label_ids))
         return scorer(self.dm, h)
 
+    def _capacity(self, jobs):
+        """Upper bound of a chunk-major batch's (works, segments) for this
+        session's unit count, so one captured graph serves every batch of the
+        shape (engine.chunk_major_tables: a chunk shared by E rows is cut into
+        ceil(E / slab) <= E / slab + 1 works per kv head)."""
+        c = self.dm.config
+        slab = 256 // c.group_size
+        n_new = np.array([len(j.ids) for j in jobs])
+        n_ch = np.array([len(np.asarray(j.chunks).reshape(-1, 3)) for j in jobs])
+        keys = min(self.n_units, int(n_ch.sum()))
+        e_total = int((n_new * n_ch).sum())
+        self_works = int((-(-n_new // slab)).sum())
+        works = c.n_kv_heads * (-(-e_total // slab) + keys + self_works)
+        return works, keys + self_works
+
     def answer(self, scores, query_ids_list, graphed: bool = True):
         """K4 selection, planning and the scored forward of one batch.  With
         `graphed`, batches of a shape seen before replay a captured CUDA graph
@@ -286,7 +301,8 @@ class Stage2Session:
         key = engine.plan_key(plan, scorer)
         graphs = self.__dict__.setdefault("_graphs", {})
         if key not in graphs or not engine.fits_graph(graphs[key], plan):
-            graphs[key] = engine.GraphedStage2(self.dm, self.cache.store, jobs, plan, len(self.label_ids))
+            graphs[key] = engine.GraphedStage2(self.dm, self.cache.store, jobs, plan, len(self.label_ids),
+                                               capacity=self._capacity(jobs))
         s, best = graphs[key].replay(plan, scorer)
         return ids, s, best
 
@@ -316,7 +332,8 @@ class Stage2Session:
             graphs = self.__dict__.setdefault("_graphs", {})
             if key not in graphs or not engine.fits_graph(graphs[key], plan):
                 main.synchronize()
-                graphs[key] = engine.GraphedStage2(self.dm, self.cache.store, jobs, plan, len(self.label_ids))
+                graphs[key] = engine.GraphedStage2(self.dm, self.cache.store, jobs, plan, len(self.label_ids),
+                                                   capacity=self._capacity(jobs))
             s_dev, best_dev = graphs[key].replay(plan, scorer)
             s_host = torch.empty(s_dev.shape, dtype=s_dev.dtype, pin_memory=True)
             b_host = torch.empty(best_dev.shape, dtype=best_dev.dtype, pin_memory=True)
