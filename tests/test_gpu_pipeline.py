@@ -112,10 +112,13 @@ def test_stage2_runner_matches_reference(name):
         assert margin < 10 * max(err, 1e-3), f"query {qi} flipped with margin {margin} (err {err})"
 
 
+@pytest.mark.parametrize("schedule", ["query", "chunk"])
 @pytest.mark.parametrize("name", CASES)
-def test_stage2_batched_k4_path_matches_reference(name):
+def test_stage2_batched_k4_path_matches_reference(name, schedule, monkeypatch):
     """Runner.infer_batch: K4 selection on the device + one tree-masked
-    forward for the whole batch; unit ids bit-exact, labels identical."""
+    forward for the whole batch (split-KV per query and chunk-major K3);
+    unit ids bit-exact, labels identical."""
+    monkeypatch.setenv("DBSA_STAGE2_SCHEDULE", schedule)
     meta, a, w, task, mc, enc = _encoded(name)
     runner = P.Runner(w, enc.cache, enc.index, task, mc)
     texts = [q["query"] for q in meta["queries"]]
@@ -278,11 +281,14 @@ def test_stage1_patterns_vs_oracle(kind, j):
     assert worst < KV_TOL, worst
 
 
+@pytest.mark.parametrize("schedule", ["query", "chunk"])
 @pytest.mark.parametrize("ordering", ["in-order", "low-to-high", "reverse"])
 @pytest.mark.parametrize("ratio", [0.01, 1.0])
-def test_stage2_orderings_and_extreme_ratios(ordering, ratio):
+def test_stage2_orderings_and_extreme_ratios(ordering, ratio, schedule, monkeypatch):
     """Anchor-only (ratio -> budget 1: few-shot ICL) and the whole pool, every
-    ordering: K4 ids bit-exact with select + order, labels equal the oracle's."""
+    ordering, through both K3 schedules (split-KV per query and chunk-major):
+    K4 ids bit-exact with select + order, labels equal the oracle's."""
+    monkeypatch.setenv("DBSA_STAGE2_SCHEDULE", schedule)
     meta, a, w, task, mc0, enc = _encoded("c1")
     mc = P.MethodConfig(block_size=16, ratio=ratio, seed=0, ordering=ordering)
     runner = P.Runner(w, enc.cache, enc.index, task, mc)
