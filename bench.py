@@ -254,7 +254,7 @@ def run_ours(args):
                            "frac_of_burst": (k1_flops / (k1_ms / 1e3) / 1e12) / tf_burst if k1_ms else None,
                            "traffic": traffic_for("k1", "c2"), "launch_ms": k1_ms,
                            "flops_per_launch": k1_flops,
-                           "share_of_step": (k1_ms * cfg.n_layers) / s1_times[-1] if k1_ms else None,
+                           "share_of_step": (k1_ms * (cfg.n_layers - 1)) / s1_times[-1] if k1_ms else None,  # the last layer stops after its page write
                            "peak_source": peak_src}}
 
     # ---------------- stage 2 (C3 at 30 %)

@@ -284,11 +284,14 @@ class _Scratch:
         self.act = torch.empty((min(n_tok, self.ffn_chunk), c.ffn_dim), dtype=torch.bfloat16, device=dev)
 
 
-def _decoder_gen(dm, ids_dev, attend, write_kv, n_layers=None):
+def _decoder_gen(dm, ids_dev, attend, write_kv, n_layers=None, kv_only_last=False):
     """Pre-norm decoder body (model.py:319-359) over n new tokens, as a
     generator: it yields after each layer's `write_kv(l, qkv)` (the point where
     a multi-shard caller exchanges pages) and returns the fp32 final hidden
-    states.  `attend(l, qkv, out)` fills the attention output."""
+    states.  `attend(l, qkv, out)` fills the attention output.  kv_only_last:
+    the caller only keeps K/V (a pool encode): the last layer stops after its
+    page write -- its attention, O projection and FFN feed nothing -- and the
+    return value is None."""
     torch = _torch()
     c = dm.config
     n = ids_dev.shape[0]
@@ -304,6 +307,8 @@ def _decoder_gen(dm, ids_dev, attend, write_kv, n_layers=None):
         torch.mm(s.x, lw["wqkv"], out=s.qkv)
         write_kv(layer, s.qkv)
         yield layer
+        if kv_only_last and layer == L - 1:
+            return None
         attend(layer, s.qkv, s.att)
         mm_f32(s.att, lw["wo"], s.proj)
         ops.add_rmsnorm(h, s.proj, lw["ffn_norm"], c.norm_eps, s.x)
@@ -414,7 +419,8 @@ def encode_groups_gen(dm, cache, new, ids, pattern, layers=None):
                       works_dev=plan.works, n_works=plan.n_works, segs_dev=plan.segs_ptr(layer), num_m=plan.num_m,
                       out=out, out_tok_stride=qw)
 
-    yield from _decoder_gen(dm, ids_dev, attend, write_kv, n_layers=layers)
+    # only the pages are kept: the last layer's attention / O / FFN are skipped
+    yield from _decoder_gen(dm, ids_dev, attend, write_kv, n_layers=layers, kv_only_last=True)
     return plan.pairs
 
 
