@@ -402,3 +402,39 @@ def test_stage2_batch_schedules_vs_float64(schedule, hd, H, Hkv):
                 want = (e / e.sum(axis=1, keepdims=True)) @ v
                 worst = max(worst, float(np.abs(got[t0:t0 + n, head] - want).max()))
     assert worst < 2e-2, worst
+
+
+@pytest.mark.parametrize("n_splits", [1, 7, 19, 40])
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+def test_lse_merge_large_vs_torch(n_splits, dtype):
+    """K3m on a merge large enough for the throughput kernels (the chunk-major
+    batch shape: many groups of 176 rows, bf16 or fp32 partials, some splits
+    empty): the single softmax over the concatenated key set (kernels.py:52-56)
+    recomputed in float64 from the same partials."""
+    dev = torch.device("cuda", 0)
+    H, Hkv, hd = 32, 8, 128
+    gs = H // Hkv
+    n_q, n_tok = 24, 44
+    rows = n_tok * gs
+    g = torch.Generator(device=dev).manual_seed(n_splits)
+    part_dtype = torch.bfloat16 if dtype == "bf16" else torch.float32
+    n_groups = n_q * Hkv
+    part_o = torch.randn(n_groups * n_splits * rows, hd, generator=g, device=dev).to(part_dtype)
+    part_lse = torch.randn(n_groups * n_splits * rows, generator=g, device=dev) * 3
+    part_lse[torch.rand(part_lse.shape, generator=g, device=dev) < 0.05] = -float("inf")  # empty splits
+    groups = np.zeros(n_groups, dtype=ops.MERGE_DTYPE)
+    for q in range(n_q):
+        for kv in range(Hkv):
+            i = q * Hkv + kv
+            groups[i] = (i * n_splits * rows, rows, n_splits, q * n_tok, kv)
+    out = torch.zeros(n_q * n_tok, H * hd, dtype=torch.bfloat16, device=dev)
+    ops.lse_merge(part_o, part_lse, ops.to_device(groups, dev), n_groups, rows, H, Hkv, hd, out, H * hd)
+    torch.cuda.synchronize()
+    po = part_o.double().view(n_groups, n_splits, rows, hd)
+    pl = part_lse.double().view(n_groups, n_splits, rows)
+    lse = torch.logsumexp(pl, dim=1, keepdim=True)
+    w = torch.nan_to_num(torch.exp(pl - lse), nan=0.0)
+    want = (w.unsqueeze(-1) * po).sum(1)  # [n_groups, rows, hd]
+    want = want.view(n_q, Hkv, n_tok, gs, hd).permute(0, 2, 1, 3, 4).reshape(n_q * n_tok, H * hd)
+    err = float((out.double() - want).abs().max())
+    assert err < 2e-2, err
