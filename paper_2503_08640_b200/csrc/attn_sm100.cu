@@ -404,7 +404,8 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
   uint64_t *o_full = p_full + NUM_M;          // [NUM_M]  O(m) of a work complete
   uint64_t *q_ready = o_full + NUM_M;         // [NUM_M]  Q(m) re-staged for a new RoPE shift
   uint64_t *o_free = q_ready + NUM_M;         // [NUM_M]  O(m) read by the epilogue (TMEM reusable)
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(o_free + NUM_M);
+  uint64_t *p_half = o_free + NUM_M;          // [NUM_M]  first 64 keys of P(m, j) in TMEM
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(p_half + NUM_M);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_works = p.n_works;
@@ -425,6 +426,7 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
       mbar_init(&o_full[m], 1);
       mbar_init(&q_ready[m], 128);
       mbar_init(&o_free[m], 128);
+      mbar_init(&p_half[m], 128);
     }
     fence_mbar_init();
     tma_prefetch(&tm_k0);
@@ -516,13 +518,16 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
       }
       __syncwarp();
     };
-    auto pv = [&](int m, int jg, bool first) {  // O(m) (+)= P(m, jg) V(jg), P from TMEM
+    // O(m) (+)= P(m, jg) V(jg) over keys 64 hf .. 64 hf + 63, P from TMEM: the
+    // first half is issued as soon as the softmax has written it (p_half), so
+    // it runs on the tensor pipe while the softmax computes the second half
+    auto pv = [&](int m, int jg, bool first, int hf) {
       const int st = jg % C::VST;
       const uint32_t d = tbase + m * HDP;
       const uint32_t pa = tbase + NUM_M * HDP + m * kBN;
       if (leader) {
 #pragma unroll
-        for (int kk = 0; kk < kBN / 16; ++kk) {
+        for (int kk = hf * kBN / 32; kk < (hf + 1) * kBN / 32; ++kk) {
           const int a = kk / 4;
           const int off = (kk % 4) * 32;
           const uint64_t bd = umma_desc_kmajor(sVa + st * C::V_BYTES + a * HDP * 128 + off, 128);
@@ -568,12 +573,15 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
           for (int m = 0; m < NUM_M; ++m) {
             if (j > 0) {
               // P(m, j-1) ready (and S(m) free): accumulate it, then reuse S(m) for tile j
-              mbar_wait(&p_full[m], (t - 1) & 1);
-              if (lane == 0) STAMP(10 + m, t - 1);
+              mbar_wait(&p_half[m], (t - 1) & 1);
               if (m == 0) mbar_wait(&v_full[(t - 1) % C::VST], ((t - 1) / C::VST) & 1);
               if (j == 1 && wk > 0) mbar_wait(&o_free[m], (wk - 1) & 1);  // previous work's O was read
               tc_fence_after();
-              pv(m, t - 1, j == 1);
+              pv(m, t - 1, j == 1, 0);
+              mbar_wait(&p_full[m], (t - 1) & 1);
+              if (lane == 0) STAMP(10 + m, t - 1);
+              tc_fence_after();
+              pv(m, t - 1, false, 1);
               if (m == NUM_M - 1) commit(&v_empty[(t - 1) % C::VST]);
             }
             if (boundary) {
@@ -587,11 +595,14 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
         }
         const int t = jg + n_tiles - 1;
         for (int m = 0; m < NUM_M; ++m) {
-          mbar_wait(&p_full[m], t & 1);
+          mbar_wait(&p_half[m], t & 1);
           if (m == 0) mbar_wait(&v_full[t % C::VST], (t / C::VST) & 1);
           if (n_tiles == 1 && wk > 0) mbar_wait(&o_free[m], (wk - 1) & 1);
           tc_fence_after();
-          pv(m, t, n_tiles == 1);
+          pv(m, t, n_tiles == 1, 0);
+          mbar_wait(&p_full[m], t & 1);
+          tc_fence_after();
+          pv(m, t, false, 1);
           commit(&o_full[m]);
         }
         commit(&v_empty[t % C::VST]);
@@ -677,6 +688,7 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
               mbar_arrive(&q_ready[m]);  // nothing to re-stage for invalid rows
             }
             tc_fence_before();
+            mbar_arrive(&p_half[m]);
             mbar_arrive(&p_full[m]);
             continue;
           }
@@ -748,6 +760,11 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
               pk[c >> 1] = pack_bf16(e.x, e.y);
             }
             tmem_st32(t_s + h * 32, pk);  // P(j): keys 64h..64h+63 over S columns 32h..32h+31
+            if (h == 0) {
+              tmem_wait_st();
+              tc_fence_before();
+              mbar_arrive(&p_half[m]);  // P.V(m, j) over keys 0..63 may start
+            }
           }
           const float2 pss = fadd2(ps[0], ps[1]);
           l_sum += pss.x + pss.y;
