@@ -241,6 +241,11 @@ int dbsa_silu_mul(const void *gate_up, void *out, int64_t rows, int64_t ffn, voi
  * logprob[r] = logits[r, target[r]] - logsumexp(logits[r, :]) in fp32. */
 int dbsa_label_logprob(const float *logits, int64_t rows, int64_t vocab, const int32_t *target,
                        float *out, void *stream);
+/* Label scores and choice (model.py:441-443, pipeline.py:376-382): output o =
+ * q * n_labels + l sums the log-probs of rows label_row0[o] .. label_row0[o+1]
+ * in order; best[q] is the first label with the maximum score. */
+int dbsa_label_reduce(const float *lp, const int32_t *label_row0, int64_t n_queries, int32_t n_labels,
+                      float *scores, int64_t *best, void *stream);
 
 int dbsa_abi_version(void);
 const char *dbsa_last_error(void);

@@ -30,6 +30,7 @@ EXPORTED_SYMBOLS = (
     "dbsa_add_rmsnorm",
     "dbsa_silu_mul",
     "dbsa_label_logprob",
+    "dbsa_label_reduce",
     "dbsa_bm25_scores",
     "dbsa_abi_version",
     "dbsa_last_error",
@@ -151,6 +152,7 @@ def load_library(path: Path | str | None = None) -> ctypes.CDLL:
         lib.dbsa_add_rmsnorm.argtypes = [_vp, _vp, _vp, _vp, _i64, _i64, _f32, _vp]
         lib.dbsa_silu_mul.argtypes = [_vp, _vp, _i64, _i64, _vp]
         lib.dbsa_label_logprob.argtypes = [_vp, _i64, _i64, _vp, _vp, _vp]
+        lib.dbsa_label_reduce.argtypes = [_vp, _vp, _i64, _i32, _vp, _vp, _vp]
         lib.dbsa_bm25_scores.argtypes = [_vp, _i64, _i32, _vp, _vp, _vp, _i64, ctypes.c_double, _vp, _vp]
         for name in EXPORTED_SYMBOLS[:-2]:
             getattr(lib, name).restype = ctypes.c_int

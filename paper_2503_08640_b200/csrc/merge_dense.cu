@@ -361,33 +361,94 @@ __global__ void silu_mul8_kernel(const uint4 *gu, uint4 *out, int64_t rows, int6
 }
 
 // logprob[r] = logits[r, target[r]] - logsumexp(logits[r, :]) (model.log_softmax_rows, model.py:414-417).
+// One pass over the row: each thread keeps an online (max, sum) over float4
+// reads, merged across the block.
+__device__ __forceinline__ void lse_combine(float &m, float &s, float m2, float s2) {
+  const float mn = fmaxf(m, m2);
+  s = (m == -INFINITY ? 0.f : s * __expf(m - mn)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - mn));
+  m = mn;
+}
 __global__ void label_logprob_kernel(const float *logits, int64_t vocab, const int32_t *target, float *out) {
   const int64_t row = blockIdx.x;
   const float *lr = logits + row * vocab;
-  __shared__ float red[32];
-  float mx = -INFINITY;
-  for (int64_t i = threadIdx.x; i < vocab; i += blockDim.x) mx = fmaxf(mx, lr[i]);
-  mx = warp_max(mx);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : -INFINITY;
-    v = warp_max(v);
-    if (threadIdx.x == 0) red[0] = v;
+  float m = -INFINITY, sum = 0.f;
+  auto add = [&](float v) {
+    if (v > m) {
+      sum = (m == -INFINITY ? 0.f : sum * __expf(m - v)) + 1.f;
+      m = v;
+    } else {
+      sum += __expf(v - m);
+    }
+  };
+  if ((vocab & 3) == 0 && (reinterpret_cast<uintptr_t>(lr) & 15) == 0) {
+    const float4 *l4 = reinterpret_cast<const float4 *>(lr);
+    for (int64_t i = threadIdx.x; i < vocab / 4; i += blockDim.x) {
+      const float4 v = l4[i];
+      const float vm = fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w));
+      if (vm > m) {
+        sum = m == -INFINITY ? 0.f : sum * __expf(m - vm);
+        m = vm;
+      }
+      sum += __expf(v.x - m) + __expf(v.y - m) + __expf(v.z - m) + __expf(v.w - m);
+    }
+  } else {
+    for (int64_t i = threadIdx.x; i < vocab; i += blockDim.x) add(lr[i]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, sum, o);
+    lse_combine(m, sum, m2, s2);
+  }
+  __shared__ float sm[32], ss[32];
+  if ((threadIdx.x & 31) == 0) {
+    sm[threadIdx.x >> 5] = m;
+    ss[threadIdx.x >> 5] = sum;
   }
   __syncthreads();
-  mx = red[0];
-  __syncthreads();
-  float s = 0.f;
-  for (int64_t i = threadIdx.x; i < vocab; i += blockDim.x) s += __expf(lr[i] - mx);
-  s = warp_sum(s);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
-  __syncthreads();
   if (threadIdx.x < 32) {
-    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
-    v = warp_sum(v);
-    if (threadIdx.x == 0) out[row] = lr[target[row]] - mx - logf(v);
+    const bool ok = threadIdx.x < (blockDim.x >> 5);
+    m = ok ? sm[threadIdx.x] : -INFINITY;
+    sum = ok ? ss[threadIdx.x] : 0.f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, sum, o);
+      lse_combine(m, sum, m2, s2);
+    }
+    if (threadIdx.x == 0) out[row] = lr[target[row]] - m - logf(sum);
   }
+}
+
+// Per query (one warp): label score = sum of its tokens' log-probs (rows
+// label_row0[o] .. label_row0[o+1] of output o = q * n_labels + l, summed in
+// order), then the strict-> argmax over the labels (the first maximum wins:
+// pipeline.py:376-382 over the sorted labels).
+__global__ void label_reduce_kernel(const float *lp, const int32_t *label_row0, int64_t n_queries, int n_labels,
+                                    float *scores, int64_t *best) {
+  const int64_t q = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (q >= n_queries) return;
+  float sc = -INFINITY;
+  int idx = 0x7fffffff;
+  for (int l = lane; l < n_labels; l += 32) {
+    const int64_t o = q * n_labels + l;
+    float acc = 0.f;
+    for (int r = label_row0[o]; r < label_row0[o + 1]; ++r) acc += lp[r];
+    scores[o] = acc;
+    if (acc > sc) {
+      sc = acc;
+      idx = l;
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const float s2 = __shfl_xor_sync(0xffffffffu, sc, off);
+    const int i2 = __shfl_xor_sync(0xffffffffu, idx, off);
+    if (s2 > sc || (s2 == sc && i2 < idx)) {
+      sc = s2;
+      idx = i2;
+    }
+  }
+  if (lane == 0) best[q] = idx == 0x7fffffff ? 0 : idx;
 }
 
 }  // namespace dbsa
@@ -454,4 +515,15 @@ extern "C" int dbsa_label_logprob(const float *logits, int64_t rows, int64_t voc
   if (rows <= 0) return DBSA_OK;
   label_logprob_kernel<<<(unsigned)rows, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(logits, vocab, target, out);
   return check_launch("label_logprob");
+}
+
+extern "C" int dbsa_label_reduce(const float *lp, const int32_t *label_row0, int64_t n_queries, int32_t n_labels,
+                                 float *scores, int64_t *best, void *stream) {
+  using namespace dbsa;
+  if (n_queries <= 0) return DBSA_OK;
+  if (n_labels <= 0) return set_error(DBSA_ERR_VALIDATION, "n_labels must be positive");
+  const int per_block = 4;  // warps (queries) per block
+  label_reduce_kernel<<<(unsigned)((n_queries + per_block - 1) / per_block), 32 * per_block, 0,
+                        reinterpret_cast<cudaStream_t>(stream)>>>(lp, label_row0, n_queries, n_labels, scores, best);
+  return check_launch("label_reduce");
 }

@@ -1095,7 +1095,7 @@ class GraphedStage2:
         if n is not t:
             pairs = [(t.new.pos, n.new.pos), (t.new.lo, n.new.lo), (t.new.ids, n.new.ids), (t.new.pages, n.new.pages),
                      (self.scorer.rows, scorer.rows), (self.scorer.targets, scorer.targets),
-                     (self.scorer.owner, scorer.owner)]
+                     (self.scorer.owner, scorer.owner), (self.scorer.label_row0, scorer.label_row0)]
             if isinstance(t.sched, ChunkMajorSchedule):
                 t.sched.copy_tables_from(n.sched)
             else:
@@ -1163,16 +1163,16 @@ class LabelScorer:
         self.rows = ops.h2d(np.asarray(rows, np.int64), dev)
         self.targets = ops.h2d(np.asarray(targets, np.int32), dev)
         self.owner = ops.h2d(np.asarray(owner, np.int64), dev)
+        # rows of output o are contiguous (appended label by label): their bounds
+        counts = np.bincount(np.asarray(owner, np.int64), minlength=len(jobs) * n_labels)
+        self.label_row0 = ops.h2d(np.concatenate([[0], np.cumsum(counts)]).astype(np.int32), dev)
         self.n_out = len(jobs) * n_labels
         self.n_labels = n_labels
 
     def __call__(self, dm, h):
-        torch = _torch()
         logits = _final_logits(dm, h.index_select(0, self.rows))
         lp = ops.label_logprob(logits, self.targets)
-        scores = torch.zeros(self.n_out, dtype=torch.float32, device=h.device).index_add_(0, self.owner, lp)
-        scores = scores.view(-1, self.n_labels)
-        return scores, torch.argmax(scores, dim=1)
+        return ops.label_reduce(lp, self.label_row0, self.n_out // self.n_labels, self.n_labels)
 
 
 def score_labels(dm, assembled, query_ids, labels):

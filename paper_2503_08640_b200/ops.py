@@ -204,6 +204,18 @@ def label_logprob(logits, targets):
     return out
 
 
+def label_reduce(lp, label_row0, n_queries: int, n_labels: int):
+    """Per-label sums of token log-probs and the first-max label per query."""
+    import torch
+
+    scores = torch.empty((n_queries, n_labels), dtype=torch.float32, device=lp.device)
+    best = torch.empty(n_queries, dtype=torch.int64, device=lp.device)
+    nat.check(nat.load_library().dbsa_label_reduce(lp.data_ptr(), label_row0.data_ptr(), n_queries, n_labels,
+                                                    scores.data_ptr(), best.data_ptr(), nat.stream_handle()))
+    _launched()
+    return scores, best
+
+
 def bm25_scores(term_ids, tf, idf, norm, k1p1: float):
     """term_ids int32 [Q, T] (-1 pad), tf uint16 [V, U], idf f64 [V], norm f64 [U] -> f64 [Q, U]."""
     import torch
