@@ -265,6 +265,18 @@ __device__ __forceinline__ void epilogue_row(const AttnParams &p, uint32_t t_o, 
   const int hd = p.head_dim;
   if (out_mode == DBSA_OUT_BF16) {
     __nv_bfloat16 *dst = p.out + (int64_t)t * p.out_tok_stride + (int64_t)head * hd;
+    if (HDP >= 16 && hd == HDP && (reinterpret_cast<uintptr_t>(dst) & 31) == 0) {  // 32-byte stores
+#pragma unroll
+      for (int c = 0; c < HDP; c += 16) {
+        uint32_t w[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) w[i] = pack_bf16(o[c + 2 * i] * inv_l, o[c + 2 * i + 1] * inv_l);
+        asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst + c), "r"(w[0]), "r"(w[1]),
+                     "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+                     : "memory");
+      }
+      return;
+    }
 #pragma unroll
     for (int c = 0; c < HDP; c += 8) {
       if (c + 8 <= hd && (hd & 7) == 0) {
@@ -279,6 +291,19 @@ __device__ __forceinline__ void epilogue_row(const AttnParams &p, uint32_t t_o, 
     }
   } else if (p.part_bf16) {
     __nv_bfloat16 *dst = reinterpret_cast<__nv_bfloat16 *>(p.part_o) + part_row * (int64_t)hd;
+    if (HDP >= 16 && hd == HDP) {  // 32-byte stores (st.global.v8, whole sectors): half the store count
+#pragma unroll
+      for (int c = 0; c < HDP; c += 16) {
+        uint32_t w[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) w[i] = pack_bf16(o[c + 2 * i] * inv_l, o[c + 2 * i + 1] * inv_l);
+        asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst + c), "r"(w[0]), "r"(w[1]),
+                     "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+                     : "memory");
+      }
+      p.part_lse[part_row] = empty ? -INFINITY : (m_used + log2f(l_sum)) * 0.69314718055994531f;
+      return;
+    }
 #pragma unroll
     for (int c = 0; c < HDP; c += 8) {
       if (c + 8 <= hd && (hd & 7) == 0) {
@@ -294,6 +319,16 @@ __device__ __forceinline__ void epilogue_row(const AttnParams &p, uint32_t t_o, 
     p.part_lse[part_row] = empty ? -INFINITY : (m_used + log2f(l_sum)) * 0.69314718055994531f;
   } else {
     float *dst = reinterpret_cast<float *>(p.part_o) + part_row * (int64_t)hd;
+    if (HDP >= 8 && hd == HDP && (reinterpret_cast<uintptr_t>(dst) & 31) == 0) {  // 32-byte stores
+#pragma unroll
+      for (int c = 0; c < HDP; c += 8)
+        asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst + c), "f"(o[c] * inv_l),
+                     "f"(o[c + 1] * inv_l), "f"(o[c + 2] * inv_l), "f"(o[c + 3] * inv_l), "f"(o[c + 4] * inv_l),
+                     "f"(o[c + 5] * inv_l), "f"(o[c + 6] * inv_l), "f"(o[c + 7] * inv_l)
+                     : "memory");
+      p.part_lse[part_row] = empty ? -INFINITY : (m_used + log2f(l_sum)) * 0.69314718055994531f;
+      return;
+    }
 #pragma unroll
     for (int c = 0; c < HDP; c += 4) {
       if (c + 4 <= hd && (hd & 3) == 0) {
