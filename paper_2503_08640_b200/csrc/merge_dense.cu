@@ -162,59 +162,61 @@ __global__ void lse_merge_kernel(DbsaMergeArgs a) {
 }
 
 // Throughput form for the chunk-major batch (bf16 partials, head_dim 128): a
-// half-warp per row, 16-byte loads (8 dims per lane), the row's split LSEs
-// spread over the half-warp 16 at a time, 8 partial rows in flight.
+// quarter-warp per row, 32-byte loads (16 dims per lane), the row's split LSEs
+// spread over the quarter-warp 8 at a time, 8 partial rows in flight.
 __device__ __forceinline__ uint32_t pack2_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t *>(&v);
 }
 __global__ void lse_merge_bf16_h128_kernel(DbsaMergeArgs a) {
+  // a quarter-warp (8 lanes) per row, 32-byte loads (16 dims per lane)
+  const int qw = threadIdx.x >> 3, ql = threadIdx.x & 7;
+  const int r = blockIdx.x * (blockDim.x >> 3) + qw;
+  const bool live = r < a.groups[blockIdx.y].rows;
   const DbsaMergeGroup g = a.groups[blockIdx.y];
-  const int hw = threadIdx.x >> 4, hl = threadIdx.x & 15;
-  const int r = blockIdx.x * (blockDim.x >> 4) + hw;
-  const bool live = r < g.rows;
   const int gs = a.n_heads / a.n_kv_heads;
   const int64_t sstride = a.split_stride > 0 ? a.split_stride : g.rows;
   const int64_t row0 = g.part_row0 + (live ? r : 0);
   const int n = g.n_splits;
   const unsigned full = 0xffffffffu;
   float mx = -INFINITY;
-  for (int s = hl; s < n; s += 16) mx = fmaxf(mx, a.part_lse[row0 + (int64_t)s * sstride]);
+  for (int s = ql; s < n; s += 8) mx = fmaxf(mx, a.part_lse[row0 + (int64_t)s * sstride]);
 #pragma unroll
-  for (int o = 8; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(full, mx, o));
+  for (int o = 4; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(full, mx, o));
   float tot = 0.f;
-  for (int s = hl; s < n; s += 16) {
+  for (int s = ql; s < n; s += 8) {
     const float l = a.part_lse[row0 + (int64_t)s * sstride];
     tot += l == -INFINITY ? 0.f : __expf(l - mx);
   }
 #pragma unroll
-  for (int o = 8; o > 0; o >>= 1) tot += __shfl_xor_sync(full, tot, o);
+  for (int o = 4; o > 0; o >>= 1) tot += __shfl_xor_sync(full, tot, o);
   const float inv = tot > 0.f ? 1.f / tot : 0.f;
-  const __nv_bfloat16 *base = reinterpret_cast<const __nv_bfloat16 *>(a.part_o) + row0 * 128 + hl * 8;
-  const int src0 = threadIdx.x & 16;  // lane 0 of this half-warp
-  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  const int n_max = __reduce_max_sync(full, n);  // both half-warps walk the same trip count
-  for (int c0 = 0; c0 < n_max; c0 += 16) {
-    const int sl = c0 + hl;
+  const __nv_bfloat16 *base = reinterpret_cast<const __nv_bfloat16 *>(a.part_o) + row0 * 128 + ql * 16;
+  const int src0 = threadIdx.x & 24;  // lane 0 of this quarter-warp
+  float acc[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) acc[i] = 0.f;
+  for (int c0 = 0; c0 < n; c0 += 8) {
+    const int sl = c0 + ql;
     const float l = sl < n ? a.part_lse[row0 + (int64_t)sl * sstride] : -INFINITY;
     const float wl = l == -INFINITY ? 0.f : __expf(l - mx) * inv;
+    uint32_t v[8][8];
 #pragma unroll
-    for (int k = 0; k < 16; k += 8) {
-      uint4 v[8];
+    for (int u = 0; u < 8; ++u)
+      if (c0 + u < n)
+        asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(v[u][0]), "=r"(v[u][1]), "=r"(v[u][2]), "=r"(v[u][3]), "=r"(v[u][4]), "=r"(v[u][5]),
+                       "=r"(v[u][6]), "=r"(v[u][7])
+                     : "l"(base + (int64_t)(c0 + u) * sstride * 128));
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (c0 + k + u < n) v[u] = *reinterpret_cast<const uint4 *>(base + (int64_t)(c0 + k + u) * sstride * 128);
+    for (int u = 0; u < 8; ++u) {
+      const float wgt = __shfl_sync(full, wl, src0 + u);
+      if (c0 + u < n) {
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const float wgt = __shfl_sync(full, wl, src0 + k + u);
-        if (c0 + k + u < n) {
-          const __nv_bfloat162 *h2 = reinterpret_cast<const __nv_bfloat162 *>(&v[u]);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const float2 f = __bfloat1622float2(h2[i]);
-            acc[2 * i] += wgt * f.x;
-            acc[2 * i + 1] += wgt * f.y;
-          }
+        for (int i = 0; i < 8; ++i) {
+          const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&v[u][i]));
+          acc[2 * i] += wgt * f.x;
+          acc[2 * i + 1] += wgt * f.y;
         }
       }
     }
@@ -222,9 +224,12 @@ __global__ void lse_merge_bf16_h128_kernel(DbsaMergeArgs a) {
   if (live) {
     const int t = g.q_tok0 + r / gs, head = g.kv_head * gs + r % gs;
     __nv_bfloat16 *dst =
-        reinterpret_cast<__nv_bfloat16 *>(a.out) + (int64_t)t * a.out_tok_stride + (int64_t)head * 128 + hl * 8;
-    *reinterpret_cast<uint4 *>(dst) = make_uint4(pack2_bf16(acc[0], acc[1]), pack2_bf16(acc[2], acc[3]),
-                                                 pack2_bf16(acc[4], acc[5]), pack2_bf16(acc[6], acc[7]));
+        reinterpret_cast<__nv_bfloat16 *>(a.out) + (int64_t)t * a.out_tok_stride + (int64_t)head * 128 + ql * 16;
+    uint32_t w[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) w[i] = pack2_bf16(acc[2 * i], acc[2 * i + 1]);
+    *reinterpret_cast<uint4 *>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+    *reinterpret_cast<uint4 *>(dst + 8) = make_uint4(w[4], w[5], w[6], w[7]);
   }
 }
 
@@ -462,7 +467,7 @@ extern "C" int dbsa_lse_merge(const DbsaMergeArgs *args, void *stream) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const bool small = (int64_t)a.n_groups * a.max_rows <= 16384;
   if (a.part_bf16 && a.head_dim == 128 && !small) {
-    lse_merge_bf16_h128_kernel<<<dim3((a.max_rows + 7) / 8, a.n_groups), 128, 0, st>>>(a);
+    lse_merge_bf16_h128_kernel<<<dim3((a.max_rows + 15) / 16, a.n_groups), 128, 0, st>>>(a);
     return check_launch("lse_merge");
   }
   if (a.part_bf16) {
