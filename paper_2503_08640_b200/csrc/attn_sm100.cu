@@ -424,7 +424,9 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
   // K/V loads and first QK overlap this work's epilogue.
   using C = AttnCfg<HDP, NUM_M>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned base by pointer arithmetic on the shared array, so the
+  // compiler keeps the shared address space (STS for the Q tile, not generic ST)
+  uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t *sQ = smem;                         // NUM_M x Q_BYTES
   uint8_t *sK = sQ + NUM_M * C::Q_BYTES;      // KST x K_BYTES
   uint8_t *sV = sK + C::KST * C::K_BYTES;     // VST x V_BYTES
@@ -955,7 +957,9 @@ __global__ void __launch_bounds__(256, 1)
                       const AttnParams p) {
   using C = Attn1Cfg<HDP>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned base by pointer arithmetic on the shared array, so the
+  // compiler keeps the shared address space (STS for the Q tile, not generic ST)
+  uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t *sK = smem;                      // KST x K_BYTES
   uint8_t *sV = sK + C::KST * C::K_BYTES;  // VST x V_BYTES
   uint64_t *bars = reinterpret_cast<uint64_t *>(sV + C::VST * C::V_BYTES);
