@@ -43,6 +43,11 @@
 namespace dbsa {
 
 constexpr int kBN = 128;  // keys per tile
+// lazy O rescale: only when a row's max grows by more than 2^DBSA_RESCALE_LOG2
+// (P <= 2^DBSA_RESCALE_LOG2 stays exact in bf16's exponent range)
+#ifndef DBSA_RESCALE_LOG2
+#define DBSA_RESCALE_LOG2 8.f
+#endif
 
 // Profiling build only (-DDBSA_STAMPS, tools/build_variant.py + tools/stamps.py):
 // per-tile clock stamps of CTA 0 for the first 256 key tiles of the two-tile
@@ -762,7 +767,7 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
           // Lazy rescale (threshold 2^8).  S(m, j) being complete implies P.V(m, j-1)
           // retired (issued before QK(m, j) on the in-order tensor pipe), so O(m)
           // is quiescent here.  tcgen05.ld/st are warp-wide: the decision is warp-uniform.
-          const bool need = (m_used != -INFINITY) && (m_new > m_used + 8.f);
+          const bool need = (m_used != -INFINITY) && (m_new > m_used + DBSA_RESCALE_LOG2);
           float alpha = 1.f;
           if (__any_sync(0xffffffffu, need)) {
             if (m_used != -INFINITY) alpha = fast_exp2(m_used - m_new);
@@ -1208,7 +1213,7 @@ __global__ void __launch_bounds__(256, 1)
         for (int i = 0; i < 8; ++i) mx[i] = fmaxf(mx[i], x[kBN - 8 + i]);
         const float tmax = fmax3(fmax3(mx[0], mx[1], mx[2]), fmax3(mx[3], mx[4], mx[5]), fmaxf(mx[6], mx[7])) * sl2;
         const float m_new = fmaxf(m_used, tmax);
-        const bool need = (m_used != -INFINITY) && (m_new > m_used + 8.f);
+        const bool need = (m_used != -INFINITY) && (m_new > m_used + DBSA_RESCALE_LOG2);
         float alpha = 1.f;
         if (__any_sync(0xffffffffu, need)) {
           // O is accumulated by P.V(j-1), issued once P(j-1) arrived: wait for it
