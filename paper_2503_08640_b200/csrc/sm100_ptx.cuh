@@ -46,6 +46,17 @@ __device__ __forceinline__ void fence_mbar_init() {
 }
 __device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
   uint32_t ok;
+#ifdef DBSA_MBAR_HINT
+  // suspend-time hint: the waiting warp sleeps (woken by the phase completion)
+  // instead of re-polling -- fewer issue slots and less power in spin loops
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"((uint32_t)DBSA_MBAR_HINT)
+      : "memory");
+#else
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
@@ -53,6 +64,7 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
       : "=r"(ok)
       : "r"(smem_u32(bar)), "r"(parity)
       : "memory");
+#endif
   return ok != 0;
 }
 // Blocking wait on the phase with parity `parity`.  With DBSA_HANG_GUARD a
