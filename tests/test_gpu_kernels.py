@@ -311,8 +311,10 @@ class _DM:
 
 
 @pytest.mark.parametrize("schedule", ["chunk", "query", "chunk-padded"])
-@pytest.mark.parametrize("hd,H,Hkv", [(128, 8, 2), (64, 4, 4), (32, 8, 1)])
+@pytest.mark.parametrize("hd,H,Hkv", [(128, 8, 2), (64, 4, 4), (32, 8, 1), (128, 4, 4), (128, 16, 2)])
 def test_stage2_batch_schedules_vs_float64(schedule, hd, H, Hkv):
+    """(128, 4, 4): MHA at head_dim 128 (C4's layout, 256-token chunk works);
+    (128, 16, 2): GQA-8 (the 70B shape's grouping, 32-token works)."""
     """A batch of label jobs over overlapping chunk tables (whole groups and
     example-granularity sub-spans, assorted orders) through one layer of K3 +
     K3m, chunk-major (DBSA_OUT_MAPPED row-map works) and split-KV per query,
