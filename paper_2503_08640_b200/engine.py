@@ -284,14 +284,17 @@ class _Scratch:
         self.act = torch.empty((min(n_tok, self.ffn_chunk), c.ffn_dim), dtype=torch.bfloat16, device=dev)
 
 
-def _decoder_gen(dm, ids_dev, attend, write_kv, n_layers=None, kv_only_last=False):
+def _decoder_gen(dm, ids_dev, attend, write_kv, n_layers=None, kv_only_last=False, keep_last=None):
     """Pre-norm decoder body (model.py:319-359) over n new tokens, as a
     generator: it yields after each layer's `write_kv(l, qkv)` (the point where
     a multi-shard caller exchanges pages) and returns the fp32 final hidden
     states.  `attend(l, qkv, out)` fills the attention output.  kv_only_last:
     the caller only keeps K/V (a pool encode): the last layer stops after its
     page write -- its attention, O projection and FFN feed nothing -- and the
-    return value is None."""
+    return value is None.  keep_last (device int64 row indices): only those rows'
+    outputs are used (the scored rows of a label batch), so the last layer's O
+    projection and FFN run on them alone and the returned hidden states are
+    those rows, in keep_last order."""
     torch = _torch()
     c = dm.config
     n = ids_dev.shape[0]
@@ -310,6 +313,21 @@ def _decoder_gen(dm, ids_dev, attend, write_kv, n_layers=None, kv_only_last=Fals
         if kv_only_last and layer == L - 1:
             return None
         attend(layer, s.qkv, s.att)
+        if keep_last is not None and layer == L - 1:
+            k = keep_last.numel()
+            att = s.att.index_select(0, keep_last)
+            h = h.index_select(0, keep_last)
+            proj, xk = s.proj[:k], s.x[:k]
+            mm_f32(att, lw["wo"], proj)
+            ops.add_rmsnorm(h, proj, lw["ffn_norm"], c.norm_eps, xk)
+            for a in range(0, k, s.ffn_chunk):
+                b = min(k, a + s.ffn_chunk)
+                gu, act = s.gu[: b - a], s.act[: b - a]
+                torch.mm(xk[a:b], lw["wgu"], out=gu)
+                ops.silu_mul(gu, c.ffn_dim, out=act)
+                mm_f32(act, lw["wdown"], proj[a:b])
+            h.add_(proj)
+            return h
         mm_f32(s.att, lw["wo"], s.proj)
         ops.add_rmsnorm(h, s.proj, lw["ffn_norm"], c.norm_eps, s.x)
         for a in range(0, n, s.ffn_chunk):
@@ -331,8 +349,8 @@ def _drain(gen):
         return e.value
 
 
-def _decoder(dm, ids_dev, attend, write_kv, n_layers=None):
-    return _drain(_decoder_gen(dm, ids_dev, attend, write_kv, n_layers))
+def _decoder(dm, ids_dev, attend, write_kv, n_layers=None, keep_last=None):
+    return _drain(_decoder_gen(dm, ids_dev, attend, write_kv, n_layers, keep_last=keep_last))
 
 
 # ============================================================== stage 1 (K1 + K2w)
@@ -935,8 +953,9 @@ def _merge_array(merges) -> np.ndarray:
     return a
 
 
-def run_jobs(dm, store, jobs, target_ctas=None, plan=None):
-    """Forward every job's new tokens; returns (plan, fp32 hidden [n_tok, d])."""
+def run_jobs(dm, store, jobs, target_ctas=None, plan=None, keep=None):
+    """Forward every job's new tokens; returns (plan, fp32 hidden [n_tok, d]), or
+    only the rows `keep` (LabelScorer.keep) when given."""
     c = dm.config
     plan = plan or Stage2Plan(dm, jobs, target_ctas)
     nt, sched = plan.new, plan.sched
@@ -954,7 +973,7 @@ def run_jobs(dm, store, jobs, target_ctas=None, plan=None):
             ops.lse_merge(sched.part_o, sched.part_lse, sched.merges, sched.n_merge, sched.max_rows, c.n_heads,
                           c.n_kv_heads, c.head_dim, out, qw)
 
-    h = _decoder(dm, nt.ids, attend, write_kv)
+    h = _decoder(dm, nt.ids, attend, write_kv, keep_last=keep)
     return plan, h
 
 
@@ -1084,8 +1103,8 @@ class GraphedStage2:
         self.launches = ops.LAUNCHES - n0
 
     def _run(self):
-        _, h = run_jobs(self.dm, self.store, None, plan=self.plan)
-        return self.scorer(self.dm, h)
+        _, h = run_jobs(self.dm, self.store, None, plan=self.plan, keep=self.scorer.keep)
+        return self.scorer(self.dm, h, subset=True)
 
     def replay(self, plan, scorer):
         """Copy `plan`'s tables into the captured buffers and replay."""
@@ -1095,7 +1114,8 @@ class GraphedStage2:
         if n is not t:
             pairs = [(t.new.pos, n.new.pos), (t.new.lo, n.new.lo), (t.new.ids, n.new.ids), (t.new.pages, n.new.pages),
                      (self.scorer.rows, scorer.rows), (self.scorer.targets, scorer.targets),
-                     (self.scorer.owner, scorer.owner), (self.scorer.label_row0, scorer.label_row0)]
+                     (self.scorer.owner, scorer.owner), (self.scorer.label_row0, scorer.label_row0),
+                     (self.scorer.keep, scorer.keep), (self.scorer.rows_in_keep, scorer.rows_in_keep)]
             if isinstance(t.sched, ChunkMajorSchedule):
                 t.sched.copy_tables_from(n.sched)
             else:
@@ -1121,7 +1141,7 @@ def plan_key(plan, scorer):
     else:
         tables = ("query", sc.n_works, sc.n_segs)
     return (plan.new.n_tok, tuple(plan.new.n_new), plan.new.n_pages, tables, sc.n_merge, sc.part_rows,
-            int(scorer.rows.numel()), scorer.n_out, plan.new.num_m)
+            int(scorer.rows.numel()), int(scorer.keep.numel()), scorer.n_out, plan.new.num_m)
 
 
 def fits_graph(graph, plan) -> bool:
@@ -1160,6 +1180,11 @@ class LabelScorer:
                     prev = base + off + k
                 off += len(lab) - 1
         dev = dm.device
+        # distinct scored rows (the last query row serves every label): the last
+        # layer's O projection and FFN run on these alone (run_jobs keep=)
+        keep = np.unique(np.asarray(rows, np.int64))
+        self.keep = ops.h2d(keep, dev)
+        self.rows_in_keep = ops.h2d(np.searchsorted(keep, np.asarray(rows, np.int64)).astype(np.int64), dev)
         self.rows = ops.h2d(np.asarray(rows, np.int64), dev)
         self.targets = ops.h2d(np.asarray(targets, np.int32), dev)
         self.owner = ops.h2d(np.asarray(owner, np.int64), dev)
@@ -1169,8 +1194,9 @@ class LabelScorer:
         self.n_out = len(jobs) * n_labels
         self.n_labels = n_labels
 
-    def __call__(self, dm, h):
-        logits = _final_logits(dm, h.index_select(0, self.rows))
+    def __call__(self, dm, h, subset: bool = False):
+        """h: all rows' final hidden states, or (subset) only the rows `keep`."""
+        logits = _final_logits(dm, h.index_select(0, self.rows_in_keep if subset else self.rows))
         lp = ops.label_logprob(logits, self.targets)
         return ops.label_reduce(lp, self.label_row0, self.n_out // self.n_labels, self.n_labels)
 
@@ -1179,8 +1205,10 @@ def score_labels(dm, assembled, query_ids, labels):
     """Per-label scores (host float array) of one query against `assembled`."""
     store, chunks, n_ctx = _ctx_of(assembled)
     job = label_job(chunks, n_ctx, query_ids, labels)
-    plan, h = run_jobs(dm, store, [job])
-    scores, _ = LabelScorer(dm, plan, [job], len(labels))(dm, h)
+    plan = Stage2Plan(dm, [job])
+    scorer = LabelScorer(dm, plan, [job], len(labels))
+    _, h = run_jobs(dm, store, [job], plan=plan, keep=scorer.keep)
+    scores, _ = scorer(dm, h, subset=True)
     return scores[0].double().cpu().numpy()
 
 

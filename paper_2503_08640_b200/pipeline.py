@@ -269,9 +269,9 @@ class Stage2Session:
 
     def run(self, jobs, plan):
         """Forward + label scoring; returns device (scores [B, n_labels], argmax [B])."""
-        _, h = engine.run_jobs(self.dm, self.cache.store, jobs, plan=plan)
         scorer = engine.LabelScorer(self.dm, plan, jobs, len(self.label_ids))
-        return scorer(self.dm, h)
+        _, h = engine.run_jobs(self.dm, self.cache.store, jobs, plan=plan, keep=scorer.keep)
+        return scorer(self.dm, h, subset=True)
 
     def _capacity(self, jobs):
         """Upper bound of a chunk-major batch's (works, segments) for this
