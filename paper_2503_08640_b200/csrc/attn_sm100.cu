@@ -45,6 +45,10 @@ namespace dbsa {
 constexpr int kBN = 128;  // keys per tile
 // lazy O rescale: only when a row's max grows by more than 2^DBSA_RESCALE_LOG2
 // (P <= 2^DBSA_RESCALE_LOG2 stays exact in bf16's exponent range)
+// Q staging: load iterations batched per round trip (1 = one at a time)
+#ifndef DBSA_QSTAGE_BATCH
+#define DBSA_QSTAGE_BATCH 4
+#endif
 #ifndef DBSA_RESCALE_LOG2
 #define DBSA_RESCALE_LOG2 8.f
 #endif
@@ -381,6 +385,54 @@ __device__ __forceinline__ void stage_q_coop(const AttnParams &p, const DbsaAttn
     for (int it = 0; it < NIT; ++it)
       if (tok[it] >= 0) rrow[it] = p.tok_pos[tok[it]] - shift;
   }
+#if DBSA_QSTAGE_BATCH > 1
+  // phase B, batched: the loads of QB iterations are issued before any of
+  // them is used, so QB round trips overlap (QB x 24 registers in flight)
+  constexpr int QB = DBSA_QSTAGE_BATCH < NIT ? DBSA_QSTAGE_BATCH : NIT;
+#pragma unroll
+  for (int i0 = 0; i0 < NIT; i0 += QB) {
+    uint4 lo4[QB], hi4[QB];
+    float4 cs4[QB][4];
+#pragma unroll
+    for (int k = 0; k < QB; ++k) {
+      const int it = i0 + k;
+      const int tk = tok[it] >= 0 ? tok[it] : tok[0] >= 0 ? tok[0] : 0;  // invalid rows read a safe row
+      const int hk = tok[it] >= 0 ? head[it] : 0, rk = tok[it] >= 0 ? rrow[it] : 0;
+      const __nv_bfloat16 *src = p.q + (int64_t)tk * p.q_tok_stride + (int64_t)hk * HDP + c * 8;
+      const float4 *rp = reinterpret_cast<const float4 *>(p.rope + (int64_t)rk * half + c * 8);
+      lo4[k] = __ldg(reinterpret_cast<const uint4 *>(src));
+      hi4[k] = __ldg(reinterpret_cast<const uint4 *>(src + half));
+#pragma unroll
+      for (int v = 0; v < 4; ++v) cs4[k][v] = __ldg(rp + v);
+    }
+#pragma unroll
+    for (int k = 0; k < QB; ++k) {
+      const int it = i0 + k;
+      const int row = q4 * 32 + it * RPI + rsub;
+      const __nv_bfloat16 *lo = reinterpret_cast<const __nv_bfloat16 *>(&lo4[k]);
+      const __nv_bfloat16 *hi = reinterpret_cast<const __nv_bfloat16 *>(&hi4[k]);
+      const float *cs = reinterpret_cast<const float *>(cs4[k]);
+      const float keep = tok[it] >= 0 ? 1.f : 0.f;
+      float a[8], b[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float cc = cs[2 * j] * keep, sn = cs[2 * j + 1] * keep;
+        const float xl = __bfloat162float(lo[j]), yh = __bfloat162float(hi[j]);
+        a[j] = xl * cc - yh * sn;
+        b[j] = xl * sn + yh * cc;
+      }
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const float(&o)[8] = hh ? b : a;
+        const int ch = hh * NCH + c;
+        const int atom = ch / (QSW / 16), cc = ch % (QSW / 16);
+        uint4 *d = reinterpret_cast<uint4 *>(q_tile + atom * 128 * QSW + swz_offset(row, cc, QSW));
+        *d = make_uint4(pack_bf16(o[0], o[1]), pack_bf16(o[2], o[3]), pack_bf16(o[4], o[5]), pack_bf16(o[6], o[7]));
+      }
+    }
+  }
+  return;
+#endif
   // phase B: q chunk pair + its (cos, sin), rotate, swizzled 16-byte stores
 #pragma unroll
   for (int it = 0; it < NIT; ++it) {
