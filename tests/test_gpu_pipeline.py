@@ -22,7 +22,7 @@ pytestmark = pytest.mark.gpu
 from golden_util import CASES, load, oracle_pool  # noqa: E402
 from oracle import dbsa_oracle as O  # noqa: E402
 import paper_2503_08640_b200 as P  # noqa: E402
-from paper_2503_08640_b200 import masks, pipeline, retrieval, tokenizer  # noqa: E402
+from paper_2503_08640_b200 import engine, masks, pipeline, retrieval, tokenizer  # noqa: E402
 
 LOGIT_TOL = 2e-2
 KV_TOL = 3e-2
@@ -142,6 +142,27 @@ def test_stage2_batched_k4_path_matches_reference(name, schedule, monkeypatch):
         np.testing.assert_array_equal(ids_b, ids1)
         np.testing.assert_array_equal(best_b, best1.cpu().numpy())
         np.testing.assert_allclose(s_b, s1.cpu().numpy(), atol=1e-5)
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_stage2_scored_row_subset_equals_full(name):
+    """The last layer's O projection and FFN on the distinct scored rows only
+    (LabelScorer.keep) give the same label scores as the full last layer."""
+    meta, a, w, task, mc, enc = _encoded(name)
+    runner = P.Runner(w, enc.cache, enc.index, task, mc)
+    texts = [q["query"] for q in meta["queries"]]
+    sess = runner.session()
+    scores = enc.index.score_matrix([retrieval.bm25_tokenize(t) for t in texts])
+    q_ids = [tokenizer.encode(task.template.render_query(t)) for t in texts]
+    jobs, plan = sess.plan(sess.select(scores), q_ids)
+    scorer = engine.LabelScorer(sess.dm, plan, jobs, len(sess.label_ids))
+    assert scorer.keep.numel() < plan.new.n_tok
+    _, h_sub = engine.run_jobs(sess.dm, sess.cache.store, jobs, plan=plan, keep=scorer.keep)
+    s_sub, b_sub = scorer(sess.dm, h_sub, subset=True)
+    _, h_all = engine.run_jobs(sess.dm, sess.cache.store, jobs, plan=plan)
+    s_all, b_all = scorer(sess.dm, h_all)
+    np.testing.assert_allclose(s_sub.cpu().numpy(), s_all.cpu().numpy(), atol=2e-3, rtol=1e-4)
+    np.testing.assert_array_equal(b_sub.cpu().numpy(), b_all.cpu().numpy())
 
 
 def test_forward_query_logits_c1():
