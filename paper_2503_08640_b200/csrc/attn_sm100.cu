@@ -431,8 +431,7 @@ __device__ __forceinline__ void stage_q_coop(const AttnParams &p, const DbsaAttn
       }
     }
   }
-  return;
-#endif
+#else
   // phase B: q chunk pair + its (cos, sin), rotate, swizzled 16-byte stores
 #pragma unroll
   for (int it = 0; it < NIT; ++it) {
@@ -469,6 +468,7 @@ __device__ __forceinline__ void stage_q_coop(const AttnParams &p, const DbsaAttn
       *d = make_uint4(pack_bf16(o[0], o[1]), pack_bf16(o[2], o[3]), pack_bf16(o[4], o[5]), pack_bf16(o[6], o[7]));
     }
   }
+#endif
 }
 
 template <int HDP, int NUM_M>
