@@ -309,23 +309,38 @@ class Stage2Session:
     def answer_stream(self, batches):
         """Pipelined answer() over an iterable of (scores, query_ids_list)
         batches; yields (ids, scores [B, n_labels], argmax [B]) as HOST arrays,
-        in order.  Batch i+1's K4 selection runs on a side stream while batch
-        i's forward replays on the current stream, so its ids come back, and
-        its chunk tables are planned on the host, while the GPU is busy; each
-        batch's results are copied out to pinned memory right behind its
-        replay (the captured graph reuses its output buffers)."""
+        in order.  Batch i+1's K4 selection is enqueued on a side stream
+        before batch i's graph replay, so its ids are back on the host (and
+        its chunk tables are planned) while the GPU runs batch i; each batch's
+        results are copied out to pinned memory right behind its replay (the
+        captured graph reuses its output buffers)."""
         import torch
 
         main = torch.cuda.current_stream(self.dm.device)
         side = torch.cuda.Stream(self.dm.device)
-        pending = None
-        for scores, q_ids in batches:
+        side.wait_stream(main)
+
+        def select_async(batch):
+            scores, q_ids = batch
             with torch.cuda.stream(side):
                 if not isinstance(scores, torch.Tensor):
                     scores = torch.from_numpy(np.ascontiguousarray(scores)).pin_memory()
                 ids_dev = engine.ops.topk_select(scores.to(self.dm.device, non_blocking=True), self.budget,
                                                  self.ordering)
-                ids = ids_dev.cpu().numpy().astype(np.int64)  # waits for the side stream only
+                ids_host = torch.empty(ids_dev.shape, dtype=ids_dev.dtype, pin_memory=True)
+                ids_host.copy_(ids_dev, non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(side)
+            return ev, ids_host, q_ids
+
+        it = iter(batches)
+        first = next(it, None)
+        nxt = select_async(first) if first is not None else None
+        pending = None
+        while nxt is not None:
+            ev_sel, ids_host, q_ids = nxt
+            ev_sel.synchronize()  # this batch's K4 only
+            ids = ids_host.numpy().astype(np.int64)
             jobs, plan = self.plan(ids, q_ids)
             scorer = engine.LabelScorer(self.dm, plan, jobs, len(self.label_ids))
             key = engine.plan_key(plan, scorer)
@@ -334,6 +349,8 @@ class Stage2Session:
                 main.synchronize()
                 graphs[key] = engine.GraphedStage2(self.dm, self.cache.store, jobs, plan, len(self.label_ids),
                                                    capacity=self._capacity(jobs))
+            b = next(it, None)
+            nxt = select_async(b) if b is not None else None  # ahead of this batch's replay
             s_dev, best_dev = graphs[key].replay(plan, scorer)
             s_host = torch.empty(s_dev.shape, dtype=s_dev.dtype, pin_memory=True)
             b_host = torch.empty(best_dev.shape, dtype=best_dev.dtype, pin_memory=True)
