@@ -145,6 +145,28 @@ def test_stage2_batched_k4_path_matches_reference(name, schedule, monkeypatch):
 
 
 @pytest.mark.parametrize("name", CASES)
+def test_answer_stream_mixed_shapes_generator(name):
+    """answer_stream over a generator of batches whose shapes change mid-stream
+    (a new graph is captured while the next batch's K4 is already in flight):
+    every batch equals answer() on its own, in order."""
+    meta, a, w, task, mc, enc = _encoded(name)
+    runner = P.Runner(w, enc.cache, enc.index, task, mc)
+    sess = runner.session()
+    texts = [q["query"] for q in meta["queries"]]
+    scores = enc.index.score_matrix([retrieval.bm25_tokenize(t) for t in texts])
+    q_ids = [tokenizer.encode(task.template.render_query(t)) for t in texts]
+    cuts = [(0, 3), (3, 6), (6, 8), (0, 1), (1, 4)]
+    got = list(sess.answer_stream((scores[i:j], q_ids[i:j]) for i, j in cuts))
+    assert len(got) == len(cuts)
+    for (i, j), (ids_b, s_b, best_b) in zip(cuts, got):
+        ids1, s1, best1 = sess.answer(scores[i:j], q_ids[i:j])
+        np.testing.assert_array_equal(ids_b, ids1)
+        np.testing.assert_array_equal(best_b, best1.cpu().numpy())
+        np.testing.assert_allclose(s_b, s1.cpu().numpy(), atol=1e-5)
+    assert list(sess.answer_stream(iter(()))) == []
+
+
+@pytest.mark.parametrize("name", CASES)
 def test_stage2_scored_row_subset_equals_full(name):
     """The last layer's O projection and FFN on the distinct scored rows only
     (LabelScorer.keep) give the same label scores as the full last layer."""
