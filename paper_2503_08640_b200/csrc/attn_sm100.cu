@@ -389,6 +389,7 @@ __device__ __forceinline__ void stage_q_coop(const AttnParams &p, const DbsaAttn
   // phase B, batched: the loads of QB iterations are issued before any of
   // them is used, so QB round trips overlap (QB x 24 registers in flight)
   constexpr int QB = DBSA_QSTAGE_BATCH < NIT ? DBSA_QSTAGE_BATCH : NIT;
+  static_assert(NIT % QB == 0, "DBSA_QSTAGE_BATCH must divide the staging iterations");
 #pragma unroll
   for (int i0 = 0; i0 < NIT; i0 += QB) {
     uint4 lo4[QB], hi4[QB];
