@@ -58,6 +58,25 @@ Q_TOK, N_LABELS, LABEL_TOK = 32, 4, 4
 RATIO = 0.30
 
 
+def workload(cfg_key: str) -> str:
+    """config.workload, identical in both arms (ours and --impl reference)."""
+    budget = int(math.ceil(RATIO * N_GROUPS))
+    return (f"{cfg_key.upper()}: {CONFIGS[cfg_key]['name']}, {RATIO:.0%} retrieval ({budget} groups, "
+            f"T'={budget * GROUP_TOK}), query {Q_TOK} tok + {N_LABELS} labels x {LABEL_TOK} tok")
+
+
+def blas_threads() -> str:
+    """The BLAS thread pools numpy uses on this host (threadpoolctl)."""
+    try:
+        from threadpoolctl import threadpool_info
+
+        info = [f"{d.get('internal_api')}={d.get('num_threads')}" for d in threadpool_info()
+                if d.get("user_api") == "blas"]
+        return ",".join(info) or "none"
+    except Exception as exc:  # pragma: no cover - diagnostic only
+        return f"unknown ({type(exc).__name__})"
+
+
 def select_config(name: str, ratio: float):
     global CFG8B, N_GROUPS, GROUP_TOK, RATIO
     c = CONFIGS[name]
@@ -188,6 +207,8 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator lines on stderr (one rank per GPU)
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=dev)
 
     cfg = P.ModelConfig(**CFG8B)
@@ -252,7 +273,7 @@ def run_ours(args):
                            "peak_burst": tf_burst, "unit": "TFLOP/s",
                            "frac": (k1_flops / (k1_ms / 1e3) / 1e12) / tf_sus if k1_ms else None,
                            "frac_of_burst": (k1_flops / (k1_ms / 1e3) / 1e12) / tf_burst if k1_ms else None,
-                           "traffic": traffic_for("k1", "c2"), "launch_ms": k1_ms,
+                           "traffic": traffic_for("k1", "c2" if args.config == "c3" else args.config), "launch_ms": k1_ms,
                            "flops_per_launch": k1_flops,
                            "share_of_step": (k1_ms * (cfg.n_layers - 1)) / s1_times[-1] if k1_ms else None,  # the last layer stops after its page write
                            "peak_source": peak_src}}
@@ -377,6 +398,27 @@ def run_ours(args):
             torch.cuda.synchronize()
             dl.append(e0b.elapsed_time(e1b))
         extra["latency_b1_device_ms"] = float(np.median(dl[3:]))
+        # batch-1 K3 against HBM (the one genuinely bandwidth-bound K3 instance):
+        # algorithmic bytes per launch = the query's selected K/V (T' tokens x
+        # 2 x Hkv x hd x 2 B, one layer) + its own tokens' K/V + Q in + O out
+        kb1, mb1 = KernelTimer(), KernelTimer()
+        orig_merge = ops.lse_merge
+        ops.attention, ops.lse_merge = kb1.wrap(orig_attn), mb1.wrap(orig_merge)
+        for _ in range(3):
+            sess.run(jobs1, plan1)
+        torch.cuda.synchronize()
+        ops.attention, ops.lse_merge = orig_attn, orig_merge
+        kb1.pairs = kb1.pairs[cfg.n_layers:]  # first forward = warm-up
+        mb1.pairs = mb1.pairs[len(mb1.pairs) // 3:]
+        n1 = plan1.new.n_tok
+        b1_bytes = (plan1.kv_tokens + n1) * 2 * cfg.n_kv_heads * cfg.head_dim * 2 + 2 * n1 * cfg.n_heads * cfg.head_dim * 2
+        b1_ms = kb1.mean_ms()
+        b1_gbs = b1_bytes / (b1_ms / 1e3) / 1e9
+        extra["roofline_b1"] = {"kernel": f"dbsa_attn_kernel (K3, batch 1, {plan1.schedule} schedule)", "bound": "hbm",
+                                "achieved": b1_gbs, "peak": hbm, "unit": "GB/s", "frac": b1_gbs / hbm,
+                                "bytes_per_launch": b1_bytes, "launch_ms": b1_ms,
+                                "merge_ms": mb1.mean_ms(), "works_per_launch": plan1.n_works,
+                                "traffic": traffic_for("k3b1", args.config), "peak_source": peak_src}
         st0 = steps[W]
         jobs0, plan0c = st0[3], st0[4]
         Tp = sess.budget * GROUP_TOK
@@ -433,29 +475,40 @@ def run_ours(args):
                                              "too); ratio_vs_per_query_dense = selected chunk-major K3 vs the dense "
                                              "run through the per-query split-KV schedule"}
 
-    # roofline of K3 (dominant stage-2 kernel): algorithmic bytes per launch =
-    # selected KV (2 * Hkv * hd * 2 B per token, one layer) + Q in + O out.
-    plan0 = steps[W][4]
+    # roofline of K3, the dominant stage-2 kernel.  The chunk-major batch streams
+    # each selected group's K/V once per batch for every query that selected
+    # it, so it is bound by the tensor pipe, not HBM: algorithmic FLOPs per
+    # launch = 4 * hd * (gs rows per token) * Hkv * sum over the batch's tokens
+    # of the keys each sees (T' context + its visible self keys).  The
+    # per-query HBM accounting (selected KV + Q + O) is kept
+    # as "effective" bandwidth only; `traffic` is ncu's measured DRAM bytes.
+    plan0, jobs0 = steps[W][4], steps[W][3]
     kv_bytes = plan0.kv_tokens * 2 * cfg.n_kv_heads * cfg.head_dim * 2  # kv_tokens = selected tokens, all queries
     qo_bytes = 2 * plan0.n_tok * cfg.n_heads * cfg.head_dim * 2
+    k3_flops = k3_algorithmic_flops(jobs0, cfg)
     k3_ms = k3.mean_ms()
-    achieved = (kv_bytes + qo_bytes) / (k3_ms / 1e3) / 1e9 if k3_ms else None
+    k3_tf = k3_flops / (k3_ms / 1e3) / 1e12 if k3_ms else None
+    traffic = traffic_for("k3", f"{args.config}_r{RATIO:.2f}")
     clocks = clk.summary()
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": dev_ms / K, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (random-init weights, uniform token ids, U(0,1) f64 retrieval scores)",
-        "config": {"workload": f"{args.config.upper()}: {CONFIGS[args.config]['name']}, {RATIO:.0%} retrieval "
-                               f"({sess.budget} groups, T'={sess.budget * GROUP_TOK}), query {Q_TOK} tok + "
-                               f"{N_LABELS} labels x {LABEL_TOK} tok",
+        "config": {"workload": workload(args.config),
                    "queries_per_step_per_gpu": B, "parallelism": f"query-dp{world}",
                               "l2": "inputs larger than L2 (KV page pool + bf16 weights, each > 126 MB L2)"},
         "e2e": {"value": e2e_ms / n_queries, "unit": UNIT, "h2d_bytes_per_step": h2d // K,
                 "d2h_bytes_per_step": d2h // K},
-        "roofline": {"kernel": "dbsa_attn_kernel (K3)", "bound": "hbm", "achieved": achieved, "peak": hbm,
-                     "unit": "GB/s", "frac": achieved / hbm if achieved else None,
-                     "traffic": traffic_for("k3", "c3"), "launch_ms": k3_ms,
-                     "bytes_per_launch": kv_bytes + qo_bytes,
+        "roofline": {"kernel": "dbsa_attn_kernel<128,2> (K3, chunk-major batch)", "bound": "tensor",
+                     "achieved": k3_tf, "peak": tf_sus, "unit": "TFLOP/s",
+                     "frac": k3_tf / tf_sus if k3_tf else None,
+                     "peak_kind": "sustained bf16 (K3 is timed inside the long stage-2 step)",
+                     "frac_of_burst": k3_tf / tf_burst if k3_tf else None, "peak_burst": tf_burst,
+                     "flops_per_launch": k3_flops, "launch_ms": k3_ms,
+                     "traffic": traffic,
+                     "traffic_hbm_frac": (traffic / (k3_ms / 1e3) / 1e9) / hbm if traffic and k3_ms else None,
+                     "effective_per_query_bytes": kv_bytes + qo_bytes,
+                     "effective_gbs": (kv_bytes + qo_bytes) / (k3_ms / 1e3) / 1e9 if k3_ms else None,
                      "share_of_step": (k3_ms * cfg.n_layers) / (dev_ms / K) if k3_ms else None,
                      "peak_source": peak_src},
         "stage1": stage1,
@@ -472,6 +525,20 @@ def run_ours(args):
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
+
+
+def k3_algorithmic_flops(jobs, cfg) -> float:
+    """4 * hd * H * sum over the batch's new tokens of the keys each one sees:
+    the query's T' selected context tokens plus its visible self keys under
+    the query/label tree mask (model.py:381-384; engine.label_job)."""
+    keys = 0
+    for j in jobs:
+        n = len(j.ids)
+        i = np.arange(n)
+        lo = np.asarray(j.lo, np.int64)
+        vis = np.where(i < j.prefix, i + 1, j.prefix + (i - np.maximum(lo, j.prefix) + 1))
+        keys += n * j.n_ctx + int(vis.sum())
+    return 4.0 * cfg.head_dim * cfg.n_heads * keys
 
 
 def c1_end_to_end(dev):
@@ -581,8 +648,8 @@ def cpu_reference_sample(steps=1, seconds=20.0):
     cores = len(os.sched_getaffinity(0))
     return {"value": per_query * 1e3, "unit": UNIT, "cores": cores, "kind": "port",
             "sample": f"{len(layer_s)} x (one layer of reference _forward for one label, 36 tok vs T'={Tp}, 8B shape; "
-                      f"plus one layer of assemble); extrapolated x{N_LABELS} labels x{L} layers; numpy/OpenBLAS "
-                      f"threads={os.environ.get('OPENBLAS_NUM_THREADS', 'default')}",
+                      f"plus one layer of assemble); extrapolated x{N_LABELS} labels x{L} layers; numpy BLAS "
+                      f"threads: {blas_threads()}",
             "layer_label_s": float(np.median(layer_s)), "assemble_layer_s": float(np.median(asm_s))}
 
 
@@ -605,9 +672,7 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall * 1e3 / max(1, args.steps),
             "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": f"{args.config.upper()}: {CONFIGS[args.config]['name']}, {RATIO:.0%} retrieval, "
-                                   f"query {Q_TOK} tok + {N_LABELS} labels x {LABEL_TOK} tok",
-                       "parallelism": "host CPU"},
+            "config": {"workload": workload(args.config), "parallelism": "host CPU"},
             "cpu_baseline": cb, "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 
@@ -627,6 +692,20 @@ def main():
     ap.add_argument("--schedule", default=None, choices=["chunk", "query"],
                     help="stage-2 K3 schedule (default: chunk-major for batches, split-KV per query for one query)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        # one process per GPU: relaunch this command under torchrun on 127.0.0.1
+        import socket
+
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        env = dict(os.environ)
+        env.setdefault("NCCL_DEBUG", "INFO")  # communicator lines on stderr: one rank per GPU, transport used
+        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()),
+               *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd, env=env))
     select_config(args.config, args.ratio)
     if args.schedule:
         os.environ["DBSA_STAGE2_SCHEDULE"] = args.schedule

@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define DBSA_ABI_VERSION 4
+#define DBSA_ABI_VERSION 5
 #define DBSA_PAGE_TOKENS 64
 
 /* Error codes -> reference exceptions (errors.py:4-29). */
@@ -136,6 +136,10 @@ typedef struct DbsaAttnArgs {
   float *part_lse; /* fp32 [rows], natural-log LSE (out_mode 1 / 2) */
   const DbsaRowMap *row_map; /* device; required when any work is DBSA_OUT_MAPPED, else may be NULL */
   int32_t part_bf16;         /* partial O element type: 0 fp32, 1 bf16 */
+  unsigned long long *pair_count; /* optional (NULL = off): the kernel adds the number of (query row, key)
+                                     pairs whose score entered its softmax, i.e. the unmasked entries of every
+                                     tile it visited, over all heads.  For stage 1 this equals
+                                     n_heads * masks.count_allowed_token_pairs (masks.py:111-123). */
 } DbsaAttnArgs;
 int dbsa_attention(const DbsaAttnArgs *args, void *stream);
 

@@ -36,7 +36,7 @@ EXPORTED_SYMBOLS = (
     "dbsa_last_error",
 )
 
-ABI_VERSION = 4
+ABI_VERSION = 5
 OUT_BF16, OUT_PARTIAL, OUT_MAPPED = 0, 1, 2
 PAGE_TOKENS = 64
 SEG_FULL = 0
@@ -70,7 +70,7 @@ class AttnArgs(ctypes.Structure):
         ("scale", _f32), ("num_m", _i32),
         ("works", _vp), ("n_works", _i32), ("segs", _vp),
         ("out", _vp), ("out_tok_stride", _i64), ("part_o", _vp), ("part_lse", _vp),
-        ("row_map", _vp), ("part_bf16", _i32),
+        ("row_map", _vp), ("part_bf16", _i32), ("pair_count", _vp),
     ]
 
 

@@ -119,7 +119,23 @@ struct AttnParams {
   int part_bf16;  // out_mode DBSA_OUT_MAPPED works: q_tok0 indexes this map
   int dbg;  // profiling switches (DBSA_DEBUG_MODE): 1 = skip softmax math, 2 = skip MMAs, 4 = skip TMA loads,
             // 8 = skip epilogue stores, 16 = skip Q staging (two-tile kernel)
+  unsigned long long *pair_count;  // optional: (row, key) pairs that entered the softmax (all heads)
 };
+
+// Pair counter (DbsaAttnArgs.pair_count): the unmasked entries of the S row a
+// thread just masked, i.e. exactly the keys its softmax takes in.
+__device__ __forceinline__ uint32_t count_visible(const float (&x)[kBN]) {
+  uint32_t n = 0;
+#pragma unroll
+  for (int c = 0; c < kBN; ++c) n += x[c] != -INFINITY ? 1u : 0u;
+  return n;
+}
+__device__ __forceinline__ void flush_pair_count(unsigned long long *dst, uint32_t n) {
+  unsigned long long v = n;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(dst, v);
+}
 
 // 2^x for a pair on the FMA/ALU pipes (FA4's MUFU offload): round to the
 // nearest integer with the 1.5*2^23 trick, a cubic for 2^f on f in [-0.5, 0.5]
@@ -723,6 +739,7 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
     const uint32_t t_o = lane_base + m * HDP;
     const float sl2 = p.scale_log2;
     int jg = 0, wk = 0;
+    uint32_t n_pairs = 0;  // pair counter (p.pair_count)
 
     const bool coop = HDP >= 16 && p.head_dim == HDP && (p.q_tok_stride & 7) == 0;
     auto stage_q = [&](const DbsaAttnWork &wq, bool restage, int shift) {
@@ -804,6 +821,7 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
               for (int c = 0; c < kBN; ++c) x[c] = (c >= c_lo) & (c < c_hi) ? x[c] : -INFINITY;
             }
           }
+          if (p.pair_count && valid) n_pairs += count_visible(x);
           float mx[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) mx[i] = fmax3(x[i], x[i + 8], x[i + 16]);
@@ -900,6 +918,7 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
       mbar_arrive(&o_free[m]);  // O(m) may be overwritten by the next work's first P.V
       if (trow == 0) WSTAMP(m * 4 + 3, wk);
     }
+    if (p.pair_count) flush_pair_count(p.pair_count, n_pairs);
   }
 
   tc_fence_before();
@@ -1209,6 +1228,7 @@ __global__ void __launch_bounds__(256, 1)
     const float sl2 = p.scale_log2;
     const bool warp_dead = __all_sync(0xffffffffu, !valid);
     float m_used = -INFINITY, l_sum = 0.f;
+    uint32_t n_pairs = 0;  // pair counter (p.pair_count)
     int j = 0;
     for (int si = w.seg_begin; si < w.seg_end; ++si) {
       const DbsaAttnSeg sg = p.segs[si];
@@ -1255,6 +1275,7 @@ __global__ void __launch_bounds__(256, 1)
             x[c] = ok ? x[c] : -INFINITY;
           }
         }
+        if (p.pair_count && valid) n_pairs += count_visible(x);
         float mx[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) mx[i] = fmax3(x[i], x[i + 8], x[i + 16]);
@@ -1315,6 +1336,7 @@ __global__ void __launch_bounds__(256, 1)
     mbar_wait(o_full, 0);
     tc_fence_after();
     epilogue_row<HDP>(p, t_o, valid, t, head, w.out_mode, xr.part_row, l_sum, m_used);
+    if (p.pair_count) flush_pair_count(p.pair_count, n_pairs);
   }
 
   tc_fence_before();
@@ -1459,6 +1481,7 @@ extern "C" int dbsa_attention(const DbsaAttnArgs *args, void *stream) {
   p.part_lse = a.part_lse;
   p.row_map = a.row_map;
   p.part_bf16 = a.part_bf16;
+  p.pair_count = a.pair_count;
   {
     const char *e = getenv("DBSA_DEBUG_MODE");
     p.dbg = e ? atoi(e) : 0;

@@ -76,7 +76,7 @@ __global__ void lse_merge_kernel(DbsaMergeArgs a) {
 #pragma unroll
     for (int s = 0; s < kFast; ++s) {
       const float ws = __shfl_sync(0xffffffffu, wl, s);
-      if (s < g.n_splits) {
+      if (s < g.n_splits && ws != 0.f) {  // an empty split (LSE -inf) may hold garbage: 0 * NaN
 #pragma unroll
         for (int i = 0; i < 4; ++i) acc[i] += ws * v[s][i];
       }
@@ -128,20 +128,25 @@ __global__ void lse_merge_kernel(DbsaMergeArgs a) {
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
             const float wu = __shfl_sync(0xffffffffu, wl, k + u);
+            if (wu != 0.f) {
 #pragma unroll
-            for (int i = 0; i < 4; ++i) acc[i] += wu * v[u][i];
+              for (int i = 0; i < 4; ++i) acc[i] += wu * v[u][i];
+            }
           }
         }
         for (; k < cnt; ++k) {
           float v[4];
           load4<BF16>(a.part_o, (row0 + (int64_t)(s0 + k) * sstride) * hd + dl, v);
           const float wu = __shfl_sync(0xffffffffu, wl, k);
+          if (wu != 0.f) {
 #pragma unroll
-          for (int i = 0; i < 4; ++i) acc[i] += wu * v[i];
+            for (int i = 0; i < 4; ++i) acc[i] += wu * v[i];
+          }
         }
       } else {
         for (; k < cnt; ++k) {
           const float wu = __shfl_sync(0xffffffffu, wl, k);
+          if (wu == 0.f) continue;
           const int64_t off = (row0 + (int64_t)(s0 + k) * sstride) * hd + d;
           for (int i = 0; i < 4; ++i)
             if (d + i < hd) acc[i] += wu * load1<BF16>(a.part_o, off + i);
@@ -211,7 +216,7 @@ __global__ void lse_merge_bf16_h128_kernel(DbsaMergeArgs a) {
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const float wgt = __shfl_sync(full, wl, src0 + u);
-      if (c0 + u < n) {
+      if (c0 + u < n && wgt != 0.f) {  // skip empty splits (LSE -inf): their rows may be unwritten
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&v[u][i]));

@@ -418,10 +418,16 @@ def encode_groups_gen(dm, cache, new, ids, pattern, layers=None):
     """Stage 1 for groups `new` (BlockEntry list) whose concatenated token ids
     are `ids`, as a generator pausing after each layer's page write (see
     _decoder_gen).  Returns the attended pair count of these groups
-    (pipeline.py:231-232)."""
+    (pipeline.py:231-232) as COUNTED BY K1: layer 0's launch adds every
+    (row, key) pair that entered its softmax (DbsaAttnArgs.pair_count), all
+    heads; that total must equal n_heads x the plan's pair count
+    (masks.count_allowed_token_pairs, masks.py:111-123), else the kernel
+    visited a wrong tile set and this raises."""
     torch = _torch()
     c = dm.config
     plan = Stage1Plan(dm, cache, new, pattern)
+    n_layers = c.n_layers if layers is None else layers
+    counter = torch.zeros(1, dtype=torch.int64, device=dm.device) if n_layers > 1 else None
     store = cache.store
     qw, kw = c.n_heads * c.head_dim, c.n_kv_heads * c.head_dim
     stride = qw + 2 * kw
@@ -435,11 +441,16 @@ def encode_groups_gen(dm, cache, new, ids, pattern, layers=None):
         ops.attention(q=qkv, q_tok_stride=stride, tok_pos=plan.pos, tok_lo=None, rope=dm.rope,
                       pool=store.planes(), aux=None, n_heads=c.n_heads, n_kv_heads=c.n_kv_heads, head_dim=c.head_dim,
                       works_dev=plan.works, n_works=plan.n_works, segs_dev=plan.segs_ptr(layer), num_m=plan.num_m,
-                      out=out, out_tok_stride=qw)
+                      out=out, out_tok_stride=qw, pair_count=counter if layer == 0 else None)
 
     # only the pages are kept: the last layer's attention / O / FFN are skipped
     yield from _decoder_gen(dm, ids_dev, attend, write_kv, n_layers=layers, kv_only_last=True)
-    return plan.pairs
+    if counter is None:  # a one-layer model runs no attention in stage 1 (its output feeds nothing)
+        return plan.pairs
+    visited = int(counter.item())
+    if visited != plan.pairs * c.n_heads:
+        raise RuntimeError(f"K1 visited {visited} (row, key) pairs, expected n_heads x {plan.pairs}")
+    return visited // c.n_heads
 
 
 def encode_groups(dm, cache, new, ids, pattern, layers=None) -> int:
@@ -1031,7 +1042,9 @@ class ShardedStage2:
         R = self.nt.canon_rows
         self.R = R
         n_local = len(caches)
-        self.part_o = torch.empty((n_local, R, c.head_dim), dtype=torch.float32, device=dm.device)
+        # zero-filled: a shard with no chunk for a query writes no rows for it
+        # (LSE -inf, and K3m skips zero-weight splits), so its rows stay finite
+        self.part_o = torch.zeros((n_local, R, c.head_dim), dtype=torch.float32, device=dm.device)
         self.part_lse = torch.empty((n_local, R), dtype=torch.float32, device=dm.device)
 
     def forward(self):
@@ -1145,8 +1158,13 @@ def plan_key(plan, scorer):
 
 
 def fits_graph(graph, plan) -> bool:
-    """Whether `plan`'s chunk-major tables fit `graph`'s captured capacity."""
+    """Whether `plan` can replay `graph`: its chunk-major tables fit the
+    captured capacity, and the rope table it needs is the captured one (a
+    plan reaching past the table grows it, DeviceModel.rope_for, and the graph
+    must then be recaptured)."""
     sc, t = plan.sched, graph.plan.sched
+    if sc.rope is not t.rope:
+        return False
     if not isinstance(sc, ChunkMajorSchedule):
         return True
     return sc.n_real_works <= t.n_works and sc.n_real_segs <= t.n_segs

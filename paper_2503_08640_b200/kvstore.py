@@ -322,6 +322,10 @@ def serialize(cache: SegmentedKVCache, path) -> None:
         raise ValidationError("a group-sharded cache holds only part of the pool; serialize each owner's groups")
     store, dev = cache.store, cache.device
     total = cache.total_tokens
+    if total == 0:  # an empty cache is a header with an empty block table (kvstore.py:238-258)
+        with open(path, "wb") as fh:
+            fh.write(_header_bytes(cache))
+        return
     pos = torch.arange(total, dtype=torch.int32, device=dev)
     pages = engine._pages_for([(e.pos_start, e.token_count, e.row0) for e in cache.blocks])
     pdev = ops.to_device(pages, dev)
@@ -378,6 +382,10 @@ def deserialize(path, config: model.ModelConfig, device=None) -> SegmentedKVCach
                 raise FormatError(f"inconsistent block table entry {i}")
             expect_start = end
         cache = SegmentedKVCache(config, device, capacity_tokens=expect_start)
+        if expect_start == 0:  # empty cache: header only
+            if fh.read(1):
+                raise FormatError("trailing bytes after final segment")
+            return cache.seal()
         entries = cache._reserve([t[1] for t in table], [t[4] for t in table], [t[5] for t in table])
         total, per_tok = expect_start, config.n_kv_heads * config.head_dim
         dev = cache.device

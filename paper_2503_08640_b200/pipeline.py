@@ -288,6 +288,38 @@ class Stage2Session:
         works = c.n_kv_heads * (-(-e_total // slab) + keys + self_works)
         return works, keys + self_works
 
+    # Captured graphs per launch shape (engine.plan_key).  A shape is captured
+    # the second time it is seen (a one-off shape runs eagerly instead of paying
+    # a capture plus a private memory pool), and at most MAX_GRAPHS are kept,
+    # least recently used first out, so variable-length queries cannot grow
+    # the cache without bound.
+    MAX_GRAPHS = 8
+
+    def _graph_for(self, jobs, plan, scorer, before_capture=None):
+        """The captured graph for this plan's shape, or None to run it eagerly."""
+        from collections import OrderedDict
+
+        key = engine.plan_key(plan, scorer)
+        graphs = self.__dict__.setdefault("_graphs", OrderedDict())
+        seen = self.__dict__.setdefault("_seen", {})
+        g = graphs.get(key)
+        if g is not None and engine.fits_graph(g, plan):
+            graphs.move_to_end(key)
+            return g
+        seen[key] = seen.get(key, 0) + 1
+        if g is None and seen[key] < 2:
+            if len(seen) > 64 * self.MAX_GRAPHS:
+                seen.clear()
+            return None
+        if before_capture is not None:
+            before_capture()
+        graphs.pop(key, None)
+        graphs[key] = engine.GraphedStage2(self.dm, self.cache.store, jobs, plan, len(self.label_ids),
+                                           capacity=self._capacity(jobs))
+        while len(graphs) > self.MAX_GRAPHS:
+            graphs.popitem(last=False)
+        return graphs[key]
+
     def answer(self, scores, query_ids_list, graphed: bool = True):
         """K4 selection, planning and the scored forward of one batch.  With
         `graphed`, batches of a shape seen before replay a captured CUDA graph
@@ -298,12 +330,12 @@ class Stage2Session:
             s, best = self.run(jobs, plan)
             return ids, s, best
         scorer = engine.LabelScorer(self.dm, plan, jobs, len(self.label_ids))
-        key = engine.plan_key(plan, scorer)
-        graphs = self.__dict__.setdefault("_graphs", {})
-        if key not in graphs or not engine.fits_graph(graphs[key], plan):
-            graphs[key] = engine.GraphedStage2(self.dm, self.cache.store, jobs, plan, len(self.label_ids),
-                                               capacity=self._capacity(jobs))
-        s, best = graphs[key].replay(plan, scorer)
+        g = self._graph_for(jobs, plan, scorer)
+        if g is None:
+            _, h = engine.run_jobs(self.dm, self.cache.store, jobs, plan=plan, keep=scorer.keep)
+            s, best = scorer(self.dm, h, subset=True)
+        else:
+            s, best = g.replay(plan, scorer)
         return ids, s, best
 
     def answer_stream(self, batches):
@@ -318,15 +350,20 @@ class Stage2Session:
 
         main = torch.cuda.current_stream(self.dm.device)
         side = torch.cuda.Stream(self.dm.device)
-        side.wait_stream(main)
 
         def select_async(batch):
             scores, q_ids = batch
+            # device scores may come from work queued on the main stream (e.g.
+            # score_matrix_device inside the generator): order K4 after it, and
+            # keep the allocator from recycling the block while K4 reads it
+            side.wait_stream(main)
             with torch.cuda.stream(side):
                 if not isinstance(scores, torch.Tensor):
                     scores = torch.from_numpy(np.ascontiguousarray(scores)).pin_memory()
-                ids_dev = engine.ops.topk_select(scores.to(self.dm.device, non_blocking=True), self.budget,
-                                                 self.ordering)
+                sc_dev = scores.to(self.dm.device, non_blocking=True)
+                if sc_dev.device.type == "cuda":
+                    sc_dev.record_stream(side)
+                ids_dev = engine.ops.topk_select(sc_dev, self.budget, self.ordering)
                 ids_host = torch.empty(ids_dev.shape, dtype=ids_dev.dtype, pin_memory=True)
                 ids_host.copy_(ids_dev, non_blocking=True)
                 ev = torch.cuda.Event()
@@ -343,15 +380,14 @@ class Stage2Session:
             ids = ids_host.numpy().astype(np.int64)
             jobs, plan = self.plan(ids, q_ids)
             scorer = engine.LabelScorer(self.dm, plan, jobs, len(self.label_ids))
-            key = engine.plan_key(plan, scorer)
-            graphs = self.__dict__.setdefault("_graphs", {})
-            if key not in graphs or not engine.fits_graph(graphs[key], plan):
-                main.synchronize()
-                graphs[key] = engine.GraphedStage2(self.dm, self.cache.store, jobs, plan, len(self.label_ids),
-                                                   capacity=self._capacity(jobs))
+            g = self._graph_for(jobs, plan, scorer, before_capture=main.synchronize)
             b = next(it, None)
             nxt = select_async(b) if b is not None else None  # ahead of this batch's replay
-            s_dev, best_dev = graphs[key].replay(plan, scorer)
+            if g is None:
+                _, h = engine.run_jobs(self.dm, self.cache.store, jobs, plan=plan, keep=scorer.keep)
+                s_dev, best_dev = scorer(self.dm, h, subset=True)
+            else:
+                s_dev, best_dev = g.replay(plan, scorer)
             s_host = torch.empty(s_dev.shape, dtype=s_dev.dtype, pin_memory=True)
             b_host = torch.empty(best_dev.shape, dtype=best_dev.dtype, pin_memory=True)
             s_host.copy_(s_dev, non_blocking=True)

@@ -13,7 +13,7 @@ Each fixture records, for one (model config, task, method config):
   and per test query: BM25 scores (retrieval.py:129-141), ordered unit ids
   (retrieval.py:352-388), assembled length, per-label scores
   (model.score_label, model.py:420-443) and the predicted label
-  (pipeline.py:369-384); plus forward_query logits of query 0
+  (pipeline.py:369-384); plus forward_query logits of the first 8 queries
   (model.py:400-411).
 """
 
@@ -93,9 +93,9 @@ def run_case(name: str, spec: dict) -> None:
         arrays[f"q{qi}_bm25"] = np.array(scores, np.float64)
         arrays[f"q{qi}_units"] = np.array(sel.unit_ids, np.int64)
         arrays[f"q{qi}_label_scores"] = np.array(lab_scores, np.float64)
-        if qi == 0:
+        if qi < 8:  # forward_query logits (model.py:400-411) of the first 8 queries
             seq = model.TokenSequence.at_offset(q_ids, asm.total_tokens)
-            arrays["q0_logits"] = model.forward_query(weights, asm, seq).astype(np.float32)
+            arrays[f"q{qi}_logits"] = model.forward_query(weights, asm, seq).astype(np.float32)
         queries.append(dict(query=test.query, answer=test.answer, predicted=label, assembled_tokens=asm.total_tokens,
                             attended_pairs=qm.attended_pairs))
     t_inf = time.perf_counter() - t1

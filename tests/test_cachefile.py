@@ -122,3 +122,18 @@ def test_deserialize_reference_file_into_pages_and_back(tmp_path):
     assert torch.equal(cache2.store.v[..., :n], cache.store.v[..., :n])
     dk = (cache2.store.k[:, :, :n].float() - cache.store.k[:, :, :n].float()).abs().max().item()
     assert dk < 2e-2, dk
+
+
+@pytest.mark.gpu
+def test_empty_cache_round_trip(tmp_path):
+    """An empty cache (no groups) writes a header-only file and reads back as a
+    sealed empty cache, as the reference's serialize/deserialize allow."""
+    meta = _meta()
+    cfg = _cfg(meta)
+    cache = P.SegmentedKVCache(cfg).seal()
+    out = tmp_path / "empty.dbsacache"
+    kvstore.serialize(cache, out)
+    raw = out.read_bytes()
+    assert len(raw) == kvstore.expected_file_size(cfg, [], [])
+    back = kvstore.deserialize(out, cfg)
+    assert back.sealed and back.n_blocks == 0 and back.total_tokens == 0

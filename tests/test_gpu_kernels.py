@@ -440,3 +440,205 @@ def test_lse_merge_large_vs_torch(n_splits, dtype):
     want = want.view(n_q, Hkv, n_tok, gs, hd).permute(0, 2, 1, 3, 4).reshape(n_q * n_tok, H * hd)
     err = float((out.double() - want).abs().max())
     assert err < 2e-2, err
+
+
+# ---------------------------------------------------------------- north-star shapes
+def _rope64_t(x, pos, theta):
+    """torch float64 paired-halves RoPE (model.py:222-239); x [..., T, hd], pos [T]."""
+    hd = x.shape[-1]
+    f = torch.from_numpy(ops.inv_freq(hd, theta)).to(x.device)
+    ang = pos.double()[:, None] * f[None, :]
+    c, s = torch.cos(ang), torch.sin(ang)
+    lo, hi = x[..., : hd // 2], x[..., hd // 2:]
+    return torch.cat([lo * c - hi * s, lo * s + hi * c], dim=-1)
+
+
+def _stage2_at_scale(H, Hkv, hd, theta, n_groups, group_tok, budget, n_queries, q_tok, labels, check, seed=0):
+    """One layer of K3 (chunk-major, bf16 partials) + K3m at a north-star
+    shape against float64 attention over the ASSEMBLED context: selected
+    groups' keys rotated at their new positions 0..T'-1 (kvstore.assemble,
+    kvstore.py:188-221), queries at their own positions T'+i, the query/label
+    tree mask (model.py:381-392), softmax in float64 (kernels.py:43-100)."""
+    import paper_2503_08640_b200 as P
+    from paper_2503_08640_b200 import engine
+
+    dev = torch.device("cuda", 0)
+    cfg = P.ModelConfig(d_model=H * hd, n_layers=1, n_heads=H, n_kv_heads=Hkv, head_dim=hd, ffn_dim=64,
+                        vocab_size=300, rope_theta=theta, max_seq_len=131072)
+    dm = _DM(cfg, dev)
+    cache = P.SegmentedKVCache(cfg, dev, capacity_tokens=n_groups * group_tok)
+    blocks = cache._reserve([group_tok] * n_groups, [b"\0" * 32] * n_groups, [()] * n_groups)
+    g = torch.Generator(device=dev).manual_seed(seed)
+    st = cache.store
+    st.k.normal_(generator=g)
+    st.v.normal_(generator=g)
+    for e in blocks:  # page tails stay zero, as K2w leaves them
+        tail = -(-e.token_count // ops.PAGE) * ops.PAGE
+        st.k[:, :, e.row0 + e.token_count:e.row0 + tail] = 0
+        st.v[..., e.row0 + e.token_count:e.row0 + tail] = 0
+    rng = np.random.default_rng(seed)
+    rows0 = np.array([e.row0 for e in blocks])
+    pos0 = np.array([e.pos_start for e in blocks])
+    jobs, picks = [], []
+    for qi in range(n_queries):
+        pick = np.concatenate([[0], np.sort(rng.choice(np.arange(1, n_groups), budget - 1, replace=False))])
+        ln = np.full(budget, group_tok)
+        new_start = np.cumsum(ln) - ln
+        tab = np.stack([rows0[pick], ln, new_start - pos0[pick]], axis=1)
+        q_ids = rng.integers(3, 200, q_tok).tolist()
+        labs = [rng.integers(3, 200, labels[1]).tolist() for _ in range(labels[0])]
+        jobs.append(engine.label_job(tab, int(ln.sum()), q_ids, labs))
+        picks.append(pick)
+    plan = engine.Stage2Plan(dm, jobs, schedule="chunk")
+    assert plan.sched.part_o.dtype == torch.bfloat16
+    nt = plan.new
+    qw, kw = H * hd, Hkv * hd
+    qkv = (torch.randn(nt.n_tok, qw + 2 * kw, generator=g, device=dev) * 0.5).to(torch.bfloat16)
+    ops.kv_write(qkv[:, qw:], qkv[:, qw + kw:], qw + 2 * kw, nt.pos, dm.rope, nt.pages, nt.n_pages, nt.k_aux,
+                 nt.v_aux, nt.aux_rows, 1, 0, Hkv, hd)
+    out = torch.zeros(nt.n_tok, qw, dtype=torch.bfloat16, device=dev)
+    plan.sched.launch(dm, nt, 0, qkv, out, st.planes())
+    ops.lse_merge(plan.sched.part_o, plan.sched.part_lse, plan.sched.merges, plan.sched.n_merge,
+                  plan.sched.max_rows, H, Hkv, hd, out, qw)
+    torch.cuda.synchronize()
+    gs = H // Hkv
+    scale = 1.0 / math.sqrt(hd)
+    worst = 0.0
+    for qi in check:
+        job, pick = jobs[qi], picks[qi]
+        t0, n = int(nt.tok0[qi]), nt.n_new[qi]
+        Tp = budget * group_tok
+        pos = torch.from_numpy(nt.pos_host[t0:t0 + n].astype(np.int64)).to(dev)
+        # assembled context: stored keys are R(p_orig) k; un-rotate, re-rotate at p_new
+        kc = torch.cat([st.k[0, :, r:r + group_tok, :hd] for r in rows0[pick]], dim=1).double()  # [Hkv, T', hd]
+        vc = torch.cat([st.v[0, :, :hd, r:r + group_tok] for r in rows0[pick]], dim=2).double().transpose(1, 2)
+        p_orig = torch.cat([torch.arange(pos0[b], pos0[b] + group_tok, device=dev) for b in pick])
+        k_pre = _rope64_t(kc, -p_orig, theta)
+        k_asm = _rope64_t(k_pre, torch.arange(Tp, device=dev), theta)
+        qn = qkv[t0:t0 + n, :qw].double().view(n, H, hd).transpose(0, 1)  # [H, n, hd]
+        kn = qkv[t0:t0 + n, qw:qw + kw].double().view(n, Hkv, hd).transpose(0, 1)
+        vn = qkv[t0:t0 + n, qw + kw:].double().view(n, Hkv, hd).transpose(0, 1)
+        qr = _rope64_t(qn, pos, theta)
+        kr = _rope64_t(kn, pos, theta)
+        lo = torch.as_tensor(np.asarray(job.lo), device=dev)
+        r_i = torch.arange(n, device=dev)[:, None]
+        k_i = torch.arange(n, device=dev)[None, :]
+        vis = (k_i <= r_i) & ((k_i < job.prefix) | (k_i >= lo[:, None]))
+        K = torch.cat([k_asm, kr], dim=1)  # [Hkv, T'+n, hd]
+        V = torch.cat([vc, vn], dim=1)
+        mask = torch.cat([torch.ones(n, Tp, dtype=torch.bool, device=dev), vis], dim=1)
+        for kv in range(Hkv):
+            q = qr[kv * gs:(kv + 1) * gs]  # [gs, n, hd]
+            s = (q @ K[kv].T) * scale
+            s = torch.where(mask[None], s, -torch.inf)
+            p_ = torch.softmax(s, dim=-1)
+            want = p_ @ V[kv]  # [gs, n, hd]
+            got = out[t0:t0 + n].view(n, H, hd)[:, kv * gs:(kv + 1) * gs].transpose(0, 1).double()
+            worst = max(worst, float((got - want).abs().max()))
+    return worst
+
+
+def test_k3_at_c3_shape_vs_float64():
+    """C3: Llama-3.1-8B heads (32 q / 8 kv, hd 128, theta 5e5), a 90k-token
+    pool of 60 x 1,500-token groups, 18 groups per query (T' = 27,000, so 211
+    key tiles per work stream and re-positioning deltas up to ~63k with rope
+    rows up to 90k), 64 queries of 32 tokens + 4 labels x 4 tokens."""
+    worst = _stage2_at_scale(32, 8, 128, 500000.0, 60, 1500, 18, 64, 32, (4, 4), check=[0, 17, 40, 63])
+    assert worst < 2e-2, worst
+
+
+def test_k3_at_c4_shape_vs_float64():
+    """C4: Llama-2-7B MHA (32 heads, Hkv 32, hd 128, theta 1e4), 7 groups of
+    4,096 tokens, 3 selected (T' = 12,288), 16 queries."""
+    worst = _stage2_at_scale(32, 32, 128, 10000.0, 7, 4096, 3, 16, 32, (4, 4), check=[0, 9, 15])
+    assert worst < 2e-2, worst
+
+
+def _stage1_at_scale(H, Hkv, hd, theta, lengths, j=2, check_groups=None, seed=7):
+    """One layer of K1 over whole groups (sink + prev-j + causal self,
+    masks.py:80-99, 164-177) at a north-star shape against float64 attention
+    over each group's allowed keys (torch on the GPU)."""
+    dev = torch.device("cuda", 0)
+    gs = H // Hkv
+    T = sum(lengths)
+    pos0 = np.concatenate([[0], np.cumsum(lengths)[:-1]]).astype(np.int64)
+    page0, p = [], 0
+    for n in lengths:
+        page0.append(p)
+        p += -(-n // ops.PAGE)
+    rows = p * ops.PAGE
+    hdp = ops.hd_pad(hd)
+    g = torch.Generator(device=dev).manual_seed(seed)
+    k_pre = torch.randn(T, Hkv, hd, generator=g, device=dev).to(torch.bfloat16)
+    v = torch.randn(T, Hkv, hd, generator=g, device=dev).to(torch.bfloat16)
+    q = torch.randn(T, H, hd, generator=g, device=dev).to(torch.bfloat16)
+    kp = torch.zeros(1, Hkv, rows, hdp, dtype=torch.bfloat16, device=dev)
+    vp = torch.zeros(1, Hkv, hdp, rows, dtype=torch.bfloat16, device=dev)
+    rope = ops.rope_table(T + 64, hd, theta, dev)
+    pages = []
+    for b, n in enumerate(lengths):
+        for i in range(0, n, ops.PAGE):
+            pages.append((int(pos0[b]) + i, min(ops.PAGE, n - i), page0[b] * ops.PAGE + i, 0))
+    pages = np.array(pages, dtype=np.int32).view(ops.PAGE_DTYPE).reshape(-1)
+    pos = torch.arange(T, dtype=torch.int32, device=dev)
+    ops.kv_write(k_pre.reshape(T, -1), v.reshape(T, -1), Hkv * hd, pos, rope, ops.to_device(pages, dev), len(pages),
+                 kp, vp, rows, 1, 0, Hkv, hd)
+    num_m = 2 if max(lengths) * gs > 128 else 1
+    slab = (128 * num_m) // gs
+    works, segs = [], []
+    ctx_of = []
+    for b, n in enumerate(lengths):
+        ctx = sorted({0} | set(range(max(0, b - j), b)) - {b}) if b > 0 else []
+        ctx_of.append(ctx)
+        for kv in range(Hkv):
+            for t0 in range(0, n, slab):
+                nt = min(slab, n - t0)
+                sb = len(segs)
+                for c in ctx:
+                    segs.append((0, 0, page0[c] * ops.PAGE, lengths[c], ops.nat.SEG_FULL, 0, 0, 0))
+                segs.append((0, 0, page0[b] * ops.PAGE, t0 + nt, ops.nat.SEG_SELF, 0, 0, 0))
+                works.append((int(pos0[b]) + t0, nt, int(pos0[b]), kv, sb, len(segs), 0, 0, 0))
+    wa = np.zeros(len(works), dtype=ops.WORK_DTYPE)
+    for i, name in enumerate(ops.WORK_DTYPE.names):
+        wa[name] = [w[i] for w in works]
+    sa = np.array(segs, dtype=np.int32).view(ops.SEG_DTYPE).reshape(-1)
+    out = torch.zeros(T, H, hd, dtype=torch.bfloat16, device=dev)
+    ops.attention(q=q, q_tok_stride=H * hd, tok_pos=pos, tok_lo=None, rope=rope, pool=(kp, vp, rows, 1), aux=None,
+                  n_heads=H, n_kv_heads=Hkv, head_dim=hd, works_dev=ops.to_device(wa, dev), n_works=len(wa),
+                  segs_dev=ops.to_device(sa, dev), num_m=num_m, out=out, out_tok_stride=H * hd)
+    torch.cuda.synchronize()
+    posd = torch.arange(T, device=dev)
+    kr = _rope64_t(k_pre.double().transpose(0, 1), posd, theta)  # [Hkv, T, hd]
+    qr = _rope64_t(q.double().transpose(0, 1), posd, theta)      # [H, T, hd]
+    vv = v.double().transpose(0, 1)
+    scale = 1.0 / math.sqrt(hd)
+    worst = 0.0
+    for b in (check_groups if check_groups is not None else range(len(lengths))):
+        n, s0 = lengths[b], int(pos0[b])
+        keys = torch.cat([torch.arange(pos0[c], pos0[c] + lengths[c], device=dev) for c in ctx_of[b]]
+                         + [torch.arange(s0, s0 + n, device=dev)])
+        n_ctx = keys.numel() - n
+        mask = torch.ones(n, keys.numel(), dtype=torch.bool, device=dev)
+        mask[:, n_ctx:] = torch.tril(torch.ones(n, n, dtype=torch.bool, device=dev))
+        for kv in range(Hkv):
+            qq = qr[kv * gs:(kv + 1) * gs, s0:s0 + n]
+            s = (qq @ kr[kv, keys].T) * scale
+            s = torch.where(mask[None], s, -torch.inf)
+            want = torch.softmax(s, dim=-1) @ vv[kv, keys]
+            got = out[s0:s0 + n, kv * gs:(kv + 1) * gs].transpose(0, 1).double()
+            worst = max(worst, float((got - want).abs().max()))
+    return worst
+
+
+def test_k1_at_c2_shape_vs_float64():
+    """C2: Llama-3.1-8B heads (32 / 8, hd 128, theta 5e5), 1,500-token groups,
+    sink + prev-2 + self (groups 3.. see 4,500 context keys + causal self)."""
+    worst = _stage1_at_scale(32, 8, 128, 500000.0, [1500] * 6, j=2, check_groups=[0, 1, 3, 5])
+    assert worst < 2e-2, worst
+
+
+def test_k1_at_c4_shape_vs_float64():
+    """C4: MHA (gs 1) with 4,096-token groups, theta 1e4 (8 heads keep the
+    float64 check quick; the per-head work is the C4 shape)."""
+    worst = _stage1_at_scale(8, 8, 128, 10000.0, [4096] * 3, j=2)
+    assert worst < 2e-2, worst

@@ -70,6 +70,5 @@ def test_stage2_group_sharded_cache_matches_unsharded(world):
     labels = [runner.labels[int(i)] for i in best.cpu().numpy()]
     for qi, q in enumerate(queries):
         ref = a[f"q{qi}_label_scores"]
-        srt = np.sort(ref)
-        if labels[qi] != q["predicted"]:
-            assert srt[-1] - srt[-2] < 0.05, f"query {qi} flipped"
+        assert np.abs(scores[qi] - ref).max() < 0.04
+        assert labels[qi] == q["predicted"], f"query {qi}: label differs from the reference"

@@ -8,9 +8,10 @@ fixtures do not store.  Gates (north star):
   * partition, block mask, attended pairs, selected unit ids: bit-exact;
   * K/V pages vs the reference's f32 cache: max-abs 3e-2 (bf16 storage);
   * forward_query logits: max-abs 2e-2 vs the reference's f32 logits;
-  * per-label scores: max-abs 0.1 (sum of ~6 bf16 log-probs); predicted
-    labels identical wherever the reference's top-2 margin exceeds 10x the
-    observed score error (near-tie guard; every C1 margin is reported).
+  * per-label scores: max-abs 0.04 (a sum of ~6 bf16 log-probs; the
+    measured worst is ~0.03 on the chunk-major bf16-partial path);
+  * predicted labels: identical, no exceptions (the smallest reference top-2
+    margin over the three cases is 0.043, m64ex; it is printed).
 """
 
 import numpy as np
@@ -26,7 +27,7 @@ from paper_2503_08640_b200 import engine, masks, pipeline, retrieval, tokenizer 
 
 LOGIT_TOL = 2e-2
 KV_TOL = 3e-2
-SCORE_TOL = 0.1
+SCORE_TOL = 0.04
 
 
 def _setup(name):
@@ -108,8 +109,7 @@ def test_stage2_runner_matches_reference(name):
             flips.append((qi, margin, err))
     print(f"{name}: max |score err| {worst:.4g}; min top-2 margin {min(margins):.4g}; flips {flips}")
     assert worst < SCORE_TOL, worst
-    for qi, margin, err in flips:
-        assert margin < 10 * max(err, 1e-3), f"query {qi} flipped with margin {margin} (err {err})"
+    assert not flips, f"predicted labels differ from the reference: {flips}"
 
 
 @pytest.mark.parametrize("schedule", ["query", "chunk"])
@@ -343,6 +343,88 @@ def test_stage2_orderings_and_extreme_ratios(ordering, ratio, schedule, monkeypa
         label, scores, units, n_ctx = O.infer(st["cfg"], st["weights"], st["kv"], st["index"], st["refs"],
                                               st["labels"], t, ratio, ordering)
         assert list(want.unit_ids) == units
-        if lab != label:
-            srt = np.sort(scores)
-            assert srt[-1] - srt[-2] < 0.05
+        srt = np.sort(scores)
+        assert lab == label, f"label differs from the oracle's (top-2 margin {srt[-1] - srt[-2]:.4g})"
+
+
+def _permuted_scores(scores, seed=1):
+    """Same batch shape, different selections: the non-anchor columns shuffled."""
+    rng = np.random.default_rng(seed)
+    out = scores.copy()
+    cols = np.arange(1, scores.shape[1])
+    out[:, cols] = scores[:, rng.permutation(cols)]
+    return out
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_benchmarked_path_graph_replay_vs_reference(name, monkeypatch):
+    """The path every bench number comes from: GPU BM25 -> K4 -> chunk-major
+    K3 with bf16 partials (DBSA_OUT_MAPPED row-map works) + K3m, the whole
+    forward + label scoring replayed from a captured CUDA graph
+    (engine.GraphedStage2).  The graph is captured on a batch with DIFFERENT
+    selections (same shape), then replayed with the real batch's tables copied
+    in.  Gates: unit ids bit-exact, label scores <= 0.04 from the reference's
+    float64 scores (model.score_label, model.py:420-443), predicted labels
+    identical (pipeline.py:369-384) with no near-tie exceptions."""
+    monkeypatch.setenv("DBSA_STAGE2_SCHEDULE", "chunk")
+    meta, a, w, task, mc, enc = _encoded(name)
+    runner = P.Runner(w, enc.cache, enc.index, task, mc)
+    sess = runner.session()
+    texts = [q["query"] for q in meta["queries"]]
+    q_ids = [tokenizer.encode(task.template.render_query(t)) for t in texts]
+    scores_dev = enc.index.score_matrix_device([retrieval.bm25_tokenize(t) for t in texts])
+    ids = sess.select(scores_dev)
+    for qi in range(len(texts)):
+        np.testing.assert_array_equal(ids[qi], a[f"q{qi}_units"])
+    jobs, plan = sess.plan(ids, q_ids)
+    assert isinstance(plan.sched, engine.ChunkMajorSchedule)
+    assert plan.sched.part_o.dtype == torch.bfloat16
+    other = sess.select(_permuted_scores(scores_dev.cpu().numpy()))
+    assert not np.array_equal(other, ids)
+    jobs_o, plan_o = sess.plan(other, q_ids)
+    graph = engine.GraphedStage2(sess.dm, sess.cache.store, jobs_o, plan_o, len(sess.label_ids),
+                                 capacity=sess._capacity(jobs))
+    scorer = engine.LabelScorer(sess.dm, plan, jobs, len(sess.label_ids))
+    assert engine.plan_key(plan, scorer) == graph.key and engine.fits_graph(graph, plan)
+    s_dev, best_dev = graph.replay(plan, scorer)
+    got = s_dev.double().cpu().numpy()
+    best = best_dev.cpu().numpy()
+    worst, margins = 0.0, []
+    for qi, q in enumerate(meta["queries"]):
+        ref = a[f"q{qi}_label_scores"]
+        worst = max(worst, float(np.abs(got[qi] - ref).max()))
+        srt = np.sort(ref)
+        margins.append(float(srt[-1] - srt[-2]))
+        assert runner.labels[int(best[qi])] == q["predicted"], (qi, got[qi], ref)
+    print(f"{name}: graph-replayed chunk-major path, max |score err| {worst:.4g}, min margin {min(margins):.4g}")
+    assert worst < SCORE_TOL, worst
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_batched_chunk_major_logits_vs_reference(name):
+    """forward_query (model.py:400-411) for the first 8 queries as ONE batch
+    through the chunk-major K3 (bf16 partials) + K3m: every row's logits
+    within 2e-2 of the reference's f32 logits."""
+    meta, a, w, task, mc, enc = _encoded(name)
+    runner = P.Runner(w, enc.cache, enc.index, task, mc)
+    sess = runner.session()
+    n_q = min(8, len(meta["queries"]))
+    ids = np.stack([a[f"q{qi}_units"] for qi in range(n_q)]).astype(np.int64)
+    tabs, n_ctx = sess.chunks_for(ids)
+    jobs = []
+    for qi in range(n_q):
+        q_ids = tokenizer.encode(task.template.render_query(meta["queries"][qi]["query"]))
+        n = len(q_ids)
+        jobs.append(engine.QueryJob(tabs[qi], int(n_ctx[qi]), list(q_ids), list(range(n)), [0] * n, n))
+    plan = engine.Stage2Plan(sess.dm, jobs, schedule="chunk")
+    assert plan.sched.part_o.dtype == torch.bfloat16
+    _, h = engine.run_jobs(sess.dm, sess.cache.store, jobs, plan=plan)
+    logits = engine._final_logits(sess.dm, h).cpu().numpy()
+    worst = 0.0
+    for qi in range(n_q):
+        t0, n = int(plan.new.tok0[qi]), plan.new.n_new[qi]
+        ref = a[f"q{qi}_logits"]
+        assert ref.shape == logits[t0:t0 + n].shape
+        worst = max(worst, float(np.abs(logits[t0:t0 + n] - ref).max()))
+    print(f"{name}: batched chunk-major logits max-abs error {worst:.4g}")
+    assert worst < LOGIT_TOL, worst

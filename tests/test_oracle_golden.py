@@ -63,14 +63,16 @@ def test_stage2_selection_scores_and_labels(name):
         assert label == q["predicted"]
 
 
-def test_forward_query_logits_c1():
-    meta, a = load("c1")
-    st = oracle_pool("c1")
-    q = meta["queries"][0]
-    units = list(a["q0_units"])
-    asm, n_ctx = O.assemble(st["cfg"], st["kv"], [st["refs"][u] for u in units])
-    got = O.forward_query(st["cfg"], st["weights"], asm, n_ctx, O.encode(O.QUERY_FMT.format(query=q["query"])))
-    assert np.abs(got - a["q0_logits"]).max() <= 1e-5
+@pytest.mark.parametrize("name", CASES)
+def test_forward_query_logits(name):
+    """forward_query logits of the first 8 queries (model.py:400-411)."""
+    meta, a = load(name)
+    st = oracle_pool(name)
+    for qi, q in enumerate(meta["queries"][:8]):
+        units = list(a[f"q{qi}_units"])
+        asm, n_ctx = O.assemble(st["cfg"], st["kv"], [st["refs"][u] for u in units])
+        got = O.forward_query(st["cfg"], st["weights"], asm, n_ctx, O.encode(O.QUERY_FMT.format(query=q["query"])))
+        assert np.abs(got - a[f"q{qi}_logits"]).max() <= 1e-5
 
 
 def test_known_answer_vectors():
