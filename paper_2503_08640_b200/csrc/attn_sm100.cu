@@ -67,7 +67,23 @@ __device__ long long g_wstamps[256 * 12];  // per work of CTA 0: m*4 + {softmax 
   do {                                                                         \
     if (blockIdx.x == 0 && (j) < 256) g_stamps[(j) * 12 + (slot)] = clock64(); \
   } while (0)
+// per-CTA globaltimer (ns) milestones of the last launch: 0 entry, 1 setup done,
+// 2 first Q staged (m0), 3 MMA saw the first K tile, 4 last O committed,
+// 5 / 6 last epilogue done (m0 / m1), 7 exit
+__device__ unsigned long long g_cta[1024 * 8];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define CSTAMP(slot)                                                    \
+  do {                                                                  \
+    if (blockIdx.x < 1024) g_cta[blockIdx.x * 8 + (slot)] = gtimer(); \
+  } while (0)
 #else
+#define CSTAMP(slot) \
+  do {               \
+  } while (0)
 #define STAMP(slot, j) \
   do {               \
   } while (0)
@@ -520,6 +536,7 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_works = p.n_works;
+  if (threadIdx.x == 0) CSTAMP(0);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::KST; ++s) {
@@ -550,6 +567,7 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
+  if (threadIdx.x == 0) CSTAMP(1);
   // The control warpgroup hands registers to the two softmax warpgroups; each
   // role's code sits inside the branch of its setmaxnreg so ptxas allocates
   // it under that budget.
@@ -681,6 +699,7 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
           const int t = jg + j;
           mbar_wait(&k_full[t % C::KST], (t / C::KST) & 1);
           tc_fence_after();
+          if (t == 0 && lane == 0) CSTAMP(3);
           for (int m = 0; m < NUM_M; ++m) {
             if (j > 0) {
               // P(m, j-1) ready (and S(m) free): accumulate it, then reuse S(m) for tile j
@@ -716,6 +735,7 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
           pv(m, t, false, 1);
           commit(&o_full[m]);
         }
+        if (lane == 0) CSTAMP(4);
         commit(&v_empty[t % C::VST]);
         jg += n_tiles;
       } else {
@@ -755,6 +775,7 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
       stage_q(p.works[blockIdx.x], false, 0);
       fence_proxy_async_smem();
       mbar_arrive(&q_full[m]);
+      if (m == 0 && trow == 0) CSTAMP(2);
     }
     for (int wi = blockIdx.x; wi < n_works; wi += gridDim.x, ++wk) {
       const DbsaAttnWork w = p.works[wi];
@@ -917,6 +938,7 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
       tc_fence_before();
       mbar_arrive(&o_free[m]);  // O(m) may be overwritten by the next work's first P.V
       if (trow == 0) WSTAMP(m * 4 + 3, wk);
+      if (trow == 0) CSTAMP(5 + m);
     }
     if (p.pair_count) flush_pair_count(p.pair_count, n_pairs);
   }
@@ -924,6 +946,7 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (threadIdx.x == 0) CSTAMP(7);
   if (warp == 2) tmem_dealloc(tbase, C::TMEM_COLS);
 }
 
@@ -1424,6 +1447,12 @@ static int launch_attn(const DbsaAttnArgs &a, const AttnParams &p, const CUtenso
 #ifdef DBSA_STAMPS
 extern "C" int dbsa_debug_stamps(long long *host, int n) {
   return cudaMemcpyFromSymbol(host, dbsa::g_stamps, sizeof(long long) * (n < 256 * 12 ? n : 256 * 12)) == cudaSuccess
+             ? 0
+             : DBSA_ERR_CUDA;
+}
+extern "C" int dbsa_debug_cta(unsigned long long *host, int n) {
+  return cudaMemcpyFromSymbol(host, dbsa::g_cta, sizeof(unsigned long long) * (n < 1024 * 8 ? n : 1024 * 8)) ==
+                 cudaSuccess
              ? 0
              : DBSA_ERR_CUDA;
 }

@@ -55,6 +55,23 @@ hbm = 6537.3
 
 def timeit(fn, reps):
     fn(); torch.cuda.synchronize()
+    if os.environ.get("KB_GRAPH"):  # back-to-back launches in one CUDA graph: no host launch gaps
+        n = 20
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                for _ in range(n):
+                    fn()
+        torch.cuda.current_stream().wait_stream(s)
+        g.replay(); torch.cuda.synchronize()
+        ts = []
+        for _ in range(max(reps, 3)):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(); g.replay(); b.record(); torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b) / n)
+        return float(np.median(ts))
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
     for a, b in ev:
         a.record(); fn(); b.record()
