@@ -51,6 +51,14 @@ CONFIGS = {
     "c4": dict(model=dict(d_model=4096, n_layers=32, n_heads=32, n_kv_heads=32, head_dim=128, ffn_dim=11008,
                           vocab_size=32000, rope_theta=10000.0, norm_eps=1e-5, max_seq_len=65536),
                n_groups=7, group_tok=4096, name="Llama-2-7B shape (MHA), 28,672-token pool (7 groups x 4096)"),
+    # C5: the cache is sharded by group, 42 groups x 1500 tokens per GPU (336 groups = 504k tokens at 8
+    # GPUs, weak scaling: the pool grows with N).  Pool positions run to 504k and the selected context
+    # (30 %) to 151k, past Llama-3.1's 131,072, so max_seq_len is raised (random init: a shape, not a
+    # checkpoint).  Every rank holds the replicated 70B weights (~143 GB) and its shard (~23 GB).
+    "c5": dict(model=dict(d_model=8192, n_layers=80, n_heads=64, n_kv_heads=8, head_dim=128, ffn_dim=28672,
+                          vocab_size=128256, rope_theta=500000.0, norm_eps=1e-5, max_seq_len=524288),
+               n_groups=42, group_tok=1500,
+               name="Llama-3.1-70B shape, group-sharded cache (42 groups x 1500 per GPU; 504k tokens at 8 GPUs)"),
 }
 CFG8B = CONFIGS["c3"]["model"]
 N_GROUPS, GROUP_TOK = 60, 1500
@@ -60,6 +68,9 @@ RATIO = 0.30
 
 def workload(cfg_key: str) -> str:
     """config.workload, identical in both arms (ours and --impl reference)."""
+    if cfg_key == "c5":
+        return (f"C5: {CONFIGS['c5']['name']}, {RATIO:.0%} retrieval of the global pool, query {Q_TOK} tok + "
+                f"{N_LABELS} labels x {LABEL_TOK} tok")
     budget = int(math.ceil(RATIO * N_GROUPS))
     return (f"{cfg_key.upper()}: {CONFIGS[cfg_key]['name']}, {RATIO:.0%} retrieval ({budget} groups, "
             f"T'={budget * GROUP_TOK}), query {Q_TOK} tok + {N_LABELS} labels x {LABEL_TOK} tok")
@@ -223,7 +234,7 @@ def run_ours(args):
     s1_times = []
     cache = None
     for it in range(2):
-        cache = P.SegmentedKVCache(cfg, dev, capacity_tokens=N_GROUPS * GROUP_TOK)
+        cache = P.SegmentedKVCache(cfg, dev, capacity_tokens=N_GROUPS * (-(-GROUP_TOK // 64) * 64))
         if it == 1:
             ops.attention = k1.wrap(orig_attn)
         torch.cuda.synchronize()
@@ -527,6 +538,178 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def run_c5(args):
+    """C5: Llama-3.1-70B shape over a group-sharded cache.
+    Every rank holds the replicated weights and its own 42 groups; stage 1
+    encodes them group-sharded (NCCL halo per layer); a stage-2 step answers
+    the SAME B queries on every rank: K4 selects 30 % of the global pool, each
+    rank runs the chunk-major K3 over its own chunks, per layer the per-rank
+    (O, LSE) are all-gathered and merged (engine.ShardedStage2), the whole
+    step replayed as one CUDA graph.  value = device ms per query (max over
+    ranks); the pool grows with N (weak scaling)."""
+    import hashlib
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2503_08640_b200 as P
+    from paper_2503_08640_b200 import engine, masks, ops, parallel
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        comm = parallel.DistComm()
+    else:
+        comm = parallel.LocalComm(1)
+    cfg = P.ModelConfig(**CFG8B)
+    dm = engine.DeviceModel.random(cfg, seed=0, device=dev)
+    n_groups = N_GROUPS * world
+    rng = np.random.default_rng(0)
+    pool = [rng.integers(3, cfg.vocab_size, size=GROUP_TOK).tolist() for _ in range(n_groups)]
+    blocks = [(ids, hashlib.sha256(np.asarray(ids, np.int64).tobytes()).digest(), ()) for ids in pool]
+    pattern = masks.AttentionPattern.sink_prev_self(2)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    caches, pairs, ranges = engine.encode_pool_sharded(dm, blocks, pattern, comm)
+    b.record()
+    torch.cuda.synchronize()
+    s1_ms = a.elapsed_time(b)
+    own = ranges[rank][1] - ranges[rank][0]
+    mem_weights, mem_cache = dm.nbytes(), sum(c.store.nbytes() for c in caches.values())
+
+    budget = int(math.ceil(RATIO * n_groups))
+    labels = label_ids()
+    B, K, W = args.batch, args.steps, args.warmup
+
+    def units_of(ids_row):
+        return [(int(g), 0, GROUP_TOK) for g in ids_row]
+
+    def make_step(seed):
+        r2 = np.random.default_rng(seed)  # same seed on every rank: the same queries everywhere
+        q = [r2.integers(3, cfg.vocab_size, size=Q_TOK).tolist() for _ in range(B)]
+        sc = r2.random((B, n_groups))
+        return q, sc
+
+    def plan_of(q, ids):
+        return engine.ShardedPlan(dm, caches, ranges, [units_of(r) for r in ids], q, labels, world)
+
+    steps = []
+    for s in range(W + K):
+        q, sc = make_step(5000 + s)
+        sc_dev = torch.from_numpy(sc).to(dev)
+        ids = ops.topk_select(sc_dev, budget, "in-order").cpu().numpy()
+        plan = plan_of(q, ids)
+        steps.append((q, sc_dev, plan, engine.LabelScorer(dm, plan.new, plan.jobs, len(labels))))
+    graph = engine.GraphedShardedStage2(dm, caches, comm, steps[0][2], len(labels))
+    for q, sc_dev, plan, scorer in steps[:W]:
+        ops.topk_select(sc_dev, budget, "in-order")
+        graph.replay(plan, scorer)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    n0 = ops.LAUNCHES
+    with Clocks(local) as clk:
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        for q, sc_dev, plan, scorer in steps[W:]:
+            ops.topk_select(sc_dev, budget, "in-order")
+            graph.replay(plan, scorer)
+        ev1.record()
+        torch.cuda.synchronize()
+    launches = ops.LAUNCHES - n0
+    dev_ms = ev0.elapsed_time(ev1)
+    # e2e: pinned host scores -> K4 -> ids D2H -> host planning -> graph replay -> labels D2H
+    host = []
+    for s in range(K):
+        q, sc = make_step(9000 + s)
+        host.append((q, torch.from_numpy(sc).pin_memory()))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    h2d = d2h = 0
+    for q, sc in host:
+        ids = ops.topk_select(sc.to(dev, non_blocking=True), budget, "in-order").cpu().numpy()
+        plan = plan_of(q, ids)
+        scorer = engine.LabelScorer(dm, plan.new, plan.jobs, len(labels))
+        if not graph.fits(plan):
+            graph = engine.GraphedShardedStage2(dm, caches, comm, plan, len(labels))
+        scores, best = graph.replay(plan, scorer)
+        best_h = best.cpu().numpy()
+        h2d += sc.numel() * 8 + B * Q_TOK * 8
+        d2h += ids.size * ids.itemsize + best_h.size * best_h.itemsize
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    # K3 (chunk-major, this rank's chunks) per launch, eager with events around each launch
+    k3 = KernelTimer()
+    orig = ops.attention
+    ops.attention = k3.wrap(orig)
+    engine.ShardedStage2(dm, caches, comm, ranges, plan=steps[W][2]).run()
+    torch.cuda.synchronize()
+    ops.attention = orig
+    k3_ms = k3.mean_ms()
+    if world > 1:
+        t = torch.tensor([dev_ms, e2e_ms, s1_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_ms, e2e_ms, s1_ms = (float(x) for x in t.tolist())
+    # this rank's K3 FLOPs per launch: 4 hd H x (keys each new token sees on this rank)
+    p0 = steps[W][2]
+    sc0 = p0.scheds[rank]
+    keys = sc0.kv_tokens * (Q_TOK + N_LABELS * (LABEL_TOK - 1))  # context keys x new tokens, this shard
+    if rank == 0:
+        keys += int(sum(k3_self_keys(j) for j in p0.jobs))
+    k3_flops = 4.0 * cfg.head_dim * cfg.n_heads * keys
+    hbm, tf_burst, tf_sus, peak_src = peaks()
+    k3_tf = k3_flops / (k3_ms / 1e3) / 1e12 if k3_ms else None
+    line = {
+        "metric": METRIC, "value": dev_ms / (B * K), "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": dev_ms / K, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic (random-init weights, uniform token ids, U(0,1) f64 retrieval scores)",
+        "config": {"workload": workload("c5"), "queries_per_step": B, "global_groups": n_groups,
+                   "groups_per_gpu": own, "selected_groups_per_query": budget,
+                   "parallelism": f"cache sharded by group over {world} GPU(s); per-layer (O, LSE) all-gather + K3m",
+                   "l2": "inputs larger than L2 (70B bf16 weights, KV shard)"},
+        "e2e": {"value": e2e_ms / (B * K), "unit": UNIT, "h2d_bytes_per_step": h2d // K,
+                "d2h_bytes_per_step": d2h // K},
+        "roofline": {"kernel": "dbsa_attn_kernel<128,2> (K3, chunk-major, this rank's chunks)", "bound": "tensor",
+                     "achieved": k3_tf, "peak": tf_sus, "unit": "TFLOP/s", "frac": k3_tf / tf_sus if k3_tf else None,
+                     "peak_kind": "sustained bf16", "flops_per_launch": k3_flops, "launch_ms": k3_ms,
+                     "share_of_step": k3_ms * cfg.n_layers / (dev_ms / K) if k3_ms else None,
+                     "traffic": traffic_for("k3", "c5"), "peak_source": peak_src},
+        "stage1": {"metric": "stage-1 pre-encode tok/s (this GPU's shard)", "value": own * GROUP_TOK / (s1_ms / 1e3),
+                   "unit": "tok/s", "ms": s1_ms, "pool_tokens_per_gpu": own * GROUP_TOK,
+                   "attended_pairs_local": int(sum(pairs.values())),
+                   "mode": f"group-sharded over {world} GPU(s), NCCL halo per layer" if world > 1 else "one shard"},
+        "memory_gb": {"weights": mem_weights / 1e9, "kv_shard": mem_cache / 1e9,
+                      "peak_allocated": torch.cuda.max_memory_allocated(dev) / 1e9,
+                      "device_total": torch.cuda.get_device_properties(dev).total_memory / 1e9},
+        "gpu_launches": launches, "clocks": clk.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def k3_self_keys(j) -> int:
+    """Visible self keys summed over a job's new tokens (query/label tree)."""
+    n = len(j.ids)
+    i = np.arange(n)
+    lo = np.asarray(j.lo, np.int64)
+    vis = np.where(i < j.prefix, i + 1, j.prefix + (i - np.maximum(lo, j.prefix) + 1))
+    return int(vis.sum())
+
+
 def k3_algorithmic_flops(jobs, cfg) -> float:
     """4 * hd * H * sum over the batch's new tokens of the keys each one sees:
     the query's T' selected context tokens plus its visible self keys under
@@ -711,6 +894,8 @@ def main():
         os.environ["DBSA_STAGE2_SCHEDULE"] = args.schedule
     if args.impl == "reference":
         run_reference(args)
+    elif args.config == "c5":
+        run_c5(args)
     else:
         run_ours(args)
 

@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define DBSA_ABI_VERSION 5
+#define DBSA_ABI_VERSION 6
 #define DBSA_PAGE_TOKENS 64
 
 /* Error codes -> reference exceptions (errors.py:4-29). */
@@ -165,6 +165,13 @@ typedef struct DbsaMergeArgs {
   int64_t split_stride; /* rows between split s and s+1 of a group; 0 = the group's `rows`
                            (a gathered [world][R] partial buffer uses R: the C5 shard merge) */
   int32_t part_bf16;
+  int32_t part_tok_layout; /* 1: partial rows are token-major like `out` -- row r of split s of a group is
+                              (q_tok0 + r / gs) * n_heads + kv_head * gs + r % gs + s * split_stride, and
+                              part_row0 is unused (the C5 per-layer gather of per-rank merged partials) */
+  float *out_lse;          /* optional: write a partial instead of the final output -- the merged O
+                              (normalised, bf16) into out and its natural-log LSE into
+                              out_lse[t * n_heads + head]; a row with no visible key gets O = 0 and
+                              LSE = -inf (the per-rank half of the C5 merge) */
 } DbsaMergeArgs;
 int dbsa_lse_merge(const DbsaMergeArgs *args, void *stream);
 

@@ -36,7 +36,7 @@ EXPORTED_SYMBOLS = (
     "dbsa_last_error",
 )
 
-ABI_VERSION = 5
+ABI_VERSION = 6
 OUT_BF16, OUT_PARTIAL, OUT_MAPPED = 0, 1, 2
 PAGE_TOKENS = 64
 SEG_FULL = 0
@@ -86,7 +86,7 @@ class MergeArgs(ctypes.Structure):
     _fields_ = [
         ("part_o", _vp), ("part_lse", _vp), ("groups", _vp), ("n_groups", _i32), ("max_rows", _i32),
         ("n_heads", _i32), ("n_kv_heads", _i32), ("head_dim", _i32), ("out", _vp), ("out_tok_stride", _i64),
-        ("split_stride", _i64), ("part_bf16", _i32),
+        ("split_stride", _i64), ("part_bf16", _i32), ("part_tok_layout", _i32), ("out_lse", _vp),
     ]
 
 

@@ -47,6 +47,16 @@ __device__ __forceinline__ float load1(const void *base, int64_t off) {
     return reinterpret_cast<const float *>(base)[off];
 }
 
+// Partial row of split 0, row r of group g (DbsaMergeArgs.part_tok_layout).
+__device__ __forceinline__ int64_t merge_row0(const DbsaMergeArgs &a, const DbsaMergeGroup &g, int r, int gs) {
+  return a.part_tok_layout ? (int64_t)(g.q_tok0 + r / gs) * a.n_heads + g.kv_head * gs + r % gs
+                           : g.part_row0 + r;
+}
+// Partial-out mode (DbsaMergeArgs.out_lse): the merged row's natural-log LSE.
+__device__ __forceinline__ void merge_store_lse(const DbsaMergeArgs &a, int t, int head, float mx, float tot) {
+  a.out_lse[(int64_t)t * a.n_heads + head] = tot > 0.f ? mx + __logf(tot) : -INFINITY;
+}
+
 template <bool BF16, bool LATENCY>
 __global__ void lse_merge_kernel(DbsaMergeArgs a) {
   const DbsaMergeGroup g = a.groups[blockIdx.y];
@@ -55,7 +65,7 @@ __global__ void lse_merge_kernel(DbsaMergeArgs a) {
   if (r >= g.rows) return;
   const int hd = a.head_dim, gs = a.n_heads / a.n_kv_heads;
   const int64_t sstride = a.split_stride > 0 ? a.split_stride : g.rows;
-  const int64_t row0 = g.part_row0 + r;
+  const int64_t row0 = merge_row0(a, g, r, gs);
   constexpr int kFast = 24;
   if (LATENCY && hd <= 128 && (hd & 3) == 0 && g.n_splits <= kFast) {
     // latency path (few rows, e.g. one query): every split's partial row is
@@ -81,6 +91,7 @@ __global__ void lse_merge_kernel(DbsaMergeArgs a) {
         for (int i = 0; i < 4; ++i) acc[i] += ws * v[s][i];
       }
     }
+    if (a.out_lse && lane == 0) merge_store_lse(a, g.q_tok0 + r / gs, g.kv_head * gs + r % gs, mx, tot);
     if (lane * 4 + 3 < hd) {
       const int t = g.q_tok0 + r / gs, head = g.kv_head * gs + r % gs;
       __nv_bfloat16 *dst =
@@ -106,6 +117,7 @@ __global__ void lse_merge_kernel(DbsaMergeArgs a) {
   tot = warp_sum(tot);
   const float inv = tot > 0.f ? 1.f / tot : 0.f;
   const int t = g.q_tok0 + r / gs, head = g.kv_head * gs + r % gs;
+  if (a.out_lse && lane == 0) merge_store_lse(a, t, head, mx, tot);
   __nv_bfloat16 *dst = reinterpret_cast<__nv_bfloat16 *>(a.out) + (int64_t)t * a.out_tok_stride + (int64_t)head * hd;
   const bool vec = (hd & 3) == 0;
   for (int d0 = 0; d0 < hd; d0 += 128) {
@@ -181,7 +193,7 @@ __global__ void lse_merge_bf16_h128_kernel(DbsaMergeArgs a) {
   const DbsaMergeGroup g = a.groups[blockIdx.y];
   const int gs = a.n_heads / a.n_kv_heads;
   const int64_t sstride = a.split_stride > 0 ? a.split_stride : g.rows;
-  const int64_t row0 = g.part_row0 + (live ? r : 0);
+  const int64_t row0 = merge_row0(a, g, live ? r : 0, gs);
   const int n = g.n_splits;
   const unsigned full = 0xffffffffu;
   float mx = -INFINITY;
@@ -228,6 +240,7 @@ __global__ void lse_merge_bf16_h128_kernel(DbsaMergeArgs a) {
   }
   if (live) {
     const int t = g.q_tok0 + r / gs, head = g.kv_head * gs + r % gs;
+    if (a.out_lse && ql == 0) merge_store_lse(a, t, head, mx, tot);
     __nv_bfloat16 *dst =
         reinterpret_cast<__nv_bfloat16 *>(a.out) + (int64_t)t * a.out_tok_stride + (int64_t)head * 128 + ql * 16;
     uint32_t w[8];

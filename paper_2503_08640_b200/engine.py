@@ -478,7 +478,8 @@ def encode_pool_sharded(dm, blocks, pattern, comm, device=None):
     caches, gens = {}, {}
     for r in comm.local_ranks:
         present = parallel.local_groups(pattern, ranges, r, n_blocks)
-        cache = SegmentedKVCache(c, device or dm.device, capacity_tokens=sum(counts[g] for g in present))
+        # page-rounded capacity: reserve() must not grow (a second buffer while the first lives)
+        cache = SegmentedKVCache(c, device or dm.device, capacity_tokens=sum(_round_page(counts[g]) for g in present))
         cache._reserve_subset(counts, [d for _, d, _ in blocks], [sp for _, _, sp in blocks], present)
         compute = sorted({0} | set(range(*ranges[r])))
         new = [cache.blocks[g] for g in compute]
@@ -707,14 +708,14 @@ class ChunkMajorSchedule:
     The RoPE re-positioning delta of (query, chunk) is folded into each map
     entry's rope row (tok_pos - delta)."""
 
-    def __init__(self, dm, jobs, nt: NewTokens, chunk_tables=None, num_m: int = 2):
+    def __init__(self, dm, jobs, nt: NewTokens, chunk_tables=None, num_m: int = 2, include_self: bool = True):
         torch = _torch()
         c = dm.config
         hd = c.head_dim
         tables = chunk_tables if chunk_tables is not None else [j.chunks for j in jobs]
         self.num_m = num_m
         t = chunk_major_tables(tables, nt.n_new, nt.pos_host, nt.aux_row0, [j.prefix for j in jobs], c.group_size,
-                               c.n_kv_heads, num_m)
+                               c.n_kv_heads, num_m, include_self=include_self)
         emap, works, segs, merges = t["row_map"], t["works"], t["segs"], t["merges"]
         self.kv_tokens = t["kv_tokens"]
         self.n_works, self.n_segs, self.n_merge = len(works), len(segs), len(merges)
@@ -754,11 +755,21 @@ class ChunkMajorSchedule:
     def part_lse(self):
         return self._partials()[1]
 
-    def pad_to(self, works_cap: int, segs_cap: int) -> None:
+    def pad_to(self, works_cap: int, segs_cap: int, rows_cap: int = 0, part_cap: int = 0) -> None:
         """Grow the device tables to fixed capacities (a captured graph's launch
         shape): extra works are empty (no segment, no row) and cost a CTA a
-        few barrier round trips; extra segments are never referenced."""
+        few barrier round trips; extra segments are never referenced.
+        rows_cap / part_cap: row-map entries and partial rows (a C5 shard's
+        share of a batch varies with how the selections fall on it)."""
         torch = _torch()
+        nb = rows_cap * ops.ROWMAP_DTYPE.itemsize  # the row map is a byte tensor
+        if nb > self.row_map.numel():
+            rm = torch.zeros(nb, dtype=torch.uint8, device=self.row_map.device)
+            rm[: self.row_map.numel()].copy_(self.row_map)
+            self.row_map = rm
+        if part_cap > self.part_rows:
+            self.part_rows = part_cap
+            self._part = None
         L = self.segs.numel() // (self.n_segs * ops.SEG_DTYPE.itemsize) if self.n_segs else 0
         if works_cap < self.n_real_works or segs_cap < self.n_real_segs:
             raise ValueError("capacity below the schedule's size")
@@ -779,7 +790,11 @@ class ChunkMajorSchedule:
         L = self.segs.numel() // (self.n_segs * ops.SEG_DTYPE.itemsize)
         ns = other.n_real_segs * ops.SEG_DTYPE.itemsize
         self.segs.view(L, -1)[:, :ns].copy_(other.segs.view(L, -1)[:, :ns], non_blocking=True)
-        self.row_map.copy_(other.row_map, non_blocking=True)
+        if other.part_rows > self.part_rows:
+            raise ValueError("schedule's partials exceed the captured capacity")
+        if other.row_map.numel() > self.row_map.numel():
+            raise ValueError("row map exceeds the captured capacity")
+        self.row_map[: other.row_map.numel()].copy_(other.row_map, non_blocking=True)
         self.merges.copy_(other.merges, non_blocking=True)
 
     def segs_ptr(self, layer: int) -> int:
@@ -797,11 +812,15 @@ class ChunkMajorSchedule:
                       part_lse=self.part_lse if part_lse is None else part_lse, row_map=self.row_map)
 
 
-def chunk_major_tables(tables, n_new, pos_host, aux_row0, prefixes, gs: int, hkv: int, num_m: int = 2) -> dict:
+def chunk_major_tables(tables, n_new, pos_host, aux_row0, prefixes, gs: int, hkv: int, num_m: int = 2,
+                       include_self: bool = True) -> dict:
     """Host tables of a chunk-major K3 launch (ChunkMajorSchedule), vectorised
     numpy: the row map, works (chunk works kv-major then balanced row slices,
     then each query's SELF works), segments (one FULL per distinct chunk, one
-    SELF per query slab) and the K3m merge groups."""
+    SELF per query slab) and the K3m merge groups.  include_self=False (a C5
+    shard that is not the self rank): no SELF works, so a query's splits are
+    its local chunks alone (possibly none: its merge then yields O = 0, LSE =
+    -inf)."""
     slab = (128 * num_m) // gs
     if slab < 1:
         raise ConfigError(f"group size {gs} exceeds the {128 * num_m} rows of one K3 work")
@@ -811,7 +830,7 @@ def chunk_major_tables(tables, n_new, pos_host, aux_row0, prefixes, gs: int, hkv
     tok0 = np.concatenate([[0], np.cumsum(n_new)[:-1]]).astype(np.int64)
     tabs = [np.asarray(t, dtype=np.int64).reshape(-1, 3) for t in tables]
     n_ch = np.array([len(t) for t in tabs], np.int64)
-    n_split = n_ch + 1
+    n_split = n_ch + int(include_self)
     tokbase = np.concatenate([[0], np.cumsum(n_split * n_new)])
     kv_rows = int(tokbase[-1]) * gs  # partial rows per kv head
     # ---- (query, chunk) pairs grouped by chunk (pool row, length), queries ascending
@@ -864,8 +883,8 @@ def chunk_major_tables(tables, n_new, pos_host, aux_row0, prefixes, gs: int, hkv
         cseg = np.zeros(0, dtype=ops.SEG_DTYPE)
         n_keys = 0
     # ---- SELF works (each query's own tokens, causal tree) into its last split
-    ks = -(-n_new // slab)
-    ssize = -(-n_new // ks)
+    ks = -(-n_new // slab) * int(include_self)
+    ssize = -(-n_new // np.maximum(ks, 1))
     sq = np.repeat(np.arange(n_jobs), ks)
     st0 = (np.arange(int(ks.sum())) - np.repeat(np.cumsum(ks) - ks, ks)) * ssize[sq]
     sn = np.minimum(ssize[sq], n_new[sq] - st0)
@@ -1003,79 +1022,166 @@ def shard_chunk_table(cache, units, ranges, rank):
     return np.asarray(rows, dtype=np.int64).reshape(-1, 3), new_start
 
 
-class ShardedStage2:
-    """C5 stage 2 over a group-sharded cache: per layer every rank computes
-    canonical (O, LSE) partials over its own chunks (rank `self_rank` also over
-    the new tokens), the partials are all-gathered and merged by K3m."""
+class ShardedPlan:
+    """Tables of one C5 batch over the local shards of a
+    group-sharded cache: every query's ordered units are split by owner with
+    GLOBAL new positions kept (shard_chunk_table), each local rank gets a
+    chunk-major K3 schedule over its own chunks (bf16 partials; only the self
+    rank also covers the queries' own tokens), a per-rank K3m merge turns a
+    rank's partials into one (O, LSE) per (token, head), and the final K3m
+    merges the gathered per-rank results: the single softmax over the
+    concatenated key set of kernels.py:52-56, split by owner."""
 
-    def __init__(self, dm, caches, comm, ranges, units_per_query, query_ids, labels, self_rank=0):
-        torch = _torch()
+    def __init__(self, dm, caches, ranges, units_per_query, query_ids, labels, world, self_rank=0):
         c = dm.config
-        self.dm, self.caches, self.comm, self.ranges = dm, caches, comm, ranges
-        any_cache = next(iter(caches.values()))
+        self.ranks = list(caches)
         tables = {r: [] for r in caches}
         jobs = []
         for q, units in zip(query_ids, units_per_query):
-            n_ctx = 0
+            n_ctx = sum(e - s0 for _, s0, e in units)
             for r in caches:
-                tab, n_ctx = shard_chunk_table(caches[r], units, ranges, r)
+                tab, _ = shard_chunk_table(caches[r], units, ranges, r)
                 tables[r].append(tab)
-            if not caches:
-                n_ctx = sum(e - s for _, s, e in units)
             jobs.append(label_job(np.zeros((0, 3), np.int64), n_ctx, q, labels))
-        del any_cache
         self.jobs = jobs
-        self.nt = NewTokens(dm, jobs)
-        self.scheds = {r: AttnSchedule(dm, jobs, self.nt, chunk_tables=tables[r], mode="canonical",
-                                       include_self=(r == self_rank)) for r in caches}
+        self.new = NewTokens(dm, jobs)
+        self.tok0, self.n_tok, self.num_m = self.new.tok0, self.new.n_tok, self.new.num_m
+        self.scheds = {r: ChunkMajorSchedule(dm, jobs, self.new, chunk_tables=tables[r],
+                                             include_self=(r == self_rank)) for r in caches}
+        self.kv_tokens = sum(sc.kv_tokens for sc in self.scheds.values())
+        # final merge: one group per (query, kv head), one split per rank
         gs, hkv = c.group_size, c.n_kv_heads
-        merges = []
-        for qi in range(len(jobs)):
-            q0 = int(self.nt.tok0[qi])
-            for si, (t0, ntk) in enumerate(self.nt.slabs[qi]):
-                rows = ntk * gs
-                for kv in range(hkv):
-                    merges.append((self.nt.part_base[qi][si] + kv * rows, rows, comm.world, q0 + t0, kv))
-        self.merges = ops.to_device(_merge_array(merges), dm.device)
-        self.n_merge = len(merges)
-        self.max_rows = max(m[1] for m in merges)
-        R = self.nt.canon_rows
-        self.R = R
-        n_local = len(caches)
-        # zero-filled: a shard with no chunk for a query writes no rows for it
-        # (LSE -inf, and K3m skips zero-weight splits), so its rows stay finite
-        self.part_o = torch.zeros((n_local, R, c.head_dim), dtype=torch.float32, device=dm.device)
-        self.part_lse = torch.empty((n_local, R), dtype=torch.float32, device=dm.device)
+        mg = np.zeros((len(jobs), hkv), dtype=ops.MERGE_DTYPE)
+        mg["rows"] = (np.asarray(self.new.n_new, np.int64) * gs)[:, None]
+        mg["n_splits"] = world
+        mg["q_tok0"] = self.new.tok0[:-1, None]
+        mg["kv_head"] = np.arange(hkv)[None, :]
+        self.merges = ops.to_device(mg.reshape(-1), dm.device)
+        self.n_merge = len(jobs) * hkv
+        self.max_rows = int(mg["rows"].max())
+        self.rope = dm.rope_for(max(sc.rope.shape[0] for sc in self.scheds.values()))
 
-    def forward(self):
+
+class ShardedStage2:
+    """C5 stage 2 over a group-sharded cache.  Per layer: each local rank runs
+    its chunk-major K3 and the per-rank K3m merge into (O bf16, LSE fp32) per
+    (token, head); the per-rank results are all-gathered (NCCL all-gather over
+    NVLink; LocalComm stacks logical shards) and the final K3m merges the
+    `world` splits in token layout into the attention output."""
+
+    def __init__(self, dm, caches, comm, ranges, units_per_query=None, query_ids=None, labels=None, self_rank=0,
+                 plan=None):
+        torch = _torch()
+        c = dm.config
+        self.dm, self.caches, self.comm, self.ranges = dm, caches, comm, ranges
+        self.plan = plan or ShardedPlan(dm, caches, ranges, units_per_query, query_ids, labels, comm.world,
+                                        self_rank)
+        n_local = len(caches)
+        n_tok = self.plan.new.n_tok
+        self.canon_o = torch.zeros((n_local, n_tok, c.n_heads * c.head_dim), dtype=torch.bfloat16, device=dm.device)
+        self.canon_lse = torch.zeros((n_local, n_tok, c.n_heads), dtype=torch.float32, device=dm.device)
+
+    @property
+    def jobs(self):
+        return self.plan.jobs
+
+    def run(self, keep=None):
+        """Forward of the batch; returns the fp32 final hidden states (the rows
+        `keep` only, when given)."""
         c = self.dm.config
-        nt = self.nt
+        plan = self.plan
+        nt = plan.new
         qw, kw = c.n_heads * c.head_dim, c.n_kv_heads * c.head_dim
         stride = qw + 2 * kw
-        ranks = list(self.caches)
+        ranks = plan.ranks
+        n_tok = nt.n_tok
 
         def write_kv(layer, qkv):
             ops.kv_write(qkv[:, qw:], qkv[:, qw + kw:], stride, nt.pos, self.dm.rope, nt.pages, nt.n_pages,
                          nt.k_aux, nt.v_aux, nt.aux_rows, 1, 0, c.n_kv_heads, c.head_dim)
 
         def attend(layer, qkv, out):
-            self.part_lse.fill_(-float("inf"))
             for i, r in enumerate(ranks):
-                self.scheds[r].launch(self.dm, nt, layer, qkv, out, self.caches[r].store.planes(),
-                                      part_o=self.part_o[i], part_lse=self.part_lse[i])
+                sc = plan.scheds[r]
+                sc.launch(self.dm, nt, layer, qkv, out, self.caches[r].store.planes())
+                ops.lse_merge(sc.part_o, sc.part_lse, sc.merges, sc.n_merge, sc.max_rows, c.n_heads,
+                              c.n_kv_heads, c.head_dim, self.canon_o[i], qw, out_lse=self.canon_lse[i])
             if len(ranks) == self.comm.world:
-                go, gl = self.part_o, self.part_lse  # all shards are local: already [world, R, ...]
+                go, gl = self.canon_o, self.canon_lse  # every shard is local: already [world, ...]
             else:
-                go = self.comm.all_gather([self.part_o[0]])
-                gl = self.comm.all_gather([self.part_lse[0]])
-            ops.lse_merge(go, gl, self.merges, self.n_merge, self.max_rows, c.n_heads, c.n_kv_heads, c.head_dim,
-                          out, qw, split_stride=self.R)
+                go = self.comm.all_gather([self.canon_o[0]])
+                gl = self.comm.all_gather([self.canon_lse[0]])
+            ops.lse_merge(go, gl, plan.merges, plan.n_merge, plan.max_rows, c.n_heads, c.n_kv_heads, c.head_dim,
+                          out, qw, split_stride=n_tok * c.n_heads, tok_layout=True)
 
-        return _decoder(self.dm, nt.ids, attend, write_kv)
+        return _decoder(self.dm, nt.ids, attend, write_kv, keep_last=keep)
+
+    def forward(self):
+        return self.run()
 
     def scores(self):
-        h = self.forward()
-        return LabelScorer(self.dm, self.nt, self.jobs, len(self.jobs[0].labels))(self.dm, h)
+        scorer = LabelScorer(self.dm, self.plan.new, self.plan.jobs, len(self.plan.jobs[0].labels))
+        h = self.run(keep=scorer.keep)
+        return scorer(self.dm, h, subset=True)
+
+
+class GraphedShardedStage2:
+    """One C5 batch step -- the sharded forward (per layer: K3 per local rank,
+    per-rank K3m, all-gather, final K3m) plus label scoring -- captured as one
+    CUDA graph, NCCL all-gathers included.  A shard's chunk-major tables vary
+    with how a batch's selections fall on it, so they are padded to
+    capacities (`headroom` over the template) and every later batch copies
+    its tables in and replays."""
+
+    def __init__(self, dm, caches, comm, plan, n_labels, headroom: float = 1.5):
+        torch = _torch()
+        self.dm, self.plan = dm, plan
+        for sc in plan.scheds.values():
+            h = lambda n: int(n * headroom) + 64  # noqa: E731
+            sc.pad_to(-(-h(sc.n_real_works) // 64) * 64, -(-h(sc.n_real_segs) // 16) * 16,
+                      rows_cap=h(sc.row_map.numel() // ops.ROWMAP_DTYPE.itemsize), part_cap=h(sc.part_rows))
+        self.runner = ShardedStage2(dm, caches, comm, None, plan=plan)
+        self.scorer = LabelScorer(dm, plan.new, plan.jobs, n_labels)
+        self._run()  # warm-up: workspaces, cuBLAS handles, NCCL communicator, kernel attributes
+        torch.cuda.current_stream(dm.device).synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        n0 = ops.LAUNCHES
+        with torch.cuda.graph(self.graph):
+            self.scores, self.best = self._run()
+        self.launches = ops.LAUNCHES - n0
+
+    def _run(self):
+        h = self.runner.run(keep=self.scorer.keep)
+        return self.scorer(self.dm, h, subset=True)
+
+    def fits(self, plan) -> bool:
+        t = self.plan
+        if plan.new.n_tok != t.new.n_tok or tuple(plan.new.n_new) != tuple(t.new.n_new) or plan.rope is not t.rope:
+            return False
+        for r, sc in plan.scheds.items():
+            c = t.scheds[r]
+            if (sc.n_real_works > c.n_works or sc.n_real_segs > c.n_segs or sc.part_rows > c.part_rows
+                    or sc.row_map.numel() > c.row_map.numel()):
+                return False
+        return True
+
+    def replay(self, plan, scorer):
+        """Copy `plan`'s tables into the captured buffers and replay."""
+        if not self.fits(plan):
+            raise ValueError("batch does not fit the captured sharded graph")
+        t = self.plan
+        if plan is not t:
+            for dst, src in [(t.new.pos, plan.new.pos), (t.new.lo, plan.new.lo), (t.new.ids, plan.new.ids),
+                             (t.new.pages, plan.new.pages), (t.merges, plan.merges),
+                             (self.scorer.rows, scorer.rows), (self.scorer.targets, scorer.targets),
+                             (self.scorer.owner, scorer.owner), (self.scorer.label_row0, scorer.label_row0),
+                             (self.scorer.keep, scorer.keep), (self.scorer.rows_in_keep, scorer.rows_in_keep)]:
+                dst.copy_(src, non_blocking=True)
+            for r, sc in plan.scheds.items():
+                t.scheds[r].copy_tables_from(sc)
+        self.graph.replay()
+        ops.LAUNCHES += self.launches
+        return self.scores, self.best
 
 
 class GraphedStage2:

@@ -142,11 +142,16 @@ def attention(*, q, q_tok_stride, tok_pos, tok_lo, rope, pool, aux, n_heads, n_k
 
 
 def lse_merge(part_o, part_lse, groups_dev, n_groups, max_rows, n_heads, n_kv_heads, head_dim, out,
-              out_tok_stride, split_stride=0):
+              out_tok_stride, split_stride=0, out_lse=None, tok_layout=False):
+    """K3m.  out_lse (fp32 [tokens, n_heads], device): write the merged partial
+    (bf16 O into `out`, its LSE into out_lse) instead of the final output;
+    tok_layout: the partials are token-major [split][tokens][n_heads][hd] (a
+    gathered set of out_lse-mode results, split_stride = tokens * n_heads)."""
     a = nat.MergeArgs(part_o=part_o.data_ptr(), part_lse=part_lse.data_ptr(), groups=groups_dev.data_ptr(),
                       n_groups=n_groups, max_rows=max_rows, n_heads=n_heads, n_kv_heads=n_kv_heads,
                       head_dim=head_dim, out=out.data_ptr(), out_tok_stride=out_tok_stride,
-                      split_stride=split_stride, part_bf16=int(part_o.element_size() == 2))
+                      split_stride=split_stride, part_bf16=int(part_o.element_size() == 2),
+                      part_tok_layout=int(bool(tok_layout)), out_lse=nat.ptr(out_lse))
     nat.check(nat.load_library().dbsa_lse_merge(ctypes.byref(a), nat.stream_handle()))
     _launched()
 

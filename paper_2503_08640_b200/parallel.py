@@ -139,7 +139,10 @@ class LocalComm:
 
 
 class DistComm:
-    """torch.distributed transport: one local rank per process."""
+    """torch.distributed transport: one local rank per process.  NCCL moves
+    device tensors directly over NVLink; under gloo (the CPU tests, and the
+    two-process test of the sharded paths on ONE GPU, where NCCL cannot run
+    two ranks on one device) device tensors are staged through host memory."""
 
     def __init__(self, group=None):
         import torch.distributed as dist
@@ -149,6 +152,7 @@ class DistComm:
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self.local_ranks = [self.rank]
+        self.host_staged = dist.get_backend(group) == "gloo"
         # a collective every rank joins, before any batched P2P (NCCL requirement)
         dist.barrier(group=group)
 
@@ -158,14 +162,20 @@ class DistComm:
         this rank.  Returns the received tensors."""
         ops = []
         for (src, dst, key), t in sorted(sends.items()):
-            ops.append(self.dist.P2POp(self.dist.isend, t.contiguous(), dst, self.group))
-        out = {}
+            t = t.contiguous()
+            ops.append(self.dist.P2POp(self.dist.isend, t.cpu() if self.host_staged else t, dst, self.group))
+        out, staged = {}, []
         for (src, dst, key), t in sorted((recv_like or {}).items()):
             out[(src, dst, key)] = t
-            ops.append(self.dist.P2POp(self.dist.irecv, t, src, self.group))
+            buf = t.cpu() if self.host_staged and t.is_cuda else t
+            if buf is not t:
+                staged.append((buf, t))
+            ops.append(self.dist.P2POp(self.dist.irecv, buf, src, self.group))
         if ops:
             for req in self.dist.batch_isend_irecv(ops):
                 req.wait()
+        for buf, t in staged:
+            t.copy_(buf)
         return out
 
     def all_gather(self, parts):
@@ -173,6 +183,10 @@ class DistComm:
 
         (part,) = parts
         part = part.contiguous()
+        if self.host_staged:
+            bufs = [torch.empty(part.shape, dtype=part.dtype) for _ in range(self.world)]
+            self.dist.all_gather(bufs, part.cpu(), group=self.group)
+            return torch.stack(bufs, 0).to(part.device)
         out = torch.empty((self.world * part.shape[0],) + tuple(part.shape[1:]), dtype=part.dtype,
                           device=part.device)
         self.dist.all_gather_into_tensor(out, part, group=self.group)

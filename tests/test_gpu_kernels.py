@@ -442,6 +442,64 @@ def test_lse_merge_large_vs_torch(n_splits, dtype):
     assert err < 2e-2, err
 
 
+@pytest.mark.parametrize("n_local", [1, 24])
+def test_lse_merge_two_level_equals_one_level(n_local):
+    """The C5 merge (engine.ShardedStage2): each of 3 "ranks" merges its own
+    splits into a bf16 (O, LSE) per (token, head) (out_lse mode; a rank with
+    no split for a row yields O = 0, LSE = -inf), and the token-layout merge
+    of the 3 results equals the single softmax over all splits
+    (kernels.py:52-56) within the bf16 tolerance."""
+    dev = torch.device("cuda", 0)
+    H, Hkv, hd = 32, 8, 128
+    gs = H // Hkv
+    n_q, n_tok = (4 if n_local == 1 else 12), 44  # 12 queries: the throughput kernel path
+    rows = n_tok * gs
+    world = 3
+    g = torch.Generator(device=dev).manual_seed(n_local)
+    n_groups = n_q * Hkv
+    T = n_q * n_tok
+    splits = [n_local, 0 if n_local > 1 else 1, n_local]  # rank 1 holds nothing for these queries (n_local > 1)
+    parts = []
+    canon_o = torch.zeros(world, T, H * hd, dtype=torch.bfloat16, device=dev)
+    canon_lse = torch.zeros(world, T, H, dtype=torch.float32, device=dev)
+    for r in range(world):
+        ns = splits[r]
+        po = torch.randn(max(1, n_groups * ns * rows), hd, generator=g, device=dev).to(torch.bfloat16)
+        pl = torch.randn(max(1, n_groups * ns * rows), generator=g, device=dev) * 3
+        grp = np.zeros(n_groups, dtype=ops.MERGE_DTYPE)
+        for q in range(n_q):
+            for kv in range(Hkv):
+                i = q * Hkv + kv
+                grp[i] = (i * ns * rows, rows, ns, q * n_tok, kv)
+        ops.lse_merge(po, pl, ops.to_device(grp, dev), n_groups, rows, H, Hkv, hd, canon_o[r], H * hd,
+                      out_lse=canon_lse[r])
+        parts.append((po[: n_groups * ns * rows].double().view(n_groups, ns, rows, hd),
+                      pl[: n_groups * ns * rows].double().view(n_groups, ns, rows)))
+    fin = np.zeros(n_groups, dtype=ops.MERGE_DTYPE)
+    for q in range(n_q):
+        for kv in range(Hkv):
+            fin[q * Hkv + kv] = (0, rows, world, q * n_tok, kv)
+    out = torch.zeros(T, H * hd, dtype=torch.bfloat16, device=dev)
+    ops.lse_merge(canon_o, canon_lse, ops.to_device(fin, dev), n_groups, rows, H, Hkv, hd, out, H * hd,
+                  split_stride=T * H, tok_layout=True)
+    torch.cuda.synchronize()
+    po = torch.cat([p[0] for p in parts], dim=1)
+    pl = torch.cat([p[1] for p in parts], dim=1)
+    lse = torch.logsumexp(pl, dim=1, keepdim=True)
+    w = torch.exp(pl - lse)
+    want = (w.unsqueeze(-1) * po).sum(1).view(n_q, Hkv, n_tok, gs, hd).permute(0, 2, 1, 3, 4).reshape(T, H * hd)
+    err = float((out.double() - want).abs().max())
+    # two bf16 roundings (the per-rank O, the output) of N(0, 1) partial values:
+    # 2 x 2^-9 relative each, with a 2x margin
+    tol = 4 * 2.0 ** -9 * float(want.abs().max()) + 1e-3
+    assert err < tol, (err, tol)
+    if n_local > 1:  # the empty rank's rows: O = 0, LSE = -inf
+        assert torch.all(canon_lse[1] == -float("inf")) and torch.all(canon_o[1] == 0)
+    # per-rank LSE = logsumexp of that rank's splits, token-major
+    l0 = torch.logsumexp(parts[0][1], dim=1).view(n_q, Hkv, n_tok, gs).permute(0, 2, 1, 3).reshape(T, H)
+    assert float((canon_lse[0].double() - l0).abs().max()) < 1e-4
+
+
 # ---------------------------------------------------------------- north-star shapes
 def _rope64_t(x, pos, theta):
     """torch float64 paired-halves RoPE (model.py:222-239); x [..., T, hd], pos [T]."""

@@ -63,9 +63,10 @@ def test_stage2_group_sharded_cache_matches_unsharded(world):
     jobs, plan = sess.plan(ids, q_ids)
     ref_scores, _ = sess.run(jobs, plan)
     ref_scores = ref_scores.double().cpu().numpy()
-    # two bf16 computations of the same scores (the unsharded batch runs chunk-major
-    # with bf16 partials, the shards split-KV with fp32 partials), each ~2e-2 from
-    # the reference's float64 (tools/precision_probe.py)
+    # two bf16 computations of the same scores (the unsharded batch merges its
+    # chunk-major bf16 partials once; the shards merge per rank into bf16 (O, LSE)
+    # and again across ranks), each ~2e-2 from the reference's float64
+    # (tools/precision_probe.py)
     assert np.abs(scores - ref_scores).max() < 4e-2, np.abs(scores - ref_scores).max()
     labels = [runner.labels[int(i)] for i in best.cpu().numpy()]
     for qi, q in enumerate(queries):
