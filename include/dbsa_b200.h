@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define DBSA_ABI_VERSION 6
+#define DBSA_ABI_VERSION 7
 #define DBSA_PAGE_TOKENS 64
 
 /* Error codes -> reference exceptions (errors.py:4-29). */
@@ -174,6 +174,28 @@ typedef struct DbsaMergeArgs {
                               LSE = -inf (the per-rank half of the C5 merge) */
 } DbsaMergeArgs;
 int dbsa_lse_merge(const DbsaMergeArgs *args, void *stream);
+
+/* Component K5: the fused label-scoring epilogue of stage 2 -- the reference's
+ * logits_from_hidden -> log_softmax_rows -> gather of the label token
+ * (model.py:393-397, 414-417, 441-443).  One tcgen05 GEMM pass over
+ * x @ lm_head, 256 vocab columns x 256 rows per tile with fp32 accumulators in
+ * TMEM, keeps a running (max, sum of exp) per row and tile; no logit reaches
+ * HBM.  A second launch folds each scored (row, target) pair's tiles into
+ * the row's LSE and subtracts it from the target logit (a dot product of the
+ * same bf16 operands with fp32 accumulation). */
+typedef struct DbsaLabelScoreArgs {
+  const void *x;              /* bf16 [rows, d]: final-normed hidden states of the scored rows */
+  int64_t rows;
+  int64_t d;                  /* model dim, a multiple of 8 */
+  const void *w;              /* bf16 [vocab, d]: lm_head, K-major (transposed from the reference's [d, vocab]) */
+  int64_t vocab;
+  void *workspace;            /* fp32 [ceil(vocab / 256)][ceil(rows / 128) * 128][2]: per-tile (max, sum) */
+  const int64_t *pair_row;    /* [n_pairs] row of x of each scored pair */
+  const int32_t *pair_target; /* [n_pairs] target token */
+  int64_t n_pairs;
+  float *out;                 /* fp32 [n_pairs]: log p(target | row) */
+} DbsaLabelScoreArgs;
+int dbsa_label_score(const DbsaLabelScoreArgs *args, void *stream);
 
 /* Component K2w: page write of one layer's K (rotated at tok_pos) and V
  * (transposed) for a set of 64-token pages.  Replaces the per-block copy of

@@ -31,12 +31,13 @@ EXPORTED_SYMBOLS = (
     "dbsa_silu_mul",
     "dbsa_label_logprob",
     "dbsa_label_reduce",
+    "dbsa_label_score",
     "dbsa_bm25_scores",
     "dbsa_abi_version",
     "dbsa_last_error",
 )
 
-ABI_VERSION = 6
+ABI_VERSION = 7
 OUT_BF16, OUT_PARTIAL, OUT_MAPPED = 0, 1, 2
 PAGE_TOKENS = 64
 SEG_FULL = 0
@@ -87,6 +88,13 @@ class MergeArgs(ctypes.Structure):
         ("part_o", _vp), ("part_lse", _vp), ("groups", _vp), ("n_groups", _i32), ("max_rows", _i32),
         ("n_heads", _i32), ("n_kv_heads", _i32), ("head_dim", _i32), ("out", _vp), ("out_tok_stride", _i64),
         ("split_stride", _i64), ("part_bf16", _i32), ("part_tok_layout", _i32), ("out_lse", _vp),
+    ]
+
+
+class LabelScoreArgs(ctypes.Structure):
+    _fields_ = [
+        ("x", _vp), ("rows", _i64), ("d", _i64), ("w", _vp), ("vocab", _i64), ("workspace", _vp),
+        ("pair_row", _vp), ("pair_target", _vp), ("n_pairs", _i64), ("out", _vp),
     ]
 
 
@@ -153,6 +161,7 @@ def load_library(path: Path | str | None = None) -> ctypes.CDLL:
         lib.dbsa_silu_mul.argtypes = [_vp, _vp, _i64, _i64, _vp]
         lib.dbsa_label_logprob.argtypes = [_vp, _i64, _i64, _vp, _vp, _vp]
         lib.dbsa_label_reduce.argtypes = [_vp, _vp, _i64, _i32, _vp, _vp, _vp]
+        lib.dbsa_label_score.argtypes = [ctypes.POINTER(LabelScoreArgs), _vp]
         lib.dbsa_bm25_scores.argtypes = [_vp, _i64, _i32, _vp, _vp, _vp, _i64, ctypes.c_double, _vp, _vp]
         for name in EXPORTED_SYMBOLS[:-2]:
             getattr(lib, name).restype = ctypes.c_int

@@ -71,16 +71,18 @@ def default_device(device=None):
 class DeviceModel:
     """Weights resident in HBM, laid out for the fused projections:
     wqkv = [wq | wk | wv] (d, (H + 2 Hkv) hd) and wgu = [w_gate | w_up]
-    (d, 2 ffn) as bf16 GEMM operands; embedding, norms and the residual
-    stream stay fp32 (the reference's f32 storage, kernels.py:1-7)."""
+    (d, 2 ffn) as bf16 GEMM operands; lm_head K-major as lm_head_t
+    (vocab, d), the B operand of K5 (the fused label scoring); embedding,
+    norms and the residual stream stay fp32 (the reference's f32 storage,
+    kernels.py:1-7)."""
 
-    def __init__(self, config, device, embed, layers, out_norm, lm_head):
+    def __init__(self, config, device, embed, layers, out_norm, lm_head=None, lm_head_t=None):
         self.config = config
         self.device = device
         self.embed = embed
         self.layers = layers
         self.out_norm = out_norm
-        self.lm_head = lm_head
+        self.lm_head_t = lm_head_t if lm_head_t is not None else lm_head.t().contiguous()
         self.rope = ops.rope_table(config.max_seq_len, config.head_dim, config.rope_theta, device)
         self.config_hash = config.hash_bytes()
 
@@ -102,7 +104,8 @@ class DeviceModel:
             layers.append(dict(attn_norm=f32(p + "attn_norm"), wqkv=bf(p + "wq", p + "wk", p + "wv"),
                                wo=bf(p + "wo"), ffn_norm=f32(p + "ffn_norm"), wgu=bf(p + "w_gate", p + "w_up"),
                                wdown=bf(p + "w_down")))
-        return cls(weights.config, device, f32("tok_embed"), layers, f32("out_norm"), bf("lm_head"))
+        lm_t = torch.from_numpy(np.ascontiguousarray(t["lm_head"].T)).to(device).to(torch.bfloat16)
+        return cls(weights.config, device, f32("tok_embed"), layers, f32("out_norm"), lm_head_t=lm_t)
 
     @classmethod
     def random(cls, config, seed: int = 0, device=None):
@@ -128,7 +131,12 @@ class DeviceModel:
                        wgu=u((c.d_model, 2 * c.ffn_dim), c.d_model), wdown=u((c.ffn_dim, c.d_model), c.ffn_dim))
                   for _ in range(c.n_layers)]
         embed = torch.empty((c.vocab_size, c.d_model), dtype=torch.float32, device=dev).uniform_(-0.1, 0.1, generator=g)
-        return cls(c, dev, embed, layers, ones(c.d_model), u((c.d_model, c.vocab_size), c.d_model))
+        return cls(c, dev, embed, layers, ones(c.d_model), lm_head_t=u((c.vocab_size, c.d_model), c.d_model))
+
+    @property
+    def lm_head(self):
+        """The reference's (d, vocab) lm_head, as a transposed view."""
+        return self.lm_head_t.t()
 
     def rope_for(self, rows: int):
         """Rope table covering positions [0, rows) (stage 2 reads rows
@@ -139,7 +147,7 @@ class DeviceModel:
         return self.rope
 
     def nbytes(self) -> int:
-        n = self.embed.numel() * 4 + self.lm_head.numel() * 2
+        n = self.embed.numel() * 4 + self.lm_head_t.numel() * 2
         for lw in self.layers:
             n += sum(v.numel() * v.element_size() for v in lw.values())
         return n
@@ -1319,9 +1327,11 @@ class LabelScorer:
         self.n_labels = n_labels
 
     def __call__(self, dm, h, subset: bool = False):
-        """h: all rows' final hidden states, or (subset) only the rows `keep`."""
-        logits = _final_logits(dm, h.index_select(0, self.rows_in_keep if subset else self.rows))
-        lp = ops.label_logprob(logits, self.targets)
+        """h: all rows' final hidden states, or (subset) only the rows `keep`.
+        K5 (ops.label_score) scores every (row, label token) pair straight from
+        the final-normed distinct rows: no logits in HBM."""
+        x = ops.rmsnorm(h if subset else h.index_select(0, self.keep), dm.out_norm, dm.config.norm_eps)
+        lp = ops.label_score(x, dm.lm_head_t, self.rows_in_keep, self.targets)
         return ops.label_reduce(lp, self.label_row0, self.n_out // self.n_labels, self.n_labels)
 
 

@@ -210,6 +210,32 @@ def label_logprob(logits, targets):
     return out
 
 
+def label_score_workspace_shape(rows: int, vocab: int) -> tuple[int, int, int]:
+    """fp32 [vocab tiles of 256][rows rounded up to 128][(max, sum)] of K5."""
+    return (-(-vocab // 256), -(-rows // 128) * 128, 2)
+
+
+def label_score(x, lm_head_t, pair_row, pair_target, workspace=None, out=None):
+    """K5 (dbsa_label_score): log p(target | row) of every scored pair, from the
+    final-normed rows x (bf16 [rows, d]) and the K-major lm_head (bf16
+    [vocab, d]), without materialising logits."""
+    import torch
+
+    rows, d = x.shape
+    vocab = lm_head_t.shape[0]
+    shape = label_score_workspace_shape(rows, vocab)
+    if workspace is None or tuple(workspace.shape) != shape:
+        workspace = torch.empty(shape, dtype=torch.float32, device=x.device)
+    n = pair_row.numel()
+    out = out if out is not None else torch.empty(n, dtype=torch.float32, device=x.device)
+    a = nat.LabelScoreArgs(x=x.data_ptr(), rows=rows, d=d, w=lm_head_t.data_ptr(), vocab=vocab,
+                           workspace=workspace.data_ptr(), pair_row=pair_row.data_ptr(),
+                           pair_target=pair_target.data_ptr(), n_pairs=n, out=out.data_ptr())
+    nat.check(nat.load_library().dbsa_label_score(ctypes.byref(a), nat.stream_handle()))
+    _launched(2)
+    return out
+
+
 def label_reduce(lp, label_row0, n_queries: int, n_labels: int):
     """Per-label sums of token log-probs and the first-max label per query."""
     import torch

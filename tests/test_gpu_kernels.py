@@ -700,3 +700,28 @@ def test_k1_at_c4_shape_vs_float64():
     float64 check quick; the per-head work is the C4 shape)."""
     worst = _stage1_at_scale(8, 8, 128, 10000.0, [4096] * 3, j=2)
     assert worst < 2e-2, worst
+
+
+# ---------------------------------------------------------------- K5 fused label scoring
+@pytest.mark.parametrize("rows,d,vocab", [(1, 64, 259), (5, 64, 259), (130, 512, 1000), (300, 200, 777),
+                                          (832, 4096, 128256)])
+def test_label_score_vs_float64(rows, d, vocab):
+    """K5 (dbsa_label_score): log_softmax(x @ lm_head)[row, target] for scored
+    (row, target) pairs without materialising logits, against float64 over
+    the same bf16 operands (model.py:393-397, 414-417, 441-443).  Shapes: the
+    C1 tokenizer vocab, a vocab that is not a multiple of the 256-column tile,
+    a d that is not a multiple of the 64-wide K slice, rows past one and two M
+    tiles, and the C3 batch (832 distinct scored rows, Llama-3 vocab)."""
+    dev = torch.device("cuda", 0)
+    g = torch.Generator(device=dev).manual_seed(rows + d)
+    x = (torch.randn(rows, d, generator=g, device=dev) * 2).to(torch.bfloat16)
+    w = (torch.rand(vocab, d, generator=g, device=dev) * 2 - 1).mul(3.0 / d ** 0.5).to(torch.bfloat16)
+    n_pairs = max(1, rows * 5 // 4)
+    pair_row = torch.randint(0, rows, (n_pairs,), generator=g, device=dev)
+    pair_tgt = torch.randint(0, vocab, (n_pairs,), generator=g, device=dev).to(torch.int32)
+    pair_tgt[0] = vocab - 1  # the last column of a partial vocab tile
+    lp = ops.label_score(x, w, pair_row, pair_tgt)
+    torch.cuda.synchronize()
+    ref = torch.log_softmax(x.double() @ w.double().T, dim=-1)[pair_row, pair_tgt.long()]
+    err = float((lp.double() - ref).abs().max())
+    assert err < 2e-3, err
