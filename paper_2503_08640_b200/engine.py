@@ -1154,7 +1154,9 @@ class GraphedShardedStage2:
         torch.cuda.current_stream(dm.device).synchronize()
         self.graph = torch.cuda.CUDAGraph()
         n0 = ops.LAUNCHES
-        with torch.cuda.graph(self.graph):
+        # a capture stream of its own and thread-local capture mode: other threads may keep
+        # launching (Runner.infer from a thread pool) while this one captures
+        with torch.cuda.graph(self.graph, stream=torch.cuda.Stream(dm.device), capture_error_mode="thread_local"):
             self.scores, self.best = self._run()
         self.launches = ops.LAUNCHES - n0
 
@@ -1225,7 +1227,9 @@ class GraphedStage2:
         torch.cuda.current_stream(dm.device).synchronize()
         self.graph = torch.cuda.CUDAGraph()
         n0 = ops.LAUNCHES
-        with torch.cuda.graph(self.graph):
+        # a capture stream of its own and thread-local capture mode: other threads may keep
+        # launching (Runner.infer from a thread pool) while this one captures
+        with torch.cuda.graph(self.graph, stream=torch.cuda.Stream(dm.device), capture_error_mode="thread_local"):
             self.scores, self.best = self._run()
         self.launches = ops.LAUNCHES - n0
 

@@ -314,8 +314,9 @@ class Stage2Session:
         if before_capture is not None:
             before_capture()
         graphs.pop(key, None)
-        graphs[key] = engine.GraphedStage2(self.dm, self.cache.store, jobs, plan, len(self.label_ids),
-                                           capacity=self._capacity(jobs))
+        with _CAPTURE_LOCK:  # one capture at a time per process (Runner.infer may run in threads)
+            graphs[key] = engine.GraphedStage2(self.dm, self.cache.store, jobs, plan, len(self.label_ids),
+                                               capacity=self._capacity(jobs))
         while len(graphs) > self.MAX_GRAPHS:
             graphs.popitem(last=False)
         return graphs[key]
@@ -403,10 +404,16 @@ class Stage2Session:
             yield pending[1:]
 
 
+_CAPTURE_LOCK = threading.Lock()
+
+
 class Runner:
     """Inference session over (weights, cache, index) (pipeline.py:322-446).
-    Read-only after prepare(); infer() may run from several threads (each
-    thread launches on its own current stream)."""
+    Read-only after prepare(); infer() may run from several threads, as the
+    reference's bench does (bench.py:147-150): every thread gets its own CUDA
+    stream and its own Stage2Session (whose captured graphs own their table
+    and output buffers), and the shared state -- weights, cache pages, the
+    index's device tables -- is built once, before any thread uses it."""
 
     def __init__(self, weights, cache, index, task: TaskSpec, config: MethodConfig):
         self.weights = weights
@@ -426,6 +433,55 @@ class Runner:
         self.label_ids = [tokenizer.encode(task.template.render_label(lab)) for lab in self.labels]
         self._full: kvstore.AssembledCache | None = None
         self._lock = threading.Lock()
+        self._tls = threading.local()
+        self._gpu_ready = False
+
+    def _thread_state(self):
+        """(Stage2Session, CUDA stream) of the calling thread (DBSA path)."""
+        import torch
+
+        st = self._tls
+        if not hasattr(st, "sess"):
+            if not self._gpu_ready:
+                with self._lock:
+                    if not self._gpu_ready:
+                        # shared device state, built once and complete before any thread reads it
+                        self.index.device_tables(self.dm.device)
+                        torch.cuda.synchronize(self.dm.device)
+                        self._gpu_ready = True
+            st.sess = self.session()
+            st.stream = torch.cuda.Stream(self.dm.device)
+        return st.sess, st.stream
+
+    def _infer_dbsa(self, query_text: str, query_ids, qm):
+        """The drop-in single-query DBSA call on the GPU: BM25 (csrc/bm25.cu,
+        bit-identical to the reference's f64 scores) -> K4 select + order
+        (csrc/topk.cu; retrieval.py:352-388) -> chunk table (assemble without a
+        copy) -> the scored forward, replayed as a captured CUDA graph once its
+        launch shape has been seen (Stage2Session._graph_for)."""
+        import torch
+
+        sess, stream = self._thread_state()
+        with torch.cuda.stream(stream):
+            t0 = time.perf_counter()
+            scores = self.index.score_matrix_device([retrieval.bm25_tokenize(query_text)], self.dm.device)
+            ids = sess.select(scores)
+            qm.retrieval_seconds = time.perf_counter() - t0
+            t0 = time.perf_counter()
+            jobs, plan = sess.plan(ids, [query_ids])
+            n_ctx = int(jobs[0].n_ctx)
+            qm.assembly_seconds = time.perf_counter() - t0
+            t0 = time.perf_counter()
+            scorer = engine.LabelScorer(self.dm, plan, jobs, len(self.label_ids))
+            g = sess._graph_for(jobs, plan, scorer, before_capture=stream.synchronize)
+            if g is None:
+                _, h = engine.run_jobs(self.dm, self.cache.store, jobs, plan=plan, keep=scorer.keep)
+                _, best = scorer(self.dm, h, subset=True)
+            else:
+                _, best = g.replay(plan, scorer)
+            label = self.labels[int(best.cpu()[0])]
+            qm.scoring_seconds = time.perf_counter() - t0
+        return label, n_ctx
 
     def prepare(self) -> None:
         if self.method == FIXED_ICL and self._full is None:
@@ -447,7 +503,6 @@ class Runner:
         return self.labels[best], scores
 
     def infer(self, query_text: str):
-        cfg = self.config
         qm = QueryMetrics()
         t_start = time.perf_counter()
         query_ids = tokenizer.encode(self.task.template.render_query(query_text))
@@ -461,16 +516,11 @@ class Runner:
             qm.assembly_seconds = time.perf_counter() - t0
             n_ctx = assembled.total_tokens
         else:
+            label, n_ctx = self._infer_dbsa(query_text, query_ids, qm)
+        if self.method != DBSA:
             t0 = time.perf_counter()
-            sel = retrieval.order(retrieval.select(self.index, query_text, cfg.ratio, cfg.granularity), cfg.ordering)
-            qm.retrieval_seconds = time.perf_counter() - t0
-            t0 = time.perf_counter()
-            assembled = kvstore.assemble(self.cache, sel)
-            qm.assembly_seconds = time.perf_counter() - t0
-            n_ctx = assembled.total_tokens
-        t0 = time.perf_counter()
-        label, _ = self._score(assembled, query_ids)
-        qm.scoring_seconds = time.perf_counter() - t0
+            label, _ = self._score(assembled, query_ids)
+            qm.scoring_seconds = time.perf_counter() - t0
         pairs, tokens = self._pairs(n_ctx, query_ids)
         qm.attended_pairs = pairs
         qm.attention_flops = flops_attention(pairs, self.dm.config, tokens)

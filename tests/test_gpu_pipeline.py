@@ -112,6 +112,31 @@ def test_stage2_runner_matches_reference(name):
     assert not flips, f"predicted labels differ from the reference: {flips}"
 
 
+@pytest.mark.parametrize("name", ["c1", "m64ex"])
+def test_runner_infer_from_threads_equals_serial(name):
+    """The reference runs Runner.infer concurrently from a ThreadPoolExecutor
+    (bench.py:147-150).  Four threads (each on its own stream, with its own
+    captured graphs) answering every golden query twice give the serial
+    labels, which are the reference's; the drop-in single-query call runs
+    GPU BM25 + K4 (ops.LAUNCHES counts them) and replays captured graphs."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from paper_2503_08640_b200 import ops
+
+    meta, a, w, task, mc, enc = _encoded(name)
+    runner = P.Runner(w, enc.cache, enc.index, task, mc)
+    queries = [q["query"] for q in meta["queries"]]
+    n0 = ops.LAUNCHES
+    serial = [runner.infer(q)[0] for q in queries]
+    assert ops.LAUNCHES > n0
+    assert serial == [q["predicted"] for q in meta["queries"]]
+    with ThreadPoolExecutor(4) as ex:
+        par = list(ex.map(lambda q: runner.infer(q)[0], queries * 2))
+    assert par == serial * 2
+    sess = runner._thread_state()[0]
+    assert len(sess.__dict__.get("_graphs", {})) >= 1  # the repeated batch-1 shape is replayed from a graph
+
+
 @pytest.mark.parametrize("schedule", ["query", "chunk"])
 @pytest.mark.parametrize("name", CASES)
 def test_stage2_batched_k4_path_matches_reference(name, schedule, monkeypatch):
