@@ -297,6 +297,25 @@ def test_topk_bit_exact(n_units, ordering):
             assert list(got[q]) == _py_select(list(scores[q]), budget, ordering)
 
 
+@pytest.mark.parametrize("n_units", [257, 3001, 40000])
+@pytest.mark.parametrize("ordering", ["in-order", "low-to-high", "reverse"])
+def test_topk_radix_bit_exact(n_units, ordering):
+    """K4 above 256 units (example granularity: thousands of demonstrations)
+    runs the radix select; bit-exact with the reference's sort
+    (retrieval.py:352-388) with ties, all-tied rows, +-0.0 and negative scores."""
+    rng = np.random.default_rng(n_units)
+    scores = rng.random((9, n_units)) * 20 - 5
+    scores[:, ::3] = np.round(scores[:, ::3], 0)  # many ties
+    scores[0] = 0.0                               # all tied
+    scores[1, ::2] = -0.0                         # -0.0 ties +0.0 (Python compares them equal)
+    dev_scores = torch.from_numpy(scores).cuda()
+    for ratio in (0.001, 0.3, 1.0):
+        budget = max(1, math.ceil(ratio * n_units))
+        got = ops.topk_select(dev_scores, budget, ordering).cpu().numpy()
+        for q in range(scores.shape[0]):
+            assert list(got[q]) == _py_select(list(scores[q]), budget, ordering), (q, budget)
+
+
 class _DM:
     """The attributes a stage-2 plan reads (config, device, rope tables)."""
 
