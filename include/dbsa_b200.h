@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define DBSA_ABI_VERSION 7
+#define DBSA_ABI_VERSION 8
 #define DBSA_PAGE_TOKENS 64
 
 /* Error codes -> reference exceptions (errors.py:4-29). */
@@ -140,6 +140,15 @@ typedef struct DbsaAttnArgs {
                                      pairs whose score entered its softmax, i.e. the unmasked entries of every
                                      tile it visited, over all heads.  For stage 1 this equals
                                      n_heads * masks.count_allowed_token_pairs (masks.py:111-123). */
+  const int32_t *cta_works; /* optional (NULL = round-robin): device [n_ctas + 1] prefix offsets; CTA b of the
+                               num_m == 2 kernel runs works [cta_works[b], cta_works[b+1]) in order, so the
+                               host can pack a latency launch (e.g. long chunk works one per CTA, the short
+                               SELF works together on the spare CTAs) */
+  int32_t n_ctas;           /* grid size when cta_works is set (<= the SM count) */
+  int32_t pdl_early_q;      /* 1: q and every table were complete before the stream predecessor kernel STARTED
+                               (e.g. the K/V page write that precedes each layer's attention); the launch is then
+                               a programmatic dependent launch that stages Q while the predecessor runs and waits
+                               for it only before its first K/V tile load.  0: plain stream order. */
 } DbsaAttnArgs;
 int dbsa_attention(const DbsaAttnArgs *args, void *stream);
 

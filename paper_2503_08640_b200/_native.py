@@ -37,7 +37,7 @@ EXPORTED_SYMBOLS = (
     "dbsa_last_error",
 )
 
-ABI_VERSION = 7
+ABI_VERSION = 8
 OUT_BF16, OUT_PARTIAL, OUT_MAPPED = 0, 1, 2
 PAGE_TOKENS = 64
 SEG_FULL = 0
@@ -71,7 +71,7 @@ class AttnArgs(ctypes.Structure):
         ("scale", _f32), ("num_m", _i32),
         ("works", _vp), ("n_works", _i32), ("segs", _vp),
         ("out", _vp), ("out_tok_stride", _i64), ("part_o", _vp), ("part_lse", _vp),
-        ("row_map", _vp), ("part_bf16", _i32), ("pair_count", _vp),
+        ("row_map", _vp), ("part_bf16", _i32), ("pair_count", _vp), ("cta_works", _vp), ("n_ctas", _i32), ("pdl_early_q", _i32),
     ]
 
 

@@ -49,6 +49,11 @@ constexpr int kBN = 128;  // keys per tile
 #ifndef DBSA_QSTAGE_BATCH
 #define DBSA_QSTAGE_BATCH 4
 #endif
+// experiment: the producer holds the K/V stream after the first K tile until
+// the first work's Q is staged
+#ifndef DBSA_QGATE
+#define DBSA_QGATE 0
+#endif
 #ifndef DBSA_RESCALE_LOG2
 #define DBSA_RESCALE_LOG2 8.f
 #endif
@@ -57,15 +62,18 @@ constexpr int kBN = 128;  // keys per tile
 // per-tile clock stamps of CTA 0 for the first 256 key tiles of the two-tile
 // kernel, read back with dbsa_debug_stamps.
 #ifdef DBSA_STAMPS
+#ifndef DBSA_STAMP_CTA
+#define DBSA_STAMP_CTA 0
+#endif
 __device__ long long g_stamps[256 * 12];
 __device__ long long g_wstamps[256 * 12];  // per work of CTA 0: m*4 + {softmax done, Q staged, O full, epilogue done}
 #define WSTAMP(slot, w)                                                       \
   do {                                                                        \
-    if (blockIdx.x == 0 && (w) < 256) g_wstamps[(w) * 12 + (slot)] = clock64(); \
+    if (blockIdx.x == DBSA_STAMP_CTA && (w) < 256) g_wstamps[(w) * 12 + (slot)] = clock64(); \
   } while (0)
 #define STAMP(slot, j)                                                         \
   do {                                                                         \
-    if (blockIdx.x == 0 && (j) < 256) g_stamps[(j) * 12 + (slot)] = clock64(); \
+    if (blockIdx.x == DBSA_STAMP_CTA && (j) < 256) g_stamps[(j) * 12 + (slot)] = clock64(); \
   } while (0)
 // per-CTA globaltimer (ns) milestones of the last launch: 0 entry, 1 setup done,
 // 2 first Q staged (m0), 3 MMA saw the first K tile, 4 last O committed,
@@ -133,10 +141,23 @@ struct AttnParams {
   float *part_lse;
   const DbsaRowMap *row_map;
   int part_bf16;  // out_mode DBSA_OUT_MAPPED works: q_tok0 indexes this map
+  int l2_prefetch;  // producer prefetches each segment's later tiles into L2 (split-KV / latency launches)
   int dbg;  // profiling switches (DBSA_DEBUG_MODE): 1 = skip softmax math, 2 = skip MMAs, 4 = skip TMA loads,
             // 8 = skip epilogue stores, 16 = skip Q staging (two-tile kernel)
   unsigned long long *pair_count;  // optional: (row, key) pairs that entered the softmax (all heads)
+  const int32_t *cta_works;        // optional: CTA b runs works [cta_works[b], cta_works[b+1])
+  int pdl_early;                   // DbsaAttnArgs.pdl_early_q: only the producer waits for the predecessor
 };
+
+// This CTA's works: [begin, end) with stride `step` (round-robin over the grid,
+// or the host-packed contiguous range of AttnParams.cta_works).
+struct WorkRange {
+  int begin, end, step;
+};
+__device__ __forceinline__ WorkRange cta_work_range(const AttnParams &p) {
+  if (p.cta_works) return {p.cta_works[blockIdx.x], p.cta_works[blockIdx.x + 1], 1};
+  return {(int)blockIdx.x, p.n_works, (int)gridDim.x};
+}
 
 // Pair counter (DbsaAttnArgs.pair_count): the unmasked entries of the S row a
 // thread just masked, i.e. exactly the keys its softmax takes in.
@@ -535,7 +556,7 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(p_half + NUM_M);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_works = p.n_works;
+  const WorkRange wr = cta_work_range(p);
   if (threadIdx.x == 0) CSTAMP(0);
 
   if (threadIdx.x == 0) {
@@ -568,6 +589,13 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
   if (threadIdx.x == 0) CSTAMP(1);
+  // Programmatic dependent launch: by default nothing runs past this point
+  // before the stream predecessor completed.  With pdl_early (q and the tables
+  // predate the predecessor, which writes only K/V pages) the softmax warps
+  // stage the first Q while it runs; the producer waits before its first TMA
+  // load, and since the CTA cannot exit before the producer, completion stays
+  // ordered behind the predecessor.
+  if (!p.pdl_early) pdl_wait();
   // The control warpgroup hands registers to the two softmax warpgroups; each
   // role's code sits inside the branch of its setmaxnreg so ptxas allocates
   // it under that budget.
@@ -576,6 +604,7 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
+      if (p.pdl_early) pdl_wait();
       // K(t) is issued one tile ahead of V(t - 1): QK needs K early, P.V needs V late.
       int kj = 0, vj = 0;
       int pend_src = 0, pend_layer = 0, pend_kv = 0, pend_row = -1;
@@ -594,16 +623,38 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
         }
         ++vj;
       };
-      for (int wi = blockIdx.x; wi < n_works; wi += gridDim.x) {
+      bool gated = !(DBSA_QGATE);
+      for (int wi = wr.begin; wi < wr.end; wi += wr.step) {
         const DbsaAttnWork w = p.works[wi];
         for (int si = w.seg_begin; si < w.seg_end; ++si) {
           const DbsaAttnSeg sg = p.segs[si];
           const int off = sg.row0 & 63;  // tiles start on 64-row page boundaries
           const int nt = (off + sg.n_tok + kBN - 1) / kBN;
           const CUtensorMap *tk = sg.src ? &tm_k1 : &tm_k0;
+          auto prefetch_seg = [&]() {
+            // split-KV (latency) schedules: the segment's later tiles go to L2 now,
+            // so the ring refills from L2 instead of waiting a DRAM round trip
+            if (!p.l2_prefetch || (p.dbg & 4)) return;
+            const CUtensorMap *tv = sg.src ? &tm_v1 : &tm_v0;
+            for (int tt = C::KST; tt < nt; ++tt) {
+              const int row = sg.row0 - off + tt * kBN;
+#pragma unroll
+              for (int a = 0; a < C::NATOM; ++a) tma_prefetch_l2_4d(tk, a * C::KATOM, row, w.kv_head, sg.layer);
+#pragma unroll
+              for (int a = 0; a < 2; ++a) tma_prefetch_l2_4d(tv, row + a * 64, 0, w.kv_head, sg.layer);
+            }
+          };
+          if (gated) prefetch_seg();
           for (int tt = 0; tt < nt; ++tt) {
             const int row = sg.row0 - off + tt * kBN;
             const int st = kj % C::KST;
+            if (!gated && kj == 1) {
+              // first work: let the softmax warps' Q loads through before the
+              // K/V stream fills the memory system
+              for (int m = 0; m < NUM_M; ++m) mbar_wait(&q_full[m], 0);
+              gated = true;
+              prefetch_seg();
+            }
             if (kj >= C::KST) mbar_wait(&k_empty[st], ((kj / C::KST) & 1) ^ 1);
             if (p.dbg & 4) {
               mbar_arrive(&k_full[st]);
@@ -672,7 +723,7 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
     int jg = 0;        // global tile counter (ring slots and per-tile barrier phases)
     int n_bound = 0;   // RoPE-shift boundaries seen (q_ready phases)
     int wk = 0;        // works done by this CTA (q_full / o_full / o_free phases)
-    for (int wi = blockIdx.x; wi < n_works; wi += gridDim.x, ++wk) {
+    for (int wi = wr.begin; wi < wr.end; wi += wr.step, ++wk) {
       const DbsaAttnWork w = p.works[wi];
       int n_tiles = 0;
       for (int si = w.seg_begin; si < w.seg_end; ++si)
@@ -771,13 +822,13 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
         load_q_row<HDP>(p, q_tile, trow, xq.valid, xq.t, xq.head, restage ? p.tok_pos[xq.t] - shift : xq.rope_row);
       }
     };
-    if (blockIdx.x < n_works) {  // stage Q of the first work
-      stage_q(p.works[blockIdx.x], false, 0);
+    if (wr.begin < wr.end) {  // stage Q of the first work
+      stage_q(p.works[wr.begin], false, 0);
       fence_proxy_async_smem();
       mbar_arrive(&q_full[m]);
       if (m == 0 && trow == 0) CSTAMP(2);
     }
-    for (int wi = blockIdx.x; wi < n_works; wi += gridDim.x, ++wk) {
+    for (int wi = wr.begin; wi < wr.end; wi += wr.step, ++wk) {
       const DbsaAttnWork w = p.works[wi];
       const RowRef xr = row_ref(p, w, r);
       const bool valid = xr.valid;
@@ -922,8 +973,8 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
       // could complete a second q_full phase before the first was observed.
       if (j == 0) mbar_wait(&o_full[m], wk & 1);
       if (trow == 0) WSTAMP(m * 4 + 0, wk);
-      const int wn = wi + gridDim.x;
-      if (wn < n_works) {
+      const int wn = wi + wr.step;
+      if (wn < wr.end) {
         stage_q(p.works[wn], false, 0);
         fence_proxy_async_smem();
         mbar_arrive(&q_full[m]);
@@ -1434,9 +1485,10 @@ static int launch_attn(const DbsaAttnArgs &a, const AttnParams &p, const CUtenso
     if (e != cudaSuccess) return set_error(DBSA_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
     attr_set = true;
   }
-  // persistent: one CTA per SM (1 CTA fits per SM), striding over the works
-  const int grid = a.n_works < num_sms() ? a.n_works : num_sms();
-  kern<<<grid, C::THREADS, C::SMEM, s>>>(maps[0], maps[1], maps[2], maps[3], p);
+  // persistent: one CTA per SM (1 CTA fits per SM), striding over the works or
+  // running the host-packed ranges of cta_works
+  const int grid = a.cta_works ? a.n_ctas : a.n_works < num_sms() ? a.n_works : num_sms();
+  launch_k(kern, dim3(grid), dim3(C::THREADS), C::SMEM, s, true, maps[0], maps[1], maps[2], maps[3], p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(DBSA_ERR_CUDA, "attention launch: %s", cudaGetErrorString(e));
   return DBSA_OK;
@@ -1511,9 +1563,16 @@ extern "C" int dbsa_attention(const DbsaAttnArgs *args, void *stream) {
   p.row_map = a.row_map;
   p.part_bf16 = a.part_bf16;
   p.pair_count = a.pair_count;
+  p.cta_works = a.cta_works;
+  p.pdl_early = a.pdl_early_q;
+  if (a.cta_works && (a.num_m != 2 || a.n_ctas <= 0 || a.n_ctas > num_sms()))
+    return set_error(DBSA_ERR_CONFIG, "cta_works needs num_m == 2 and 0 < n_ctas <= %d, got num_m %d n_ctas %d",
+                     num_sms(), a.num_m, a.n_ctas);
   {
     const char *e = getenv("DBSA_DEBUG_MODE");
     p.dbg = e ? atoi(e) : 0;
+    const char *f = getenv("DBSA_L2PF");
+    p.l2_prefetch = f ? atoi(f) : 0;
   }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   // num_m 1 runs the single-M-tile kernel (Q in TMEM, double-buffered S) unless

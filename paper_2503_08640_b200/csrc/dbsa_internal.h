@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
+#include <utility>
 
 namespace dbsa {
 
@@ -22,5 +24,43 @@ inline int check_launch(const char *what) {
   if (e != cudaSuccess) return set_error(6, "%s: %s", what, cudaGetErrorString(e));
   return 0;
 }
+
+// Programmatic dependent launch (PDL).  A kernel launched with pdl = true may
+// start while its stream predecessor is still running; it must execute
+// pdl_wait() before touching anything the predecessor writes (and every CTA
+// waits before it exits, so completion stays transitive along the stream).
+// pdl_trigger() in a predecessor lets its dependents launch before it exits.
+// Without the launch attribute pdl_wait() returns at once.  DBSA_PDL=0 turns
+// the attribute off (A/B).
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char *e = getenv("DBSA_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl,
+                            Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  if (pdl && pdl_enabled()) {
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+  }
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+#endif
 
 }  // namespace dbsa

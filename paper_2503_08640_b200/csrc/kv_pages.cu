@@ -22,6 +22,9 @@ namespace dbsa {
 // shared-memory [64 tokens][HDP] tile so both the loads (along d) and the V^T
 // stores (along the token axis) are 16 bytes wide.
 __global__ void kv_write_kernel(DbsaKvWriteArgs a) {
+  // the attention launch that follows (pdl_early_q) may start now: it stages
+  // Q meanwhile and waits for this grid before loading any K/V tile
+  pdl_trigger();
   __shared__ __align__(16) __nv_bfloat16 vt[DBSA_PAGE_TOKENS * 128];
   const DbsaPage pg = a.pages[blockIdx.x];
   const int head = blockIdx.y;

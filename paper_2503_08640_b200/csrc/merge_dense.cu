@@ -59,7 +59,8 @@ __device__ __forceinline__ void merge_store_lse(const DbsaMergeArgs &a, int t, i
 
 template <bool BF16, bool LATENCY>
 __global__ void lse_merge_kernel(DbsaMergeArgs a) {
-  const DbsaMergeGroup g = a.groups[blockIdx.y];
+  const DbsaMergeGroup g = a.groups[blockIdx.y];  // host-written table: read before the PDL wait
+  pdl_wait();
   const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (r >= g.rows) return;
@@ -186,6 +187,7 @@ __device__ __forceinline__ uint32_t pack2_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t *>(&v);
 }
 __global__ void lse_merge_bf16_h128_kernel(DbsaMergeArgs a) {
+  pdl_wait();
   // a quarter-warp (8 lanes) per row, 32-byte loads (16 dims per lane)
   const int qw = threadIdx.x >> 3, ql = threadIdx.x & 7;
   const int r = blockIdx.x * (blockDim.x >> 3) + qw;
@@ -261,7 +263,15 @@ __global__ void rmsnorm4_kernel(float *x, const float *delta, const float *w, __
   const int64_t row = blockIdx.x;
   float4 *xr = reinterpret_cast<float4 *>(x + row * dim);
   const int n4 = (int)(dim >> 2);
-  float4 v[VPT];
+  float4 v[VPT], ww[VPT];
+  // the weights are not written by the predecessor: their loads go out before
+  // the PDL wait and are in registers by the scale pass
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) {
+    const int i = threadIdx.x + k * blockDim.x;
+    if (i < n4) ww[k] = __ldg(reinterpret_cast<const float4 *>(w) + i);
+  }
+  pdl_wait();
   float ss = 0.f;
 #pragma unroll
   for (int k = 0; k < VPT; ++k) {
@@ -292,9 +302,8 @@ __global__ void rmsnorm4_kernel(float *x, const float *delta, const float *w, __
   for (int k = 0; k < VPT; ++k) {
     const int i = threadIdx.x + k * blockDim.x;
     if (i < n4) {
-      const float4 ww = reinterpret_cast<const float4 *>(w)[i];
-      __nv_bfloat162 lo = __floats2bfloat162_rn(v[k].x * inv * ww.x, v[k].y * inv * ww.y);
-      __nv_bfloat162 hi = __floats2bfloat162_rn(v[k].z * inv * ww.z, v[k].w * inv * ww.w);
+      __nv_bfloat162 lo = __floats2bfloat162_rn(v[k].x * inv * ww[k].x, v[k].y * inv * ww[k].y);
+      __nv_bfloat162 hi = __floats2bfloat162_rn(v[k].z * inv * ww[k].z, v[k].w * inv * ww[k].w);
       uint2 u;
       u.x = *reinterpret_cast<uint32_t *>(&lo);
       u.y = *reinterpret_cast<uint32_t *>(&hi);
@@ -306,6 +315,7 @@ __global__ void rmsnorm4_kernel(float *x, const float *delta, const float *w, __
 template <bool ADD>
 __global__ void rmsnorm_kernel(float *x, const float *delta, const float *w, __nv_bfloat16 *out, int64_t dim,
                                float eps) {
+  pdl_wait();
   const int64_t row = blockIdx.x;
   float *xr = x + row * dim;
   float ss = 0.f;
@@ -341,12 +351,12 @@ static int launch_rmsnorm(float *x, const float *delta, const float *weight, voi
   if (dim % 4 == 0 && al && dim <= 4 * 256 * 8) {
     const int n4 = (int)(dim / 4);
     if (n4 <= 256 * 4)
-      rmsnorm4_kernel<ADD, 4><<<(unsigned)rows, 256, 0, st>>>(x, delta, weight, o, dim, eps);
+      launch_k(rmsnorm4_kernel<ADD, 4>, dim3((unsigned)rows), dim3(256), 0, st, true, x, delta, weight, o, dim, eps);
     else
-      rmsnorm4_kernel<ADD, 8><<<(unsigned)rows, 256, 0, st>>>(x, delta, weight, o, dim, eps);
+      launch_k(rmsnorm4_kernel<ADD, 8>, dim3((unsigned)rows), dim3(256), 0, st, true, x, delta, weight, o, dim, eps);
   } else {
     const int threads = dim >= 1024 ? 256 : (dim >= 256 ? 128 : 64);
-    rmsnorm_kernel<ADD><<<(unsigned)rows, threads, 0, st>>>(x, delta, weight, o, dim, eps);
+    launch_k(rmsnorm_kernel<ADD>, dim3((unsigned)rows), dim3(threads), 0, st, true, x, delta, weight, o, dim, eps);
   }
   return check_launch("rmsnorm");
 }
@@ -354,6 +364,7 @@ static int launch_rmsnorm(float *x, const float *delta, const float *weight, voi
 // gate_up bf16 [rows, 2*ffn] (gate | up) -> silu(gate) * up (kernels.silu_gate, kernels.py:115-123).
 __device__ __forceinline__ float silu_f(float g) { return g / (1.f + __expf(-g)); }
 __global__ void silu_mul_kernel(const __nv_bfloat16 *gu, __nv_bfloat16 *out, int64_t rows, int64_t ffn) {
+  pdl_wait();
   const int64_t n = rows * ffn;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n; idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = idx / ffn, c = idx % ffn;
@@ -364,6 +375,7 @@ __global__ void silu_mul_kernel(const __nv_bfloat16 *gu, __nv_bfloat16 *out, int
 }
 // 8 columns per thread (16-byte loads of gate and up), one CTA row-strip per y.
 __global__ void silu_mul8_kernel(const uint4 *gu, uint4 *out, int64_t rows, int64_t ffn8) {
+  pdl_wait();
   for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
     const uint4 *gr = gu + r * 2 * ffn8;
     uint4 *orow = out + r * ffn8;
@@ -485,19 +497,19 @@ extern "C" int dbsa_lse_merge(const DbsaMergeArgs *args, void *stream) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const bool small = (int64_t)a.n_groups * a.max_rows <= 16384;
   if (a.part_bf16 && a.head_dim == 128 && !small) {
-    lse_merge_bf16_h128_kernel<<<dim3((a.max_rows + 15) / 16, a.n_groups), 128, 0, st>>>(a);
+    launch_k(lse_merge_bf16_h128_kernel, dim3((a.max_rows + 15) / 16, a.n_groups), dim3(128), 0, st, true, a);
     return check_launch("lse_merge");
   }
   if (a.part_bf16) {
     if (small)
-      lse_merge_kernel<true, true><<<grid, 128, 0, st>>>(a);
+      launch_k(lse_merge_kernel<true, true>, grid, dim3(128), 0, st, true, a);
     else
-      lse_merge_kernel<true, false><<<grid, 128, 0, st>>>(a);
+      launch_k(lse_merge_kernel<true, false>, grid, dim3(128), 0, st, true, a);
   } else {
     if (small)
-      lse_merge_kernel<false, true><<<grid, 128, 0, st>>>(a);
+      launch_k(lse_merge_kernel<false, true>, grid, dim3(128), 0, st, true, a);
     else
-      lse_merge_kernel<false, false><<<grid, 128, 0, st>>>(a);
+      launch_k(lse_merge_kernel<false, false>, grid, dim3(128), 0, st, true, a);
   }
   return check_launch("lse_merge");
 }
@@ -521,8 +533,8 @@ extern "C" int dbsa_silu_mul(const void *gate_up, void *out, int64_t rows, int64
     const int64_t ffn8 = ffn / 8;
     const int bx = (int)((ffn8 + 255) / 256);
     const int by = (int)(rows < 65535 ? rows : 65535);
-    silu_mul8_kernel<<<dim3(bx, by), 256, 0, st>>>(reinterpret_cast<const uint4 *>(gate_up),
-                                                     reinterpret_cast<uint4 *>(out), rows, ffn8);
+    launch_k(silu_mul8_kernel, dim3(bx, by), dim3(256), 0, st, true, reinterpret_cast<const uint4 *>(gate_up),
+             reinterpret_cast<uint4 *>(out), rows, ffn8);
     return check_launch("silu_mul");
   }
   const int64_t n = rows * ffn;

@@ -449,7 +449,7 @@ def encode_groups_gen(dm, cache, new, ids, pattern, layers=None):
         ops.attention(q=qkv, q_tok_stride=stride, tok_pos=plan.pos, tok_lo=None, rope=dm.rope,
                       pool=store.planes(), aux=None, n_heads=c.n_heads, n_kv_heads=c.n_kv_heads, head_dim=c.head_dim,
                       works_dev=plan.works, n_works=plan.n_works, segs_dev=plan.segs_ptr(layer), num_m=plan.num_m,
-                      out=out, out_tok_stride=qw, pair_count=counter if layer == 0 else None)
+                      out=out, out_tok_stride=qw, pair_count=counter if layer == 0 else None, after_kv_write=True)
 
     # only the pages are kept: the last layer's attention / O / FFN are skipped
     yield from _decoder_gen(dm, ids_dev, attend, write_kv, n_layers=layers, kv_only_last=True)
@@ -612,12 +612,20 @@ class AttnSchedule:
     """
 
     def __init__(self, dm, jobs, nt: NewTokens, chunk_tables=None, target_ctas=None, order="query",
-                 mode="split", include_self=True):
+                 mode="split", include_self=True, pack=None):
         torch = _torch()
         c = dm.config
         gs, hkv, hd = c.group_size, c.n_kv_heads, c.head_dim
         tables = chunk_tables if chunk_tables is not None else [j.chunks for j in jobs]
         target = target_ctas or 4 * 148
+        # pack: SELF becomes a split of its own and the works are packed onto the
+        # CTAs by cost (pack_works), instead of SELF riding on the last chunk
+        # split and round-robin placement (the one-wave tail of a latency launch)
+        if pack is None:
+            import os
+
+            pack = mode == "split" and nt.num_m == 2 and os.environ.get("DBSA_PACK", "1") != "0"
+        self.pack = pack
         segs, works, merges = [], [], []
         min_shift = 0
         part_rows = 0 if mode == "split" else nt.canon_rows
@@ -649,14 +657,17 @@ class AttnSchedule:
             n_split = max(1, min(len(ch), -(-target // max(1, len(jobs) * hkv * len(slabs)))))
             bounds = _split_bounds(ch[:, 1] if len(ch) else np.zeros(0, np.int64), n_split)
             split_ranges = []
-            for sp in range(n_split - 1):
+            own_self = self.pack and include_self and len(ch) > 0
+            for sp in range(n_split - 1 + own_self):
                 sb = len(segs)
                 segs += chunk_segs[bounds[sp]:bounds[sp + 1]]
                 split_ranges.append((sb, len(segs)))
+            n_split += own_self
             for t0, ntk in slabs:
                 rows = ntk * gs
                 last_sb = len(segs)
-                segs += chunk_segs[bounds[n_split - 1]:bounds[n_split]]
+                if not own_self:
+                    segs += chunk_segs[bounds[n_split - 1]:bounds[n_split]]
                 if include_self:
                     segs.append((1, 0, int(nt.aux_row0[qi]), t0 + ntk, SEG_SELF, 0))
                 last = (last_sb, len(segs))
@@ -673,6 +684,11 @@ class AttnSchedule:
             first_row = [segs[wk[4]][2] if wk[5] > wk[4] and segs[wk[4]][0] == 0 else 1 << 30 for wk in works]
             idx = sorted(range(len(works)), key=lambda i: (first_row[i], works[i][3]))
             works = [works[i] for i in idx]
+        self.cta_works, self.n_ctas = None, 0
+        if self.pack and works:
+            works, bounds_cta = pack_works(works, segs, _num_sms(dm.device))
+            self.n_ctas = len(bounds_cta) - 1
+            self.cta_works = ops.to_device(np.asarray(bounds_cta, dtype=np.int32), dm.device)
         self.kv_tokens = kv_tok
         self.n_works, self.n_segs, self.n_merge = len(works), len(segs), len(merges)
         dev = dm.device
@@ -697,7 +713,49 @@ class AttnSchedule:
                       pool=pool, aux=nt.aux(), n_heads=c.n_heads, n_kv_heads=c.n_kv_heads, head_dim=c.head_dim,
                       works_dev=self.works, n_works=self.n_works, segs_dev=self.segs_ptr(layer), num_m=nt.num_m,
                       out=out, out_tok_stride=qw, part_o=self.part_o if part_o is None else part_o,
-                      part_lse=self.part_lse if part_lse is None else part_lse)
+                      part_lse=self.part_lse if part_lse is None else part_lse, cta_works=self.cta_works,
+                      n_ctas=self.n_ctas, after_kv_write=True)
+
+
+# Cost model of pack_works, in key tiles: a CTA's first work pays the cold
+# start (first Q staging, first-tile and epilogue code fetch: ~15 tiles of
+# batch-1 K3 time, profiles/r02f_b1_tiles.txt), later works the warm work
+# boundary (Q staging, drain, epilogue: ~5 tiles).
+PACK_FIRST, PACK_NEXT = 15, 5
+
+
+def _seg_tiles(seg) -> int:
+    return (int(seg[2]) % PAGE + int(seg[3]) + 127) // 128
+
+
+def pack_works(works, segs, n_sms: int):
+    """Longest-processing-time packing of K3 works onto at most n_sms CTAs
+    under the PACK_FIRST / PACK_NEXT cost model.  Returns the works reordered
+    so each CTA's are contiguous (longest first) and the [n_ctas + 1] prefix
+    offsets (DbsaAttnArgs.cta_works)."""
+    import heapq
+
+    tiles = [sum(_seg_tiles(segs[i]) for i in range(w[4], w[5])) for w in works]
+    n_ctas = min(n_sms, len(works))
+    order = sorted(range(len(works)), key=lambda i: -tiles[i])
+    heap = [(0, b) for b in range(n_ctas)]  # (load, cta); empty CTAs first
+    per_cta = [[] for _ in range(n_ctas)]
+    for i in order:
+        # cheapest resulting load: an empty CTA costs PACK_FIRST, a busy one PACK_NEXT
+        load, b = heap[0]
+        cost = (PACK_NEXT if per_cta[b] else PACK_FIRST) + tiles[i]
+        heapq.heapreplace(heap, (load + cost, b))
+        per_cta[b].append(i)
+    out, bounds = [], [0]
+    for lst in per_cta:
+        out += [works[i] for i in lst]
+        bounds.append(len(out))
+    return out, bounds
+
+
+def _num_sms(device) -> int:
+    torch = _torch()
+    return torch.cuda.get_device_properties(device).multi_processor_count if device.type == "cuda" else 148
 
 
 class ChunkMajorSchedule:
@@ -817,7 +875,8 @@ class ChunkMajorSchedule:
                       pool=pool, aux=nt.aux(), n_heads=c.n_heads, n_kv_heads=c.n_kv_heads, head_dim=c.head_dim,
                       works_dev=self.works, n_works=self.n_works, segs_dev=self.segs_ptr(layer), num_m=self.num_m,
                       out=out, out_tok_stride=qw, part_o=self.part_o if part_o is None else part_o,
-                      part_lse=self.part_lse if part_lse is None else part_lse, row_map=self.row_map)
+                      part_lse=self.part_lse if part_lse is None else part_lse, row_map=self.row_map,
+                      after_kv_write=True)
 
 
 def chunk_major_tables(tables, n_new, pos_host, aux_row0, prefixes, gs: int, hkv: int, num_m: int = 2,
@@ -1251,6 +1310,8 @@ class GraphedStage2:
                 t.sched.copy_tables_from(n.sched)
             else:
                 pairs += [(t.sched.works, n.sched.works), (t.sched.segs, n.sched.segs)]
+                if t.sched.cta_works is not None:
+                    pairs.append((t.sched.cta_works, n.sched.cta_works))
                 if t.sched.merges is not None:
                     pairs.append((t.sched.merges, n.sched.merges))
             for dst, src in pairs:
@@ -1270,7 +1331,7 @@ def plan_key(plan, scorer):
     if isinstance(sc, ChunkMajorSchedule):
         tables = ("chunk", sc.row_map.numel(), sc.num_m)
     else:
-        tables = ("query", sc.n_works, sc.n_segs)
+        tables = ("query", sc.n_works, sc.n_segs, sc.n_ctas)
     return (plan.new.n_tok, tuple(plan.new.n_new), plan.new.n_pages, tables, sc.n_merge, sc.part_rows,
             int(scorer.rows.numel()), int(scorer.keep.numel()), scorer.n_out, plan.new.num_m)
 

@@ -121,10 +121,14 @@ def kv_read(k_planes, v_planes, rows, layers, layer, tok_pos, rope, pages_dev, n
 
 def attention(*, q, q_tok_stride, tok_pos, tok_lo, rope, pool, aux, n_heads, n_kv_heads, head_dim,
               works_dev, n_works, segs_dev, num_m, out, out_tok_stride, part_o=None, part_lse=None,
-              row_map=None, pair_count=None):
+              row_map=None, pair_count=None, cta_works=None, n_ctas=0, after_kv_write=False):
     """Launch K1/K3.  `pool` / `aux` are (k_planes, v_planes, rows, layers); `row_map`
     (ROWMAP_DTYPE, device) backs DBSA_OUT_MAPPED works; `pair_count` (int64 [1],
-    device) makes the kernel add the (row, key) pairs it unmasked, all heads."""
+    device) makes the kernel add the (row, key) pairs it unmasked, all heads;
+    `cta_works` (int32 [n_ctas + 1], device) assigns CTA b the works
+    [cta_works[b], cta_works[b+1]) (two-tile kernel only); after_kv_write: the
+    launch directly follows the layer's K2w page write, so Q staging may
+    overlap it (DbsaAttnArgs.pdl_early_q)."""
     kp, vp, prow, pl = pool
     ka, va, arow, al = aux if aux is not None else (None, None, 0, 0)
     a = nat.AttnArgs(
@@ -136,7 +140,8 @@ def attention(*, q, q_tok_stride, tok_pos, tok_lo, rope, pool, aux, n_heads, n_k
         scale=float(1.0 / math.sqrt(head_dim)), num_m=num_m, works=_p(works_dev),
         n_works=n_works, segs=_p(segs_dev), out=out.data_ptr(), out_tok_stride=out_tok_stride,
         part_o=nat.ptr(part_o), part_lse=nat.ptr(part_lse), row_map=nat.ptr(row_map),
-        part_bf16=int(part_o is not None and part_o.element_size() == 2), pair_count=nat.ptr(pair_count))
+        part_bf16=int(part_o is not None and part_o.element_size() == 2), pair_count=nat.ptr(pair_count),
+        cta_works=nat.ptr(cta_works), n_ctas=int(n_ctas), pdl_early_q=int(bool(after_kv_write)))
     nat.check(nat.load_library().dbsa_attention(ctypes.byref(a), nat.stream_handle()))
     _launched()
 
