@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define DBSA_ABI_VERSION 8
+#define DBSA_ABI_VERSION 9
 #define DBSA_PAGE_TOKENS 64
 
 /* Error codes -> reference exceptions (errors.py:4-29). */
@@ -198,7 +198,7 @@ typedef struct DbsaLabelScoreArgs {
   int64_t d;                  /* model dim, a multiple of 8 */
   const void *w;              /* bf16 [vocab, d]: lm_head, K-major (transposed from the reference's [d, vocab]) */
   int64_t vocab;
-  void *workspace;            /* fp32 [ceil(vocab / 256)][ceil(rows / 128) * 128][2]: per-tile (max, sum) */
+  void *workspace;            /* fp32 [ceil(vocab / 128)][ceil(rows / 128) * 128][2]: per-128-column (max, sum) */
   const int64_t *pair_row;    /* [n_pairs] row of x of each scored pair */
   const int32_t *pair_target; /* [n_pairs] target token */
   int64_t n_pairs;

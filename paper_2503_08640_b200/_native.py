@@ -37,7 +37,7 @@ EXPORTED_SYMBOLS = (
     "dbsa_last_error",
 )
 
-ABI_VERSION = 8
+ABI_VERSION = 9
 OUT_BF16, OUT_PARTIAL, OUT_MAPPED = 0, 1, 2
 PAGE_TOKENS = 64
 SEG_FULL = 0

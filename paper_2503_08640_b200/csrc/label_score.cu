@@ -11,10 +11,14 @@
 // accumulator.  A second small launch combines a row's per-tile partials into
 // its LSE and subtracts it from the target logit.
 //
-//   warp 0: TMA producer (x and lm_head K slices of 64, 128B swizzle, 3 stages)
+//   warp 0: TMA producer (x and lm_head K slices of 64, 128B swizzle)
 //   warp 1: MMA issuer (tcgen05.mma.cta_group::1.kind::f16, M128 N256 K16, SS)
 //   warp 2: TMEM allocator
-//   warps 4-11: epilogue, one warpgroup per M tile, one row per thread
+//   warps 4-11: epilogue, one warpgroup per accumulator slot, one row per thread
+// Batch-1 shapes (rows <= 128, one M tile) use the narrow form: N = 128 vocab
+// tiles (twice the works, a shorter last wave), a 6-deep ring of one-M-tile
+// stages, x loaded for its real rows only, and the two TMEM slots alternating
+// between works so one slot's epilogue overlaps the next work's MMAs.
 //
 // Work = (pair of M tiles, vocab tile), M-pair fastest, so the CTAs running
 // at the same time share vocab tiles and lm_head is read from HBM about once
@@ -32,36 +36,58 @@
 namespace dbsa {
 
 constexpr int kLsBK = 64;                          // K per stage: one 128-byte swizzle row of bf16
-constexpr int kLsBN = 256;                         // vocab columns per tile: one N = 256 MMA
-constexpr int kLsStages = 3;
 constexpr int kLsMBytes = 128 * kLsBK * 2;         // one M tile's K slice (16 KB)
 constexpr int kLsABytes = 2 * kLsMBytes;           // two M tiles
-constexpr int kLsBBytes = kLsBN * kLsBK * 2;       // 32 KB
-constexpr int kLsStageBytes = kLsABytes + kLsBBytes;  // 64 KB
-constexpr int kLsSmem = kLsStages * kLsStageBytes + 1024 + 1024;
+constexpr int kLsHalf = 128;                       // workspace granularity: one (max, sum) per 128 vocab columns
 constexpr int kLsThreads = 384;
+
+// BN vocab columns per tile (one N = BN MMA): 256 for batches, 128 when the
+// rows fit one M tile (batch 1), so the vocab splits into twice as many works
+// and the last wave of the persistent grid is shorter.  Deeper ring for BN 128.
+template <int BN, bool NARROW>
+struct LsCfg {
+  static constexpr int ABytes = NARROW ? kLsMBytes : kLsABytes;  // the narrow form has one M tile
+  static constexpr int BBytes = BN * kLsBK * 2;
+  static constexpr int StageBytes = ABytes + BBytes;
+  static constexpr int Stages = (200 * 1024) / StageBytes > 8 ? 8 : (200 * 1024) / StageBytes;
+  static constexpr int Smem = Stages * StageBytes + 1024 + 1024;
+};
 
 struct LsParams {
   int64_t rows, rows_pad, vocab;
-  int m_tiles, m_pairs, n_tiles, k_steps, n_work;
-  float2 *part;  // [n_tiles][rows_pad]: (max, sum of 2^(x - max)) of x = logit * log2(e)
+  int m_tiles, m_pairs, n_tiles, k_steps, n_work, x_box_rows;
+  float2 *part;  // [vocab / 128][rows_pad]: (max, sum of 2^(x - max)) of x = logit * log2(e)
 };
 
+// Accumulator slots: a work with two M tiles uses TMEM slots 0 and 1 (one per
+// M tile); a work with one M tile (batch 1, or the odd last tile) takes slot
+// 0 / 1 alternately, so the next work's MMAs run while the other epilogue
+// warpgroup drains the previous one.  Every role walks the same work list and
+// derives the same slots.
+struct LsSlots {
+  int n_single = 0;
+  __device__ __forceinline__ int first(int nm) {  // slot of M tile 0 of the next work (nm M tiles)
+    return nm == 2 ? 0 : (n_single++ & 1);
+  }
+};
+
+template <int BN, bool NARROW>
 __global__ void __launch_bounds__(kLsThreads, 1)
     label_lse_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w,
                      const LsParams p) {
+  using C = LsCfg<BN, NARROW>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + kLsStages * kLsStageBytes);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + C::Stages * C::StageBytes);
   uint64_t *full = bars;                   // [stages] K slice landed
-  uint64_t *empty = full + kLsStages;      // [stages] K slice consumed by the MMAs
-  uint64_t *acc_full = empty + kLsStages;  // [2] M tile's accumulator complete
-  uint64_t *acc_empty = acc_full + 2;      // [2] M tile's accumulator read by the epilogue
+  uint64_t *empty = full + C::Stages;      // [stages] K slice consumed by the MMAs
+  uint64_t *acc_full = empty + C::Stages;  // [2] accumulator slot complete
+  uint64_t *acc_empty = acc_full + 2;      // [2] accumulator slot read by the epilogue
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kLsStages; ++s) {
+    for (int s = 0; s < C::Stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -86,41 +112,46 @@ __global__ void __launch_bounds__(kLsThreads, 1)
       for (int wk = blockIdx.x; wk < p.n_work; wk += gridDim.x) {
         const int m0 = (wk % p.m_pairs) * 2, nt = wk / p.m_pairs;
         const int nm = min(2, p.m_tiles - m0);
-        const uint32_t bytes = nm * kLsMBytes + kLsBBytes;
+        // narrow: only the x box rows (p.x_box_rows, the real rows rounded to 16) are
+        // loaded; the stale rows below them in the A tile only feed accumulator rows the
+        // epilogue never stores (row r of D depends on row r of A alone)
+        const uint32_t bytes = nm * (uint32_t)p.x_box_rows * (kLsBK * 2) + C::BBytes;
         for (int k = 0; k < p.k_steps; ++k, ++it) {
-          const int s = it % kLsStages;
-          if (it >= kLsStages) mbar_wait(&empty[s], ((it / kLsStages) & 1) ^ 1);
-          uint8_t *st = smem + s * kLsStageBytes;
+          const int s = it % C::Stages;
+          if (it >= C::Stages) mbar_wait(&empty[s], ((it / C::Stages) & 1) ^ 1);
+          uint8_t *st = smem + s * C::StageBytes;
           mbar_arrive_expect_tx(&full[s], bytes);
           for (int m = 0; m < nm; ++m) tma_load_2d(st + m * kLsMBytes, &tm_x, &full[s], k * kLsBK, (m0 + m) * 128);
-          tma_load_2d(st + kLsABytes, &tm_w, &full[s], k * kLsBK, nt * kLsBN);
+          tma_load_2d(st + C::ABytes, &tm_w, &full[s], k * kLsBK, nt * BN);
         }
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    constexpr uint32_t idesc = umma_idesc_bf16(128, kLsBN);
+    constexpr uint32_t idesc = umma_idesc_bf16(128, BN);
     const bool leader = elect_one();
     int it = 0;
-    int cnt[2] = {0, 0};  // tiles accumulated per M tile (acc_full / acc_empty phases)
+    int cnt[2] = {0, 0};  // tiles accumulated per slot (acc_full / acc_empty phases)
+    LsSlots sl;
     for (int wk = blockIdx.x; wk < p.n_work; wk += gridDim.x) {
       const int m0 = (wk % p.m_pairs) * 2;
       const int nm = min(2, p.m_tiles - m0);
+      const int s0 = sl.first(nm);
       for (int m = 0; m < nm; ++m)
-        if (cnt[m] > 0) mbar_wait(&acc_empty[m], (cnt[m] - 1) & 1);  // the epilogue drained it
+        if (cnt[s0 + m] > 0) mbar_wait(&acc_empty[s0 + m], (cnt[s0 + m] - 1) & 1);  // the epilogue drained it
       tc_fence_after();
       for (int k = 0; k < p.k_steps; ++k, ++it) {
-        const int s = it % kLsStages;
-        mbar_wait(&full[s], (it / kLsStages) & 1);
+        const int s = it % C::Stages;
+        mbar_wait(&full[s], (it / C::Stages) & 1);
         tc_fence_after();
         if (leader) {
-          const uint32_t sa = smem_u32(smem + s * kLsStageBytes), sb = sa + kLsABytes;
+          const uint32_t sa = smem_u32(smem + s * C::StageBytes), sb = sa + C::ABytes;
 #pragma unroll
           for (int m = 0; m < 2; ++m) {
             if (m < nm) {
 #pragma unroll
               for (int kk = 0; kk < kLsBK / 16; ++kk)
-                umma_bf16_ss(tbase + m * kLsBN, umma_desc_kmajor(sa + m * kLsMBytes + kk * 32, 128),
+                umma_bf16_ss(tbase + (s0 + m) * 256, umma_desc_kmajor(sa + m * kLsMBytes + kk * 32, 128),
                              umma_desc_kmajor(sb + kk * 32, 128), idesc, (k | kk) != 0 ? 1u : 0u);
             }
           }
@@ -129,34 +160,39 @@ __global__ void __launch_bounds__(kLsThreads, 1)
         __syncwarp();
       }
       if (leader)
-        for (int m = 0; m < nm; ++m) umma_commit(&acc_full[m]);
+        for (int m = 0; m < nm; ++m) umma_commit(&acc_full[s0 + m]);
       __syncwarp();
-      for (int m = 0; m < nm; ++m) ++cnt[m];
+      for (int m = 0; m < nm; ++m) ++cnt[s0 + m];
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue: row LSE partials
-    const int m = (warp - 4) >> 2, q4 = warp & 3;
+    const int e = (warp - 4) >> 2, q4 = warp & 3;  // this warpgroup drains accumulator slot e
     const int trow = q4 * 32 + lane;
-    const uint32_t t_acc = tbase + ((uint32_t)(q4 * 32) << 16) + m * kLsBN;
+    const uint32_t t_acc = tbase + ((uint32_t)(q4 * 32) << 16) + e * 256;
     constexpr float kLog2e = 1.4426950408889634f;
     int cnt = 0;
+    LsSlots sl;
     for (int wk = blockIdx.x; wk < p.n_work; wk += gridDim.x) {
       const int m0 = (wk % p.m_pairs) * 2, nt = wk / p.m_pairs;
-      if (m >= min(2, p.m_tiles - m0)) continue;
-      mbar_wait(&acc_full[m], cnt & 1);
+      const int nm = min(2, p.m_tiles - m0);
+      const int s0 = sl.first(nm);
+      if (e < s0 || e >= s0 + nm) continue;
+      const int m = m0 + (e - s0);  // the M tile in this slot
+      mbar_wait(&acc_full[e], cnt & 1);
       tc_fence_after();
-      const int64_t col0 = (int64_t)nt * kLsBN;
-      const int valid = p.vocab - col0 < kLsBN ? (int)(p.vocab - col0) : kLsBN;  // columns past the vocab are TMA zero fill
+      const int64_t col0 = (int64_t)nt * BN;
+      const int valid = p.vocab - col0 < BN ? (int)(p.vocab - col0) : BN;  // columns past the vocab are TMA zero fill
+      const int64_t row = (int64_t)m * 128 + trow;
       float mx = -INFINITY, sum = 0.f;
 #pragma unroll 1
-      for (int c = 0; c < kLsBN; c += 64) {
+      for (int c = 0; c < BN; c += 64) {
         float v[64];
         tmem_ld32(t_acc + c, *reinterpret_cast<float(*)[32]>(&v[0]));
         tmem_ld32(t_acc + c + 32, *reinterpret_cast<float(*)[32]>(&v[32]));
         tmem_wait_ld();
-        if (c + 64 >= kLsBN) {  // the tile is in registers: hand the accumulator back
+        if (c + 64 >= BN) {  // the tile is in registers: hand the accumulator back
           tc_fence_before();
-          mbar_arrive(&acc_empty[m]);
+          mbar_arrive(&acc_empty[e]);
         }
         float cm = -INFINITY;
 #pragma unroll
@@ -169,16 +205,20 @@ __global__ void __launch_bounds__(kLsThreads, 1)
           float acc = mx == -INFINITY ? 0.f : sum * exp2f(mx - mn);
 #pragma unroll
           for (int i = 0; i < 64; ++i) {
-            float e;
-            asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(v[i] - mn));
-            acc += e;
+            float ex;
+            asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(ex) : "f"(v[i] - mn));
+            acc += ex;
           }
           sum = acc;
           mx = mn;
         }
+        if ((c + 64) % kLsHalf == 0) {  // one partial per 128 vocab columns
+          const int64_t h0 = col0 + c + 64 - kLsHalf;  // first column of this half (halves past the vocab are not stored)
+          if (row < p.rows && h0 < p.vocab) p.part[h0 / kLsHalf * p.rows_pad + row] = make_float2(mx, sum);
+          mx = -INFINITY;
+          sum = 0.f;
+        }
       }
-      const int64_t row = (int64_t)(m0 + m) * 128 + trow;
-      if (row < p.rows) p.part[(int64_t)nt * p.rows_pad + row] = make_float2(mx, sum);
       ++cnt;
     }
   }
@@ -247,6 +287,19 @@ static int num_sms_ls() {
   return n;
 }
 
+template <int BN, bool NARROW>
+static int launch_lse(int grid, const CUtensorMap *maps, const LsParams &p, cudaStream_t s) {
+  using C = LsCfg<BN, NARROW>;
+  static thread_local bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(label_lse_kernel<BN, NARROW>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::Smem);
+    if (e != cudaSuccess) return set_error(DBSA_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+    attr_set = true;
+  }
+  label_lse_kernel<BN, NARROW><<<grid, kLsThreads, C::Smem, s>>>(maps[0], maps[1], p);
+  return check_launch("label_lse");
+}
+
 }  // namespace dbsa
 
 extern "C" int dbsa_label_score(const DbsaLabelScoreArgs *args, void *stream) {
@@ -266,7 +319,11 @@ extern "C" int dbsa_label_score(const DbsaLabelScoreArgs *args, void *stream) {
   p.rows_pad = (int64_t)p.m_tiles * 128;
   p.m_pairs = (p.m_tiles + 1) / 2;
   p.vocab = a.vocab;
-  p.n_tiles = (int)((a.vocab + kLsBN - 1) / kLsBN);
+  // batch-1 shapes (one M tile): 128-column vocab tiles, a one-M-tile stage
+  // layout with a deeper ring, and x loaded only for its real rows
+  const bool narrow = p.m_tiles == 1;
+  const int bn = narrow ? 128 : 256;
+  p.n_tiles = (int)((a.vocab + bn - 1) / bn);
   p.k_steps = (int)((a.d + kLsBK - 1) / kLsBK);
   p.n_work = p.m_pairs * p.n_tiles;
   p.part = reinterpret_cast<float2 *>(a.workspace);
@@ -274,7 +331,8 @@ extern "C" int dbsa_label_score(const DbsaLabelScoreArgs *args, void *stream) {
   {
     cuuint64_t dims[2] = {(cuuint64_t)a.d, (cuuint64_t)a.rows};
     cuuint64_t strides[1] = {(cuuint64_t)a.d * 2};
-    cuuint32_t box[2] = {(cuuint32_t)kLsBK, 128u};
+    p.x_box_rows = narrow ? (int)((a.rows + 15) / 16 * 16) : 128;
+    cuuint32_t box[2] = {(cuuint32_t)kLsBK, (cuuint32_t)p.x_box_rows};
     cuuint32_t estr[2] = {1, 1};
     if (!encode_tiled_bf16(&maps[0], a.x, 2, dims, strides, box, estr, CU_TENSOR_MAP_SWIZZLE_128B))
       return DBSA_ERR_CUDA;
@@ -282,24 +340,17 @@ extern "C" int dbsa_label_score(const DbsaLabelScoreArgs *args, void *stream) {
   {
     cuuint64_t dims[2] = {(cuuint64_t)a.d, (cuuint64_t)a.vocab};
     cuuint64_t strides[1] = {(cuuint64_t)a.d * 2};
-    cuuint32_t box[2] = {(cuuint32_t)kLsBK, (cuuint32_t)kLsBN};
+    cuuint32_t box[2] = {(cuuint32_t)kLsBK, (cuuint32_t)bn};
     cuuint32_t estr[2] = {1, 1};
     if (!encode_tiled_bf16(&maps[1], a.w, 2, dims, strides, box, estr, CU_TENSOR_MAP_SWIZZLE_128B))
       return DBSA_ERR_CUDA;
   }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  static thread_local bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(label_lse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kLsSmem);
-    if (e != cudaSuccess) return set_error(DBSA_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
-    attr_set = true;
-  }
   const int grid = p.n_work < num_sms_ls() ? p.n_work : num_sms_ls();
-  label_lse_kernel<<<grid, kLsThreads, kLsSmem, s>>>(maps[0], maps[1], p);
-  if (int rc = check_launch("label_lse")) return rc;
+  if (int rc = narrow ? launch_lse<128, true>(grid, maps, p, s) : launch_lse<256, false>(grid, maps, p, s)) return rc;
   const int64_t blocks = (a.n_pairs + 7) / 8;
   label_pair_logprob_kernel<<<(unsigned)blocks, 256, 0, s>>>(
-      p.part, p.n_tiles, p.rows_pad, reinterpret_cast<const __nv_bfloat16 *>(a.x),
+      p.part, (int)((a.vocab + kLsHalf - 1) / kLsHalf), p.rows_pad, reinterpret_cast<const __nv_bfloat16 *>(a.x),
       reinterpret_cast<const __nv_bfloat16 *>(a.w), a.d, a.pair_row, a.pair_target, a.n_pairs, a.out);
   return check_launch("label_pair_logprob");
 }

@@ -216,8 +216,8 @@ def label_logprob(logits, targets):
 
 
 def label_score_workspace_shape(rows: int, vocab: int) -> tuple[int, int, int]:
-    """fp32 [vocab tiles of 256][rows rounded up to 128][(max, sum)] of K5."""
-    return (-(-vocab // 256), -(-rows // 128) * 128, 2)
+    """fp32 [vocab / 128][rows rounded up to 128][(max, sum)] of K5."""
+    return (-(-vocab // 128), -(-rows // 128) * 128, 2)
 
 
 def label_score(x, lm_head_t, pair_row, pair_target, workspace=None, out=None):
