@@ -40,22 +40,60 @@ inline bool pdl_enabled() {
   return on;
 }
 
+// L2 residency for small, repeatedly re-read activations (the residual stream
+// of a batch-1 forward): a launch may mark one buffer persisting, so the
+// per-layer weight streams (hundreds of MB) do not evict it between layers.
+// The device's persisting carve-out is set once (DBSA_L2_PERSIST_MB, default 16;
+// 0 disables).
+constexpr size_t kPersistMaxBytes = 8u << 20;
+inline bool l2_persist_ready() {
+  static const bool ok = [] {
+    const char *e = getenv("DBSA_L2_PERSIST_MB");
+    const size_t mb = e ? (size_t)atoi(e) : 16;
+    if (!mb) return false;
+    return cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, mb << 20) == cudaSuccess;
+  }();
+  return ok;
+}
+
+struct Persist {
+  const void *base = nullptr;
+  size_t bytes = 0;
+};
+
 template <typename... KArgs, typename... Args>
-inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl,
-                            Args &&...args) {
+inline cudaError_t launch_kp(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl,
+                             Persist keep, Args &&...args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
+  int n = 0;
   if (pdl && pdl_enabled()) {
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
+    at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
   }
+  if (keep.base && keep.bytes && keep.bytes <= kPersistMaxBytes && l2_persist_ready()) {
+    at[n].id = cudaLaunchAttributeAccessPolicyWindow;
+    at[n].val.accessPolicyWindow.base_ptr = const_cast<void *>(keep.base);
+    at[n].val.accessPolicyWindow.num_bytes = keep.bytes;
+    at[n].val.accessPolicyWindow.hitRatio = 1.f;
+    at[n].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    at[n].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    ++n;
+  }
+  cfg.attrs = n ? at : nullptr;
+  cfg.numAttrs = n;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl,
+                            Args &&...args) {
+  return launch_kp(kern, grid, block, smem, s, pdl, Persist{}, std::forward<Args>(args)...);
 }
 
 #ifdef __CUDACC__

@@ -348,15 +348,21 @@ static int launch_rmsnorm(float *x, const float *delta, const float *weight, voi
   __nv_bfloat16 *o = reinterpret_cast<__nv_bfloat16 *>(out);
   const bool al = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(weight) |
                     reinterpret_cast<uintptr_t>(out) | (ADD ? reinterpret_cast<uintptr_t>(delta) : 0)) & 15) == 0;
+  // the residual stream x is re-read by the next norm one projection / FFN
+  // later: keep it in L2 across the weight streams (small batches only)
+  const Persist keep{x, ADD ? (size_t)rows * dim * sizeof(float) : 0};
   if (dim % 4 == 0 && al && dim <= 4 * 256 * 8) {
     const int n4 = (int)(dim / 4);
     if (n4 <= 256 * 4)
-      launch_k(rmsnorm4_kernel<ADD, 4>, dim3((unsigned)rows), dim3(256), 0, st, true, x, delta, weight, o, dim, eps);
+      launch_kp(rmsnorm4_kernel<ADD, 4>, dim3((unsigned)rows), dim3(256), 0, st, true, keep, x, delta, weight, o, dim,
+                eps);
     else
-      launch_k(rmsnorm4_kernel<ADD, 8>, dim3((unsigned)rows), dim3(256), 0, st, true, x, delta, weight, o, dim, eps);
+      launch_kp(rmsnorm4_kernel<ADD, 8>, dim3((unsigned)rows), dim3(256), 0, st, true, keep, x, delta, weight, o, dim,
+                eps);
   } else {
     const int threads = dim >= 1024 ? 256 : (dim >= 256 ? 128 : 64);
-    launch_k(rmsnorm_kernel<ADD>, dim3((unsigned)rows), dim3(threads), 0, st, true, x, delta, weight, o, dim, eps);
+    launch_kp(rmsnorm_kernel<ADD>, dim3((unsigned)rows), dim3(threads), 0, st, true, keep, x, delta, weight, o, dim,
+              eps);
   }
   return check_launch("rmsnorm");
 }

@@ -698,7 +698,13 @@ class AttnSchedule:
         self.max_rows = max((m[1] for m in merges), default=0)
         self.rope = dm.rope_for(nt.max_pos - min_shift + 1)
         self.part_rows = part_rows
-        self.part_o = torch.empty((max(part_rows, 1), hd), dtype=torch.float32, device=dev)
+        import os
+
+        # split-KV partials in bf16 (as the chunk-major ones): half the epilogue and
+        # K3m bytes of a latency launch; DBSA_SPLIT_BF16=0 keeps fp32
+        bf16 = mode == "split" and os.environ.get("DBSA_SPLIT_BF16", "1") == "1"
+        self.part_o = torch.empty((max(part_rows, 1), hd), dtype=torch.bfloat16 if bf16 else torch.float32,
+                                  device=dev)
         self.part_lse = torch.empty((max(part_rows, 1),), dtype=torch.float32, device=dev)
 
     def segs_ptr(self, layer: int) -> int:
