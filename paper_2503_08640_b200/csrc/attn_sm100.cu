@@ -1488,7 +1488,10 @@ static int launch_attn(const DbsaAttnArgs &a, const AttnParams &p, const CUtenso
   // persistent: one CTA per SM (1 CTA fits per SM), striding over the works or
   // running the host-packed ranges of cta_works
   const int grid = a.cta_works ? a.n_ctas : a.n_works < num_sms() ? a.n_works : num_sms();
-  launch_k(kern, dim3(grid), dim3(C::THREADS), C::SMEM, s, true, maps[0], maps[1], maps[2], maps[3], p);
+  // programmatic dependent launch only when Q staging may overlap the
+  // predecessor (pdl_early_q): a batch launch gains nothing from it, and its
+  // early-resident CTAs would hold every SM through the K2w boundary
+  launch_k(kern, dim3(grid), dim3(C::THREADS), C::SMEM, s, p.pdl_early != 0, maps[0], maps[1], maps[2], maps[3], p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(DBSA_ERR_CUDA, "attention launch: %s", cudaGetErrorString(e));
   return DBSA_OK;
