@@ -292,7 +292,8 @@ class _Scratch:
         self.act = torch.empty((min(n_tok, self.ffn_chunk), c.ffn_dim), dtype=torch.bfloat16, device=dev)
 
 
-def _decoder_gen(dm, ids_dev, attend, write_kv, n_layers=None, kv_only_last=False, keep_last=None):
+def _decoder_gen(dm, ids_dev, attend, write_kv, n_layers=None, kv_only_last=False, keep_last=None,
+                 attend_early=None):
     """Pre-norm decoder body (model.py:319-359) over n new tokens, as a
     generator: it yields after each layer's `write_kv(l, qkv)` (the point where
     a multi-shard caller exchanges pages) and returns the fp32 final hidden
@@ -302,7 +303,9 @@ def _decoder_gen(dm, ids_dev, attend, write_kv, n_layers=None, kv_only_last=Fals
     return value is None.  keep_last (device int64 row indices): only those rows'
     outputs are used (the scored rows of a label batch), so the last layer's O
     projection and FFN run on them alone and the returned hidden states are
-    those rows, in keep_last order."""
+    those rows, in keep_last order.  attend_early(l, qkv, out), when given,
+    runs right after the page write, before the yield (the part of the
+    attention that does not wait for the caller's page exchange)."""
     torch = _torch()
     c = dm.config
     n = ids_dev.shape[0]
@@ -317,8 +320,11 @@ def _decoder_gen(dm, ids_dev, attend, write_kv, n_layers=None, kv_only_last=Fals
             ops.add_rmsnorm(h, s.proj, lw["attn_norm"], c.norm_eps, s.x)
         torch.mm(s.x, lw["wqkv"], out=s.qkv)
         write_kv(layer, s.qkv)
+        last_kv_only = kv_only_last and layer == L - 1
+        if attend_early is not None and not last_kv_only:
+            attend_early(layer, s.qkv, s.att)
         yield layer
-        if kv_only_last and layer == L - 1:
+        if last_kv_only:
             return None
         attend(layer, s.qkv, s.att)
         if keep_last is not None and layer == L - 1:
@@ -366,9 +372,14 @@ class Stage1Plan:
     """Device tables of one layer-synchronous stage-1 encode of groups
     `new` (BlockEntry list; their tokens are contiguous, first at tok_base)."""
 
-    def __init__(self, dm, cache, new, pattern):
+    def __init__(self, dm, cache, new, pattern, late_blocks=None):
+        """late_blocks: groups whose pages of each layer arrive by the halo
+        exchange (encode_pool_sharded).  The works that read one of them go
+        last (`n_early` works before them), so the rest can run while the
+        exchange is in flight."""
         c = dm.config
         gs, hkv = c.group_size, c.n_kv_heads
+        late_blocks = set(late_blocks or ())
         # token buffer = the listed groups' tokens back to back (groups need not be contiguous)
         local_of = {}
         acc = 0
@@ -403,7 +414,10 @@ class Stage1Plan:
         longest = {}
         for wk in works:
             longest[wk[3]] = max(longest.get(wk[3], 0), wk[0])
-        works.sort(key=lambda wk: (-longest[wk[3]], wk[3], -wk[0]))
+        late_groups = {local_of[e.block_id] for e in new
+                       if late_blocks & set(pattern.context_of(e.block_id))}
+        works.sort(key=lambda wk: (wk[3] in late_groups, -longest[wk[3]], wk[3], -wk[0]))
+        self.n_early = sum(1 for wk in works if wk[3] not in late_groups)
         self.pairs = pairs
         self.n_works = len(works)
         self.n_segs = len(segs)
@@ -422,7 +436,7 @@ class Stage1Plan:
         return self.segs.data_ptr() + layer * self.n_segs * ops.SEG_DTYPE.itemsize
 
 
-def encode_groups_gen(dm, cache, new, ids, pattern, layers=None):
+def encode_groups_gen(dm, cache, new, ids, pattern, layers=None, late_blocks=None, kv_written=None):
     """Stage 1 for groups `new` (BlockEntry list) whose concatenated token ids
     are `ids`, as a generator pausing after each layer's page write (see
     _decoder_gen).  Returns the attended pair count of these groups
@@ -433,7 +447,7 @@ def encode_groups_gen(dm, cache, new, ids, pattern, layers=None):
     visited a wrong tile set and this raises."""
     torch = _torch()
     c = dm.config
-    plan = Stage1Plan(dm, cache, new, pattern)
+    plan = Stage1Plan(dm, cache, new, pattern, late_blocks)
     n_layers = c.n_layers if layers is None else layers
     counter = torch.zeros(1, dtype=torch.int64, device=dm.device) if n_layers > 1 else None
     store = cache.store
@@ -444,15 +458,29 @@ def encode_groups_gen(dm, cache, new, ids, pattern, layers=None):
     def write_kv(layer, qkv):
         ops.kv_write(qkv[:, qw:], qkv[:, qw + kw:], stride, plan.pos, dm.rope, plan.pages, plan.n_pages, store.k,
                      store.v, store.rows, c.n_layers, layer, c.n_kv_heads, c.head_dim)
+        if kv_written is not None:  # the halo exchange of this layer may start here
+            kv_written(layer)
 
-    def attend(layer, qkv, out):
-        ops.attention(q=qkv, q_tok_stride=stride, tok_pos=plan.pos, tok_lo=None, rope=dm.rope,
-                      pool=store.planes(), aux=None, n_heads=c.n_heads, n_kv_heads=c.n_kv_heads, head_dim=c.head_dim,
-                      works_dev=plan.works, n_works=plan.n_works, segs_dev=plan.segs_ptr(layer), num_m=plan.num_m,
-                      out=out, out_tok_stride=qw, pair_count=counter if layer == 0 else None, after_kv_write=True)
+    def launch(layer, qkv, out, w0, w1, after_kv_write):
+        if w1 > w0:
+            ops.attention(q=qkv, q_tok_stride=stride, tok_pos=plan.pos, tok_lo=None, rope=dm.rope,
+                          pool=store.planes(), aux=None, n_heads=c.n_heads, n_kv_heads=c.n_kv_heads,
+                          head_dim=c.head_dim, works_dev=plan.works.data_ptr() + w0 * ops.WORK_DTYPE.itemsize,
+                          n_works=w1 - w0, segs_dev=plan.segs_ptr(layer), num_m=plan.num_m, out=out,
+                          out_tok_stride=qw, pair_count=counter if layer == 0 else None,
+                          after_kv_write=after_kv_write)
+
+    n_early = plan.n_early if late_blocks else 0  # without a halo every work runs in attend()
+
+    def attend_early(layer, qkv, out):  # works that read no halo group: before the exchange
+        launch(layer, qkv, out, 0, n_early, True)
+
+    def attend(layer, qkv, out):  # the rest, once the layer's halo pages are in
+        launch(layer, qkv, out, n_early, plan.n_works, n_early == 0)
 
     # only the pages are kept: the last layer's attention / O / FFN are skipped
-    yield from _decoder_gen(dm, ids_dev, attend, write_kv, n_layers=layers, kv_only_last=True)
+    yield from _decoder_gen(dm, ids_dev, attend, write_kv, n_layers=layers, kv_only_last=True,
+                            attend_early=attend_early if late_blocks else None)
     if counter is None:  # a one-layer model runs no attention in stage 1 (its output feeds nothing)
         return plan.pairs
     visited = int(counter.item())
@@ -484,6 +512,21 @@ def encode_pool_sharded(dm, blocks, pattern, comm, device=None):
     ranges = parallel.plan_group_shards(counts, comm.world)
     halo = parallel.halo_plan(pattern, ranges, n_blocks)
     caches, gens = {}, {}
+    torch = _torch()
+    dev = torch.device(device) if device is not None else dm.device
+    # the halo exchange runs on a side stream that waits only for the layer's
+    # page writes; the K1 works that read no halo group run meanwhile
+    side = torch.cuda.Stream(dev) if dev.type == "cuda" else None
+    kv_events = {}
+
+    def on_kv_written(r):
+        def record(layer):
+            if side is not None:
+                ev = torch.cuda.Event()
+                ev.record()
+                kv_events[r] = ev
+        return record
+
     for r in comm.local_ranks:
         present = parallel.local_groups(pattern, ranges, r, n_blocks)
         # page-rounded capacity: reserve() must not grow (a second buffer while the first lives)
@@ -493,14 +536,23 @@ def encode_pool_sharded(dm, blocks, pattern, comm, device=None):
         new = [cache.blocks[g] for g in compute]
         ids = np.concatenate([np.asarray(blocks[g][0], np.int64) for g in compute])
         caches[r] = cache
-        gens[r] = encode_groups_gen(dm, cache, new, ids, pattern)
+        gens[r] = encode_groups_gen(dm, cache, new, ids, pattern,
+                                    late_blocks={g for g, _, dst in halo if dst == r},
+                                    kv_written=on_kv_written(r))
     pairs = {}
     stores = {r: caches[r].store for r in caches}
     entries = {r: {e.block_id: e for e in caches[r].blocks if e.row0 >= 0} for r in caches}
     for layer in range(c.n_layers):
         for r in caches:
             next(gens[r])
-        parallel.exchange_pages(comm, layer, halo, stores, entries)
+        if side is None:
+            parallel.exchange_pages(comm, layer, halo, stores, entries)
+            continue
+        for ev in kv_events.values():
+            side.wait_event(ev)
+        with torch.cuda.stream(side):
+            parallel.exchange_pages(comm, layer, halo, stores, entries)
+        torch.cuda.current_stream(dev).wait_stream(side)
     for r in caches:
         pairs[r] = _drain(gens[r])
         if r != 0:  # the sink's own pairs are counted once, on rank 0
