@@ -1572,10 +1572,17 @@ extern "C" int dbsa_attention(const DbsaAttnArgs *args, void *stream) {
     return set_error(DBSA_ERR_CONFIG, "cta_works needs num_m == 2 and 0 < n_ctas <= %d, got num_m %d n_ctas %d",
                      num_sms(), a.num_m, a.n_ctas);
   {
-    const char *e = getenv("DBSA_DEBUG_MODE");
-    p.dbg = e ? atoi(e) : 0;
-    const char *f = getenv("DBSA_L2PF");
-    p.l2_prefetch = f ? atoi(f) : 0;
+    // profiling switches, read once per process (not on every launch)
+    static const int dbg = [] {
+      const char *e = getenv("DBSA_DEBUG_MODE");
+      return e ? atoi(e) : 0;
+    }();
+    static const int l2pf = [] {
+      const char *e = getenv("DBSA_L2PF");
+      return e ? atoi(e) : 0;
+    }();
+    p.dbg = dbg;
+    p.l2_prefetch = l2pf;
   }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   // num_m 1 runs the single-M-tile kernel (Q in TMEM, double-buffered S) unless

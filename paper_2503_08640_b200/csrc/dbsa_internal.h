@@ -45,7 +45,8 @@ inline bool pdl_enabled() {
 // per-layer weight streams (hundreds of MB) do not evict it between layers.
 // The device's persisting carve-out is set once (DBSA_L2_PERSIST_MB, default 16;
 // 0 disables).
-constexpr size_t kPersistMaxBytes = 8u << 20;
+constexpr size_t kPersistMaxBytes = 8u << 20;     // activations kept resident (the residual stream)
+constexpr size_t kWindowMaxBytes = 128u << 20;     // cudaDevAttrMaxAccessPolicyWindowSize on B200
 inline bool l2_persist_ready() {
   static const bool ok = [] {
     const char *e = getenv("DBSA_L2_PERSIST_MB");
@@ -76,7 +77,7 @@ inline cudaError_t launch_kp(void (*kern)(KArgs...), dim3 grid, dim3 block, size
     at[n].val.programmaticStreamSerializationAllowed = 1;
     ++n;
   }
-  if (keep.base && keep.bytes && keep.bytes <= kPersistMaxBytes && l2_persist_ready()) {
+  if (keep.base && keep.bytes && keep.bytes <= kWindowMaxBytes && l2_persist_ready()) {
     at[n].id = cudaLaunchAttributeAccessPolicyWindow;
     at[n].val.accessPolicyWindow.base_ptr = const_cast<void *>(keep.base);
     at[n].val.accessPolicyWindow.num_bytes = keep.bytes;

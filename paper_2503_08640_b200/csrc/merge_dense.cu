@@ -350,7 +350,8 @@ static int launch_rmsnorm(float *x, const float *delta, const float *weight, voi
                     reinterpret_cast<uintptr_t>(out) | (ADD ? reinterpret_cast<uintptr_t>(delta) : 0)) & 15) == 0;
   // the residual stream x is re-read by the next norm one projection / FFN
   // later: keep it in L2 across the weight streams (small batches only)
-  const Persist keep{x, ADD ? (size_t)rows * dim * sizeof(float) : 0};
+  const size_t xbytes = (size_t)rows * dim * sizeof(float);
+  const Persist keep{x, ADD && xbytes <= kPersistMaxBytes ? xbytes : 0};
   if (dim % 4 == 0 && al && dim <= 4 * 256 * 8) {
     const int n4 = (int)(dim / 4);
     if (n4 <= 256 * 4)

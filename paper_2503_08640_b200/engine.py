@@ -782,10 +782,6 @@ class AttnSchedule:
 PACK_FIRST, PACK_NEXT = 15, 5
 
 
-def _seg_tiles(seg) -> int:
-    return (int(seg[2]) % PAGE + int(seg[3]) + 127) // 128
-
-
 def pack_works(works, segs, n_sms: int):
     """Longest-processing-time packing of K3 works onto at most n_sms CTAs
     under the PACK_FIRST / PACK_NEXT cost model.  Returns the works reordered
@@ -793,17 +789,21 @@ def pack_works(works, segs, n_sms: int):
     offsets (DbsaAttnArgs.cta_works)."""
     import heapq
 
-    tiles = [sum(_seg_tiles(segs[i]) for i in range(w[4], w[5])) for w in works]
+    sg = np.asarray(segs, dtype=np.int64).reshape(len(segs), -1)
+    seg_tiles = (sg[:, 2] % PAGE + sg[:, 3] + 127) // 128 if len(sg) else np.zeros(0, np.int64)
+    cum = np.concatenate([[0], np.cumsum(seg_tiles)])
+    w = np.asarray(works, dtype=np.int64).reshape(len(works), -1)
+    tiles = cum[w[:, 5]] - cum[w[:, 4]]
+    order = np.argsort(-tiles, kind="stable")
     n_ctas = min(n_sms, len(works))
-    order = sorted(range(len(works)), key=lambda i: -tiles[i])
-    heap = [(0, b) for b in range(n_ctas)]  # (load, cta); empty CTAs first
-    per_cta = [[] for _ in range(n_ctas)]
-    for i in order:
-        # cheapest resulting load: an empty CTA costs PACK_FIRST, a busy one PACK_NEXT
+    # the n_ctas longest works open one CTA each; the rest go to the least loaded
+    per_cta = [[int(i)] for i in order[:n_ctas]]
+    heap = [(PACK_FIRST + int(tiles[i]), b) for b, i in enumerate(order[:n_ctas])]
+    heapq.heapify(heap)
+    for i in order[n_ctas:]:
         load, b = heap[0]
-        cost = (PACK_NEXT if per_cta[b] else PACK_FIRST) + tiles[i]
-        heapq.heapreplace(heap, (load + cost, b))
-        per_cta[b].append(i)
+        heapq.heapreplace(heap, (load + PACK_NEXT + int(tiles[i]), b))
+        per_cta[b].append(int(i))
     out, bounds = [], [0]
     for lst in per_cta:
         out += [works[i] for i in lst]
