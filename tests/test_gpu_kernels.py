@@ -723,14 +723,16 @@ def test_k1_at_c4_shape_vs_float64():
 
 # ---------------------------------------------------------------- K5 fused label scoring
 @pytest.mark.parametrize("rows,d,vocab", [(1, 64, 259), (5, 64, 259), (130, 512, 1000), (300, 200, 777),
-                                          (832, 4096, 128256)])
+                                          (13, 4096, 128256), (128, 4096, 128256), (832, 4096, 128256)])
 def test_label_score_vs_float64(rows, d, vocab):
     """K5 (dbsa_label_score): log_softmax(x @ lm_head)[row, target] for scored
     (row, target) pairs without materialising logits, against float64 over
     the same bf16 operands (model.py:393-397, 414-417, 441-443).  Shapes: the
     C1 tokenizer vocab, a vocab that is not a multiple of the 256-column tile,
     a d that is not a multiple of the 64-wide K slice, rows past one and two M
-    tiles, and the C3 batch (832 distinct scored rows, Llama-3 vocab)."""
+    tiles, the batch-1 narrow form at the Llama-3 vocab (13 and 128 rows: N =
+    128 vocab tiles, x loaded for its real rows), and the C3 batch (832
+    distinct scored rows)."""
     dev = torch.device("cuda", 0)
     g = torch.Generator(device=dev).manual_seed(rows + d)
     x = (torch.randn(rows, d, generator=g, device=dev) * 2).to(torch.bfloat16)
