@@ -634,9 +634,8 @@ class NewTokens:
         self.pages = ops.to_device(_pages_for([(int(self.tok0[i]), self.n_new[i], int(self.aux_row0[i]))
                                                for i in range(len(jobs))]), dev)
         self.n_pages = int(sum(-(-n // PAGE) for n in self.n_new))
-        hdp = ops.hd_pad(c.head_dim)
-        self.k_aux = torch.zeros((1, c.n_kv_heads, self.aux_rows, hdp), dtype=torch.bfloat16, device=dev)
-        self.v_aux = torch.zeros((1, c.n_kv_heads, hdp, self.aux_rows), dtype=torch.bfloat16, device=dev)
+        self._aux_shape = (c.n_kv_heads, ops.hd_pad(c.head_dim), dev)
+        self._aux = None
         # canonical partial layout (sharded mode): one row block per (job, slab, kv head)
         self.part_base = []
         base = 0
@@ -648,8 +647,38 @@ class NewTokens:
             self.part_base.append(per)
         self.canon_rows = base
 
+    def _aux_planes(self):
+        # allocated on first use: a batch that replays a captured graph writes the
+        # graph's own aux pages, never these
+        if self._aux is None:
+            torch = _torch()
+            hkv, hdp, dev = self._aux_shape
+            self._aux = (torch.zeros((1, hkv, self.aux_rows, hdp), dtype=torch.bfloat16, device=dev),
+                         torch.zeros((1, hkv, hdp, self.aux_rows), dtype=torch.bfloat16, device=dev))
+        return self._aux
+
+    @property
+    def k_aux(self):
+        return self._aux_planes()[0]
+
+    @property
+    def v_aux(self):
+        return self._aux_planes()[1]
+
     def aux(self):
         return (self.k_aux, self.v_aux, self.aux_rows, 1)
+
+
+_SPLIT_TEMPLATES = __import__("collections").OrderedDict()  # split-KV table templates (AttnSchedule), LRU
+_SPLIT_TEMPLATES_MAX = 64
+
+
+def _split_bf16() -> bool:
+    """Split-KV partials in bf16 (as the chunk-major ones): half the epilogue
+    and K3m bytes of a latency launch; DBSA_SPLIT_BF16=0 keeps fp32."""
+    import os
+
+    return os.environ.get("DBSA_SPLIT_BF16", "1") == "1"
 
 
 class AttnSchedule:
@@ -678,7 +707,23 @@ class AttnSchedule:
 
             pack = mode == "split" and nt.num_m == 2 and os.environ.get("DBSA_PACK", "1") != "0"
         self.pack = pack
+        dev = dm.device
+        # split-KV tables depend on the chunk LENGTHS (and page offsets), not on
+        # which groups were picked: a cached template is refilled with this
+        # batch's chunk rows and shifts (the batch-1 planning cost of Runner.infer)
+        key = None
+        if mode == "split" and order == "query":
+            key = (tuple(tuple((int(r[1]), int(r[0]) % PAGE) for r in np.asarray(t, np.int64).reshape(-1, 3))
+                         for t in tables),
+                   tuple(int(x) for x in nt.n_new), tuple(int(j.prefix) for j in jobs), nt.num_m, include_self,
+                   pack, target, gs, hkv, hd, c.n_layers, str(dev), _split_bf16())
+            tpl = _SPLIT_TEMPLATES.get(key)
+            if tpl is not None:
+                _SPLIT_TEMPLATES.move_to_end(key)
+                self._from_template(dm, nt, tables, tpl)
+                return
         segs, works, merges = [], [], []
+        seg_src = []  # per segment: (job, chunk index) or (job, -1) for SELF
         min_shift = 0
         part_rows = 0 if mode == "split" else nt.canon_rows
         kv_tok = 0
@@ -713,6 +758,7 @@ class AttnSchedule:
             for sp in range(n_split - 1 + own_self):
                 sb = len(segs)
                 segs += chunk_segs[bounds[sp]:bounds[sp + 1]]
+                seg_src += [(qi, u) for u in range(bounds[sp], bounds[sp + 1])]
                 split_ranges.append((sb, len(segs)))
             n_split += own_self
             for t0, ntk in slabs:
@@ -720,8 +766,10 @@ class AttnSchedule:
                 last_sb = len(segs)
                 if not own_self:
                     segs += chunk_segs[bounds[n_split - 1]:bounds[n_split]]
+                    seg_src += [(qi, u) for u in range(bounds[n_split - 1], bounds[n_split])]
                 if include_self:
                     segs.append((1, 0, int(nt.aux_row0[qi]), t0 + ntk, SEG_SELF, 0))
+                    seg_src.append((qi, -1))
                 last = (last_sb, len(segs))
                 for kv in range(hkv):
                     base = part_rows
@@ -743,21 +791,69 @@ class AttnSchedule:
             self.cta_works = ops.to_device(np.asarray(bounds_cta, dtype=np.int32), dm.device)
         self.kv_tokens = kv_tok
         self.n_works, self.n_segs, self.n_merge = len(works), len(segs), len(merges)
-        dev = dm.device
         self.works = ops.to_device(_work_array(works), dev)
-        self.segs = ops.to_device(_per_layer_segs(_seg_array(segs), c.n_layers), dev)
+        seg_arr = _seg_array(segs)
+        self.segs = ops.to_device(_per_layer_segs(seg_arr, c.n_layers), dev)
         self.merges = ops.to_device(_merge_array(merges), dev) if merges else None
         self.max_rows = max((m[1] for m in merges), default=0)
         self.rope = dm.rope_for(nt.max_pos - min_shift + 1)
         self.part_rows = part_rows
-        import os
+        bf16 = mode == "split" and _split_bf16()
+        self._part_spec = (max(part_rows, 1), hd, torch.bfloat16 if bf16 else torch.float32, dev)
+        self._part = None
+        if key is not None:
+            src = np.asarray(seg_src, np.int64).reshape(-1, 2)
+            _SPLIT_TEMPLATES[key] = dict(
+                works=self.works, merges=self.merges, cta_works=self.cta_works, n_ctas=self.n_ctas, segs=seg_arr,
+                seg_job=src[:, 0], seg_chunk=src[:, 1], n_works=self.n_works, n_merge=self.n_merge,
+                max_rows=self.max_rows, part_rows=part_rows, kv_tokens=kv_tok, part_dtype=self._part_spec[2])
+            while len(_SPLIT_TEMPLATES) > _SPLIT_TEMPLATES_MAX:
+                _SPLIT_TEMPLATES.popitem(last=False)
 
-        # split-KV partials in bf16 (as the chunk-major ones): half the epilogue and
-        # K3m bytes of a latency launch; DBSA_SPLIT_BF16=0 keeps fp32
-        bf16 = mode == "split" and os.environ.get("DBSA_SPLIT_BF16", "1") == "1"
-        self.part_o = torch.empty((max(part_rows, 1), hd), dtype=torch.bfloat16 if bf16 else torch.float32,
-                                  device=dev)
-        self.part_lse = torch.empty((max(part_rows, 1),), dtype=torch.float32, device=dev)
+    def _from_template(self, dm, nt, tables, tpl):
+        """This batch's split-KV tables from a cached template: the works, merge
+        groups and CTA ranges as they are; the segments refilled with the
+        batch's chunk rows and RoPE shifts and its own tokens' aux rows."""
+        torch = _torch()
+        c = dm.config
+        segs = tpl["segs"].copy()
+        job, chunk = tpl["seg_job"], tpl["seg_chunk"]
+        tabs = [np.asarray(t, np.int64).reshape(-1, 3) for t in tables]
+        allch = np.concatenate(tabs) if tabs else np.zeros((0, 3), np.int64)
+        off = np.concatenate([[0], np.cumsum([len(t) for t in tabs])])
+        full = chunk >= 0
+        idx = off[job[full]] + chunk[full]
+        segs["row0"][full] = allch[idx, 0]
+        segs["shift"][full] = allch[idx, 2]
+        segs["row0"][~full] = np.asarray(nt.aux_row0, np.int64)[job[~full]]
+        min_shift = min(0, int(allch[:, 2].min())) if len(allch) else 0
+        self.works, self.merges, self.cta_works, self.n_ctas = tpl["works"], tpl["merges"], tpl["cta_works"], tpl["n_ctas"]
+        self.n_works, self.n_segs, self.n_merge = tpl["n_works"], len(segs), tpl["n_merge"]
+        self.segs = ops.to_device(_per_layer_segs(segs, c.n_layers), dm.device)
+        self.max_rows, self.part_rows, self.kv_tokens = tpl["max_rows"], tpl["part_rows"], tpl["kv_tokens"]
+        self.rope = dm.rope_for(nt.max_pos - min_shift + 1)
+        self._part_spec = (max(self.part_rows, 1), c.head_dim, tpl["part_dtype"], dm.device)
+        self._part = None
+
+    def _partials(self):
+        # allocated on first use: a batch that replays a captured graph uses the graph's
+        if self._part is None:
+            torch = _torch()
+            n, hd, dt, dev = self._part_spec
+            self._part = (torch.empty((n, hd), dtype=dt, device=dev), torch.empty((n,), dtype=torch.float32, device=dev))
+        return self._part
+
+    @property
+    def part_o(self):
+        return self._partials()[0]
+
+    @part_o.setter
+    def part_o(self, v):
+        self._part = (v, self._partials()[1])
+
+    @property
+    def part_lse(self):
+        return self._partials()[1]
 
     def segs_ptr(self, layer: int) -> int:
         return self.segs.data_ptr() + layer * self.n_segs * ops.SEG_DTYPE.itemsize
@@ -1066,7 +1162,7 @@ class Stage2Plan:
             self.sched = ChunkMajorSchedule(dm, jobs, self.new)
         else:
             self.sched = AttnSchedule(dm, jobs, self.new, target_ctas=target_ctas, order=order)
-        for name in ("tok0", "n_tok", "num_m", "pos", "lo", "ids", "pages", "n_pages", "k_aux", "v_aux", "aux_rows"):
+        for name in ("tok0", "n_tok", "num_m", "pos", "lo", "ids", "pages", "n_pages", "aux_rows"):
             setattr(self, name, getattr(self.new, name))
         for name in ("works", "n_works", "n_segs", "n_merge", "merges", "max_rows", "rope", "kv_tokens"):
             setattr(self, name, getattr(self.sched, name))
@@ -1078,6 +1174,14 @@ class Stage2Plan:
     @property
     def part_lse(self):
         return self.sched.part_lse
+
+    @property
+    def k_aux(self):
+        return self.new.k_aux
+
+    @property
+    def v_aux(self):
+        return self.new.v_aux
 
     def segs_ptr(self, layer: int) -> int:
         return self.sched.segs_ptr(layer)
@@ -1339,6 +1443,14 @@ class GraphedStage2:
                 nw, ns = max(sc.n_real_works, capacity[0]), max(sc.n_real_segs, capacity[1])
             sc.pad_to(-(-nw // 64) * 64, -(-ns // 16) * 16)
             plan.works, plan.n_works, plan.segs, plan.n_segs = sc.works, sc.n_works, sc.segs, sc.n_segs
+        else:
+            # replay() copies later batches' tables into these buffers: they must not be
+            # the shared split-KV template tensors (AttnSchedule._from_template)
+            sc = plan.sched
+            sc.works = sc.works.clone()
+            sc.merges = sc.merges.clone() if sc.merges is not None else None
+            sc.cta_works = sc.cta_works.clone() if sc.cta_works is not None else None
+            plan.works, plan.merges = sc.works, sc.merges
         self._run()  # warm-up: workspace allocation, cuBLAS handles, kernel attributes
         torch.cuda.current_stream(dm.device).synchronize()
         self.graph = torch.cuda.CUDAGraph()
