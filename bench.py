@@ -179,10 +179,13 @@ class KernelTimer:
 
         return inner
 
-    def mean_ms(self):
-        if not self.pairs:
+    def mean_ms(self, period=None):
+        """Mean launch time; period=L skips every L-th launch (the last layer of
+        a scored forward, which runs the scored rows alone: Stage2Plan.last)."""
+        pairs = self.pairs if period is None else [p for i, p in enumerate(self.pairs) if i % period != period - 1]
+        if not pairs:
             return None
-        return sum(s.elapsed_time(e) for s, e in self.pairs) / len(self.pairs)
+        return sum(s.elapsed_time(e) for s, e in pairs) / len(pairs)
 
 
 # ------------------------------------------------------------------ workload
@@ -497,7 +500,7 @@ def run_ours(args):
     kv_bytes = plan0.kv_tokens * 2 * cfg.n_kv_heads * cfg.head_dim * 2  # kv_tokens = selected tokens, all queries
     qo_bytes = 2 * plan0.n_tok * cfg.n_heads * cfg.head_dim * 2
     k3_flops = k3_algorithmic_flops(jobs0, cfg)
-    k3_ms = k3.mean_ms()
+    k3_ms = k3.mean_ms(cfg.n_layers if plan0.last is not None else None)  # full launches only
     k3_tf = k3_flops / (k3_ms / 1e3) / 1e12 if k3_ms else None
     traffic = traffic_for("k3", f"{args.config}_r{RATIO:.2f}")
     clocks = clk.summary()

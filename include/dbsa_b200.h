@@ -83,8 +83,9 @@ typedef struct DbsaAttnWork {
   int32_t seg_begin;
   int32_t seg_end;
   int32_t prefix;   /* SELF keys with local index < prefix are visible to all rows */
-  int32_t out_mode; /* DBSA_OUT_BF16 / DBSA_OUT_PARTIAL / DBSA_OUT_MAPPED (FULL segments only,
-                       every shift 0: the rope row comes from the map) */
+  int32_t out_mode; /* DBSA_OUT_BF16 / DBSA_OUT_PARTIAL / DBSA_OUT_MAPPED (one segment -- FULL, or SELF
+                       with self_tok0 / prefix / tok_lo as for plain works -- every shift 0: the
+                       rope row comes from the map) */
   int64_t part_row0; /* partial row base (out_mode 1) */
 } DbsaAttnWork;
 

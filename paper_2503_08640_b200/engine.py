@@ -326,10 +326,11 @@ def _decoder_gen(dm, ids_dev, attend, write_kv, n_layers=None, kv_only_last=Fals
         yield layer
         if last_kv_only:
             return None
-        attend(layer, s.qkv, s.att)
+        compact = attend(layer, s.qkv, s.att)
         if keep_last is not None and layer == L - 1:
             k = keep_last.numel()
-            att = s.att.index_select(0, keep_last)
+            # attend() may have produced the kept rows alone, back to back (Stage2Plan.last)
+            att = s.att[:k] if compact else s.att.index_select(0, keep_last)
             h = h.index_select(0, keep_last)
             proj, xk = s.proj[:k], s.x[:k]
             mm_f32(att, lw["wo"], proj)
@@ -928,14 +929,15 @@ class ChunkMajorSchedule:
     The RoPE re-positioning delta of (query, chunk) is folded into each map
     entry's rope row (tok_pos - delta)."""
 
-    def __init__(self, dm, jobs, nt: NewTokens, chunk_tables=None, num_m: int = 2, include_self: bool = True):
+    def __init__(self, dm, jobs, nt: NewTokens, chunk_tables=None, num_m: int = 2, include_self: bool = True,
+                 subsets=None):
         torch = _torch()
         c = dm.config
         hd = c.head_dim
         tables = chunk_tables if chunk_tables is not None else [j.chunks for j in jobs]
         self.num_m = num_m
         t = chunk_major_tables(tables, nt.n_new, nt.pos_host, nt.aux_row0, [j.prefix for j in jobs], c.group_size,
-                               c.n_kv_heads, num_m, include_self=include_self)
+                               c.n_kv_heads, num_m, include_self=include_self, subsets=subsets)
         emap, works, segs, merges = t["row_map"], t["works"], t["segs"], t["merges"]
         self.kv_tokens = t["kv_tokens"]
         self.n_works, self.n_segs, self.n_merge = len(works), len(segs), len(merges)
@@ -1033,14 +1035,19 @@ class ChunkMajorSchedule:
 
 
 def chunk_major_tables(tables, n_new, pos_host, aux_row0, prefixes, gs: int, hkv: int, num_m: int = 2,
-                       include_self: bool = True) -> dict:
+                       include_self: bool = True, subsets=None) -> dict:
     """Host tables of a chunk-major K3 launch (ChunkMajorSchedule), vectorised
     numpy: the row map, works (chunk works kv-major then balanced row slices,
     then each query's SELF works), segments (one FULL per distinct chunk, one
     SELF per query slab) and the K3m merge groups.  include_self=False (a C5
     shard that is not the self rank): no SELF works, so a query's splits are
     its local chunks alone (possibly none: its merge then yields O = 0, LSE =
-    -inf)."""
+    -inf).
+
+    subsets (per job, ascending local token indices): only those tokens' rows
+    (the last layer of a scored forward needs the scored rows alone).  Their
+    own-token (SELF) works then go through the row map too, and the merge
+    groups write a COMPACT output: the kept tokens back to back in job order."""
     slab = (128 * num_m) // gs
     if slab < 1:
         raise ConfigError(f"group size {gs} exceeds the {128 * num_m} rows of one K3 work")
@@ -1048,10 +1055,18 @@ def chunk_major_tables(tables, n_new, pos_host, aux_row0, prefixes, gs: int, hkv
     pos = np.asarray(pos_host, np.int64)
     n_new = np.asarray(n_new, np.int64)
     tok0 = np.concatenate([[0], np.cumsum(n_new)[:-1]]).astype(np.int64)
+    if subsets is None:
+        ns = n_new
+        sub_cat = np.concatenate([np.arange(n, dtype=np.int64) for n in n_new]) if n_jobs else np.zeros(0, np.int64)
+    else:
+        subs = [np.asarray(x, np.int64) for x in subsets]
+        ns = np.array([len(x) for x in subs], np.int64)
+        sub_cat = np.concatenate(subs) if n_jobs else np.zeros(0, np.int64)
+    sub_off = np.concatenate([[0], np.cumsum(ns)[:-1]]).astype(np.int64)  # job's first kept token (compact)
     tabs = [np.asarray(t, dtype=np.int64).reshape(-1, 3) for t in tables]
     n_ch = np.array([len(t) for t in tabs], np.int64)
     n_split = n_ch + int(include_self)
-    tokbase = np.concatenate([[0], np.cumsum(n_split * n_new)])
+    tokbase = np.concatenate([[0], np.cumsum(n_split * ns)])
     kv_rows = int(tokbase[-1]) * gs  # partial rows per kv head
     # ---- (query, chunk) pairs grouped by chunk (pool row, length), queries ascending
     qi = np.repeat(np.arange(n_jobs), n_ch)
@@ -1059,18 +1074,19 @@ def chunk_major_tables(tables, n_new, pos_host, aux_row0, prefixes, gs: int, hkv
     sidx = np.arange(len(qi)) - np.repeat(np.cumsum(n_ch) - n_ch, n_ch)
     order = np.lexsort((qi, ch[:, 1], ch[:, 0]))
     qi, ch, sidx = qi[order], ch[order], sidx[order]
-    # ---- row-map entries: every (pair, token) in pair order
-    ne = n_new[qi]
+    # ---- row-map entries: every (pair, kept token) in pair order
+    ne = ns[qi]
     pair_e0 = np.cumsum(ne) - ne
     rep = np.repeat(np.arange(len(qi)), ne)
     local = np.arange(int(ne.sum())) - pair_e0[rep]
     q_rep = qi[rep]
-    tok = tok0[q_rep] + local
-    emap = np.zeros((max(len(tok), 1), 4), np.int32)
+    tok = tok0[q_rep] + sub_cat[sub_off[q_rep] + local]
+    n_self_e = int(ns.sum()) if (subsets is not None and include_self) else 0
+    emap = np.zeros((max(len(tok) + n_self_e, 1), 4), np.int32)
     if len(tok):
         emap[: len(tok), 0] = tok
         emap[: len(tok), 1] = pos[tok] - ch[rep, 2]
-        emap[: len(tok), 2] = tokbase[q_rep] + sidx[rep] * n_new[q_rep] + local
+        emap[: len(tok), 2] = tokbase[q_rep] + sidx[rep] * ns[q_rep] + local
     # ---- one FULL segment + works per distinct chunk: kv-major, then balanced slices
     if len(qi):
         newkey = np.r_[True, (ch[1:, 0] != ch[:-1, 0]) | (ch[1:, 1] != ch[:-1, 1])]
@@ -1103,40 +1119,55 @@ def chunk_major_tables(tables, n_new, pos_host, aux_row0, prefixes, gs: int, hkv
         cseg = np.zeros(0, dtype=ops.SEG_DTYPE)
         n_keys = 0
     # ---- SELF works (each query's own tokens, causal tree) into its last split
-    ks = -(-n_new // slab) * int(include_self)
-    ssize = -(-n_new // np.maximum(ks, 1))
+    ks = -(-ns // slab) * int(include_self)
+    ssize = -(-ns // np.maximum(ks, 1))
     sq = np.repeat(np.arange(n_jobs), ks)
     st0 = (np.arange(int(ks.sum())) - np.repeat(np.cumsum(ks) - ks, ks)) * ssize[sq]
-    sn = np.minimum(ssize[sq], n_new[sq] - st0)
+    sn = np.minimum(ssize[sq], ns[sq] - st0)
     sseg = np.zeros(len(sq), dtype=ops.SEG_DTYPE)
     sseg["src"] = 1
     sseg["row0"] = np.asarray(aux_row0, np.int64)[sq]
-    sseg["n_tok"] = st0 + sn
     sseg["kind"] = SEG_SELF
     prefix = np.asarray(prefixes, np.int64)
     sw = np.zeros((len(sq), hkv), dtype=ops.WORK_DTYPE)
     kvs = np.arange(hkv)[None, :]
-    sw["q_tok0"] = (tok0[sq] + st0)[:, None]
     sw["n_tok"] = sn[:, None]
     sw["self_tok0"] = tok0[sq][:, None]
     sw["kv_head"] = kvs
     sw["seg_begin"] = (n_keys + np.arange(len(sq)))[:, None]
     sw["seg_end"] = sw["seg_begin"] + 1
     sw["prefix"] = prefix[sq][:, None]
-    sw["out_mode"] = nat.OUT_PARTIAL
-    sw["part_row0"] = kvs * kv_rows + ((tokbase[sq] + n_ch[sq] * n_new[sq] + st0) * gs)[:, None]
+    if subsets is None:
+        sseg["n_tok"] = st0 + sn  # the slab's keys: up to its last token
+        sw["q_tok0"] = (tok0[sq] + st0)[:, None]
+        sw["out_mode"] = nat.OUT_PARTIAL
+        sw["part_row0"] = kvs * kv_rows + ((tokbase[sq] + n_ch[sq] * ns[sq] + st0) * gs)[:, None]
+    elif n_self_e:
+        # kept tokens' own rows through the row map (entries after the chunk pairs')
+        e_self0 = len(tok) + sub_off  # first SELF entry of each job
+        sj = np.repeat(np.arange(n_jobs), ns)
+        sl_local = np.arange(n_self_e) - sub_off[sj]
+        stok = tok0[sj] + sub_cat
+        emap[len(tok): len(tok) + n_self_e, 0] = stok
+        emap[len(tok): len(tok) + n_self_e, 1] = pos[stok]
+        emap[len(tok): len(tok) + n_self_e, 2] = tokbase[sj] + n_ch[sj] * ns[sj] + sl_local
+        last_local = sub_cat[sub_off[sq] + st0 + sn - 1]
+        sseg["n_tok"] = last_local + 1  # keys up to the slab's last kept token
+        sw["q_tok0"] = (e_self0[sq] + st0)[:, None]
+        sw["out_mode"] = nat.OUT_MAPPED
+        sw["part_row0"] = kvs * kv_rows
     works = np.concatenate([cw, sw.reshape(-1)])
     segs = np.concatenate([cseg, sseg])
     mg = np.zeros((n_jobs, hkv), dtype=ops.MERGE_DTYPE)
     mg["part_row0"] = kvs * kv_rows + (tokbase[:-1] * gs)[:, None]
-    mg["rows"] = (n_new * gs)[:, None]
+    mg["rows"] = (ns * gs)[:, None]
     mg["n_splits"] = n_split[:, None]
-    mg["q_tok0"] = tok0[:, None]
+    mg["q_tok0"] = (tok0 if subsets is None else sub_off)[:, None]
     mg["kv_head"] = kvs
     merges = mg.reshape(-1)
     return {"row_map": emap, "works": works, "segs": segs, "merges": merges,
             "kv_tokens": int(ch[:, 1].sum()) if len(qi) else 0,
-            "max_rows": int((n_new * gs).max()) if n_jobs else 0, "part_rows": kv_rows * hkv}
+            "max_rows": int((ns * gs).max()) if n_jobs else 0, "part_rows": kv_rows * hkv}
 
 
 def stage2_schedule_kind(n_jobs: int) -> str:
@@ -1150,16 +1181,43 @@ def stage2_schedule_kind(n_jobs: int) -> str:
     return "chunk" if n_jobs >= 8 else "query"
 
 
+def scored_local_rows(jobs):
+    """Per label job, the ascending local indices of its scored rows (the rows
+    LabelScorer keeps: the last query token and every fed label token,
+    model.py:441-443 via label_job), i.e. the rows the last layer must produce."""
+    out = []
+    for j in jobs:
+        rows = {j.prefix - 1}
+        off = j.prefix
+        for lab in j.labels:
+            rows.update(range(off, off + len(lab) - 1))
+            off += len(lab) - 1
+        out.append(np.array(sorted(rows), np.int64))
+    return out
+
+
+def _last_layer_subset_enabled() -> bool:
+    import os
+
+    return os.environ.get("DBSA_LAST_SUBSET", "1") != "0"
+
+
 class Stage2Plan:
     """Single-device tables for a batch of QueryJobs: NewTokens + a K3
     schedule over the jobs' chunk tables (chunk-major for batches, split-KV
-    per query otherwise; see stage2_schedule_kind)."""
+    per query otherwise; see stage2_schedule_kind).  A chunk-major plan of
+    label jobs also holds `last`: the last layer's schedule over the scored
+    rows alone (chunk_major_tables subsets), whose merge writes them compactly
+    in LabelScorer.keep order; `last` is None otherwise."""
 
     def __init__(self, dm, jobs, target_ctas: int | None = None, order: str = "query", schedule: str | None = None):
         self.new = NewTokens(dm, jobs)
         self.schedule = schedule or stage2_schedule_kind(len(jobs))
+        self.last = None
         if self.schedule == "chunk":
             self.sched = ChunkMajorSchedule(dm, jobs, self.new)
+            if jobs and all(j.labels is not None for j in jobs) and _last_layer_subset_enabled():
+                self.last = ChunkMajorSchedule(dm, jobs, self.new, subsets=scored_local_rows(jobs))
         else:
             self.sched = AttnSchedule(dm, jobs, self.new, target_ctas=target_ctas, order=order)
         for name in ("tok0", "n_tok", "num_m", "pos", "lo", "ids", "pages", "n_pages", "aux_rows"):
@@ -1226,10 +1284,14 @@ def run_jobs(dm, store, jobs, target_ctas=None, plan=None, keep=None):
                      nt.v_aux, nt.aux_rows, 1, 0, c.n_kv_heads, c.head_dim)
 
     def attend(layer, qkv, out):
-        sched.launch(dm, nt, layer, qkv, out, pool)
-        if sched.n_merge:
-            ops.lse_merge(sched.part_o, sched.part_lse, sched.merges, sched.n_merge, sched.max_rows, c.n_heads,
+        # last layer of a scored forward: the scored rows alone, compact in keep order
+        compact = keep is not None and plan.last is not None and layer == c.n_layers - 1
+        sc = plan.last if compact else sched
+        sc.launch(dm, nt, layer, qkv, out, pool)
+        if sc.n_merge:
+            ops.lse_merge(sc.part_o, sc.part_lse, sc.merges, sc.n_merge, sc.max_rows, c.n_heads,
                           c.n_kv_heads, c.head_dim, out, qw)
+        return compact
 
     h = _decoder(dm, nt.ids, attend, write_kv, keep_last=keep)
     return plan, h
@@ -1443,6 +1505,10 @@ class GraphedStage2:
                 nw, ns = max(sc.n_real_works, capacity[0]), max(sc.n_real_segs, capacity[1])
             sc.pad_to(-(-nw // 64) * 64, -(-ns // 16) * 16)
             plan.works, plan.n_works, plan.segs, plan.n_segs = sc.works, sc.n_works, sc.segs, sc.n_segs
+            if plan.last is not None:  # the last layer's scored-rows schedule, same headroom
+                la = plan.last
+                nw, ns = la.n_real_works * 17 // 16 + 64, la.n_real_segs * 17 // 16 + 16
+                la.pad_to(-(-nw // 64) * 64, -(-ns // 16) * 16)
         else:
             # replay() copies later batches' tables into these buffers: they must not be
             # the shared split-KV template tensors (AttnSchedule._from_template)
@@ -1477,6 +1543,8 @@ class GraphedStage2:
                      (self.scorer.keep, scorer.keep), (self.scorer.rows_in_keep, scorer.rows_in_keep)]
             if isinstance(t.sched, ChunkMajorSchedule):
                 t.sched.copy_tables_from(n.sched)
+                if t.last is not None:
+                    t.last.copy_tables_from(n.last)
             else:
                 pairs += [(t.sched.works, n.sched.works), (t.sched.segs, n.sched.segs)]
                 if t.sched.cta_works is not None:
@@ -1498,7 +1566,7 @@ def plan_key(plan, scorer):
     instead (GraphedStage2 pads them)."""
     sc = plan.sched
     if isinstance(sc, ChunkMajorSchedule):
-        tables = ("chunk", sc.row_map.numel(), sc.num_m)
+        tables = ("chunk", sc.row_map.numel(), sc.num_m, plan.last.row_map.numel() if plan.last is not None else -1)
     else:
         tables = ("query", sc.n_works, sc.n_segs, sc.n_ctas)
     return (plan.new.n_tok, tuple(plan.new.n_new), plan.new.n_pages, tables, sc.n_merge, sc.part_rows,
@@ -1515,7 +1583,9 @@ def fits_graph(graph, plan) -> bool:
         return False
     if not isinstance(sc, ChunkMajorSchedule):
         return True
-    return sc.n_real_works <= t.n_works and sc.n_real_segs <= t.n_segs
+    last_fits = plan.last is None or (plan.last.n_real_works <= graph.plan.last.n_works
+                                      and plan.last.n_real_segs <= graph.plan.last.n_segs)
+    return sc.n_real_works <= t.n_works and sc.n_real_segs <= t.n_segs and last_fits
 
 
 def _final_logits(dm, h_rows):
