@@ -765,6 +765,9 @@ def c1_end_to_end(dev):
     out = runner.infer_batch([q for q, _ in tests])
     torch.cuda.synchronize()
     gpu_inf = time.perf_counter() - t0
+    for _ in range(2):  # steady state: a launch shape is captured the second time it is seen
+        [runner.infer(q) for q, _ in tests[:8]]
+    torch.cuda.synchronize()
     t0 = time.perf_counter()
     single = [runner.infer(q)[0] for q, _ in tests[:8]]
     gpu_single = (time.perf_counter() - t0) / 8

@@ -596,6 +596,23 @@ def label_job(chunks, n_ctx, query_ids, labels) -> QueryJob:
     return QueryJob(chunks, n_ctx, ids, pos, lo, nq, [list(x) for x in labels])
 
 
+def pad_job(job: QueryJob, n_tok: int, max_seq_len: int) -> QueryJob:
+    """`job` with dummy tokens appended up to n_tok new tokens: one more tree
+    branch after the labels (positions after the job's last, visible to
+    nothing but itself), so every real token's keys, outputs and label scores
+    are unchanged; only the launch shape is.  Returned as is when already
+    long enough or when the padding would pass max_seq_len."""
+    d = n_tok - len(job.ids)
+    if d <= 0:
+        return job
+    p0 = max(job.pos) + 1
+    if job.n_ctx + p0 + d > max_seq_len:
+        return job
+    start = len(job.ids)
+    return QueryJob(job.chunks, job.n_ctx, list(job.ids) + [0] * d, list(job.pos) + list(range(p0, p0 + d)),
+                    list(job.lo) + [start] * d, job.prefix, job.labels)
+
+
 class NewTokens:
     """The new (query / label) tokens of a stage-2 batch: ids, rotary positions,
     tree bounds and their K/V pages (one aux page set, page-aligned per job)."""
