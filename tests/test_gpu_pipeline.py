@@ -84,14 +84,17 @@ def test_stage1_whole_cache_vs_oracle_c1():
     assert worst < KV_TOL, worst
 
 
-@pytest.mark.parametrize("split", ["packed-bf16", "packed-fp32", "round-robin-fp32"])
+@pytest.mark.parametrize("split", ["packed-bf16", "packed-fp32", "round-robin-fp32", "packed-bf16-pad16"])
 @pytest.mark.parametrize("name", CASES)
 def test_stage2_runner_matches_reference(name, split, monkeypatch):
     """Runner.infer / score_label per query against the reference goldens,
     through the split-KV schedule as shipped (cost-packed CTA ranges, SELF as
-    its own split, bf16 partials) and its fp32 / round-robin variants."""
+    its own split, bf16 partials, queries padded by a dummy tree branch to a
+    multiple of 4 tokens), its fp32 / round-robin variants, and 16-token
+    padding."""
     monkeypatch.setenv("DBSA_PACK", "0" if split.startswith("round-robin") else "1")
-    monkeypatch.setenv("DBSA_SPLIT_BF16", "1" if split.endswith("bf16") else "0")
+    monkeypatch.setenv("DBSA_SPLIT_BF16", "1" if "bf16" in split else "0")
+    monkeypatch.setattr(P.Stage2Session, "PAD_TOKENS", 16 if split.endswith("pad16") else 4)
     meta, a, w, task, mc, enc = _encoded(name)
     runner = P.Runner(w, enc.cache, enc.index, task, mc)
     runner.prepare()
