@@ -59,8 +59,8 @@ __device__ __forceinline__ void merge_store_lse(const DbsaMergeArgs &a, int t, i
 
 template <bool BF16, bool LATENCY>
 __global__ void lse_merge_kernel(DbsaMergeArgs a) {
-  const DbsaMergeGroup g = a.groups[blockIdx.y];  // host-written table: read before the PDL wait
   pdl_wait();
+  const DbsaMergeGroup g = a.groups[blockIdx.y];
   const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (r >= g.rows) return;
@@ -264,14 +264,14 @@ __global__ void rmsnorm4_kernel(float *x, const float *delta, const float *w, __
   float4 *xr = reinterpret_cast<float4 *>(x + row * dim);
   const int n4 = (int)(dim >> 2);
   float4 v[VPT], ww[VPT];
-  // the weights are not written by the predecessor: their loads go out before
-  // the PDL wait and are in registers by the scale pass
+  pdl_wait();
+  // the weight loads go out with the row's (not after the reduction), so
+  // they are in registers by the scale pass
 #pragma unroll
   for (int k = 0; k < VPT; ++k) {
     const int i = threadIdx.x + k * blockDim.x;
     if (i < n4) ww[k] = __ldg(reinterpret_cast<const float4 *>(w) + i);
   }
-  pdl_wait();
   float ss = 0.f;
 #pragma unroll
   for (int k = 0; k < VPT; ++k) {
