@@ -4,6 +4,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <cstdlib>
 #include <utility>
@@ -47,14 +48,20 @@ inline bool pdl_enabled() {
 // 0 disables).
 constexpr size_t kPersistMaxBytes = 8u << 20;     // activations kept resident (the residual stream)
 constexpr size_t kWindowMaxBytes = 128u << 20;     // cudaDevAttrMaxAccessPolicyWindowSize on B200
-inline bool l2_persist_ready() {
-  static const bool ok = [] {
+inline bool l2_persist_ready(cudaStream_t s) {
+  // set once, outside any stream capture (a device-wide call there could
+  // invalidate the capture); until then launches go without the window
+  static std::atomic<int> state{0};  // 0 not yet, 1 set, -1 off / failed
+  if (state.load() == 0) {
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) return false;
     const char *e = getenv("DBSA_L2_PERSIST_MB");
     const size_t mb = e ? (size_t)atoi(e) : 16;
-    if (!mb) return false;
-    return cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, mb << 20) == cudaSuccess;
-  }();
-  return ok;
+    const bool ok = mb && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, mb << 20) == cudaSuccess;
+    if (!ok) cudaGetLastError();  // clear a failed call's error
+    state.store(ok ? 1 : -1);
+  }
+  return state.load() > 0;
 }
 
 struct Persist {
@@ -77,7 +84,7 @@ inline cudaError_t launch_kp(void (*kern)(KArgs...), dim3 grid, dim3 block, size
     at[n].val.programmaticStreamSerializationAllowed = 1;
     ++n;
   }
-  if (keep.base && keep.bytes && keep.bytes <= kWindowMaxBytes && l2_persist_ready()) {
+  if (keep.base && keep.bytes && keep.bytes <= kWindowMaxBytes && l2_persist_ready(s)) {
     at[n].id = cudaLaunchAttributeAccessPolicyWindow;
     at[n].val.accessPolicyWindow.base_ptr = const_cast<void *>(keep.base);
     at[n].val.accessPolicyWindow.num_bytes = keep.bytes;
