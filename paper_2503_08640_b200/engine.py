@@ -687,8 +687,18 @@ class NewTokens:
         return (self.k_aux, self.v_aux, self.aux_rows, 1)
 
 
-_SPLIT_TEMPLATES = __import__("collections").OrderedDict()  # split-KV table templates (AttnSchedule), LRU
+# Split-KV table templates (AttnSchedule), LRU, per thread: a template's device
+# tables are then only ever used on that thread's stream (Runner.infer gives
+# each thread its own), so eviction cannot free a block another stream reads.
+_SPLIT_TLS = __import__("threading").local()
 _SPLIT_TEMPLATES_MAX = 64
+
+
+def _split_templates():
+    d = getattr(_SPLIT_TLS, "cache", None)
+    if d is None:
+        d = _SPLIT_TLS.cache = __import__("collections").OrderedDict()
+    return d
 
 
 def _split_bf16() -> bool:
@@ -735,9 +745,10 @@ class AttnSchedule:
                          for t in tables),
                    tuple(int(x) for x in nt.n_new), tuple(int(j.prefix) for j in jobs), nt.num_m, include_self,
                    pack, target, gs, hkv, hd, c.n_layers, str(dev), _split_bf16())
-            tpl = _SPLIT_TEMPLATES.get(key)
+            templates = _split_templates()
+            tpl = templates.get(key)
             if tpl is not None:
-                _SPLIT_TEMPLATES.move_to_end(key)
+                templates.move_to_end(key)
                 self._from_template(dm, nt, tables, tpl)
                 return
         segs, works, merges = [], [], []
@@ -821,12 +832,13 @@ class AttnSchedule:
         self._part = None
         if key is not None:
             src = np.asarray(seg_src, np.int64).reshape(-1, 2)
-            _SPLIT_TEMPLATES[key] = dict(
+            templates = _split_templates()
+            templates[key] = dict(
                 works=self.works, merges=self.merges, cta_works=self.cta_works, n_ctas=self.n_ctas, segs=seg_arr,
                 seg_job=src[:, 0], seg_chunk=src[:, 1], n_works=self.n_works, n_merge=self.n_merge,
                 max_rows=self.max_rows, part_rows=part_rows, kv_tokens=kv_tok, part_dtype=self._part_spec[2])
-            while len(_SPLIT_TEMPLATES) > _SPLIT_TEMPLATES_MAX:
-                _SPLIT_TEMPLATES.popitem(last=False)
+            while len(templates) > _SPLIT_TEMPLATES_MAX:
+                templates.popitem(last=False)
 
     def _from_template(self, dm, nt, tables, tpl):
         """This batch's split-KV tables from a cached template: the works, merge
