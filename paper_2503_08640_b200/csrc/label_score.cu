@@ -229,39 +229,38 @@ __global__ void __launch_bounds__(kLsThreads, 1)
   if (warp == 2) tmem_dealloc(tbase, 512);
 }
 
-// One warp per scored (row, target) pair: the row's LSE (natural log) from its
-// per-tile partials, and the target logit as a dot product of the same bf16
-// operands with fp32 accumulation; out = logit - LSE.
-__global__ void label_pair_logprob_kernel(const float2 *part, int n_tiles, int64_t rows_pad,
-                                          const __nv_bfloat16 *x, const __nv_bfloat16 *w, int64_t d,
-                                          const int64_t *pair_row, const int32_t *pair_target, int64_t n_pairs,
-                                          float *out) {
-  const int64_t i = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (i >= n_pairs) return;
+// One CTA per scored (row, target) pair: the row's LSE (natural log) from its
+// per-128-column partials (each thread folds a strided share, then warp and
+// block combines), and the target logit as a dot product of the same bf16
+// operands with fp32 accumulation; out = logit - LSE.  A whole CTA per pair
+// keeps the ~1,000 partial loads of a Llama-vocab row in flight together
+// (a warp per pair took ~15 us at batch 1, latency-bound).
+__device__ __forceinline__ void lse_fold(float &m, float &s, float m2, float s2) {
+  const float mn = fmaxf(m, m2);
+  if (mn != -INFINITY) {
+    s = (m == -INFINITY ? 0.f : s * exp2f(m - mn)) + (m2 == -INFINITY ? 0.f : s2 * exp2f(m2 - mn));
+    m = mn;
+  }
+}
+
+__global__ void __launch_bounds__(256) label_pair_logprob_kernel(const float2 *part, int n_tiles, int64_t rows_pad,
+                                                                 const __nv_bfloat16 *x, const __nv_bfloat16 *w,
+                                                                 int64_t d, const int64_t *pair_row,
+                                                                 const int32_t *pair_target, int64_t n_pairs,
+                                                                 float *out) {
+  __shared__ float red_m[8], red_s[8], red_dot[8];
+  const int64_t i = blockIdx.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t row = pair_row[i];
   const int64_t tgt = pair_target[i];
   float m = -INFINITY, s = 0.f;
-  for (int j = lane; j < n_tiles; j += 32) {
+  for (int j = threadIdx.x; j < n_tiles; j += blockDim.x) {
     const float2 q = part[(int64_t)j * rows_pad + row];
-    const float mn = fmaxf(m, q.x);
-    if (mn != -INFINITY) {
-      s = (m == -INFINITY ? 0.f : s * exp2f(m - mn)) + (q.x == -INFINITY ? 0.f : q.y * exp2f(q.x - mn));
-      m = mn;
-    }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, s, o);
-    const float mn = fmaxf(m, m2);
-    if (mn != -INFINITY) {
-      s = (m == -INFINITY ? 0.f : s * exp2f(m - mn)) + (m2 == -INFINITY ? 0.f : s2 * exp2f(m2 - mn));
-      m = mn;
-    }
+    lse_fold(m, s, q.x, q.y);
   }
   const __nv_bfloat16 *xr = x + row * d, *wr = w + tgt * d;
   float acc = 0.f;
-  for (int64_t c = lane * 8; c < d; c += 256) {
+  for (int64_t c = (int64_t)threadIdx.x * 8; c < d; c += (int64_t)blockDim.x * 8) {
     const uint4 a = *reinterpret_cast<const uint4 *>(xr + c), b = *reinterpret_cast<const uint4 *>(wr + c);
     const __nv_bfloat162 *a2 = reinterpret_cast<const __nv_bfloat162 *>(&a);
     const __nv_bfloat162 *b2 = reinterpret_cast<const __nv_bfloat162 *>(&b);
@@ -273,8 +272,20 @@ __global__ void label_pair_logprob_kernel(const float2 *part, int n_tiles, int64
     }
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (lane == 0) out[i] = acc - (m + log2f(s)) * 0.69314718055994531f;
+  for (int o = 16; o > 0; o >>= 1) {
+    lse_fold(m, s, __shfl_xor_sync(0xffffffffu, m, o), __shfl_xor_sync(0xffffffffu, s, o));
+    acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  }
+  if (lane == 0) red_m[wid] = m, red_s[wid] = s, red_dot[wid] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float mm = -INFINITY, ss = 0.f, dot = 0.f;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) {
+      lse_fold(mm, ss, red_m[k], red_s[k]);
+      dot += red_dot[k];
+    }
+    out[i] = dot - (mm + log2f(ss)) * 0.69314718055994531f;
+  }
 }
 
 static int num_sms_ls() {
@@ -348,8 +359,7 @@ extern "C" int dbsa_label_score(const DbsaLabelScoreArgs *args, void *stream) {
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int grid = p.n_work < num_sms_ls() ? p.n_work : num_sms_ls();
   if (int rc = narrow ? launch_lse<128, true>(grid, maps, p, s) : launch_lse<256, false>(grid, maps, p, s)) return rc;
-  const int64_t blocks = (a.n_pairs + 7) / 8;
-  label_pair_logprob_kernel<<<(unsigned)blocks, 256, 0, s>>>(
+  label_pair_logprob_kernel<<<(unsigned)a.n_pairs, 256, 0, s>>>(
       p.part, (int)((a.vocab + kLsHalf - 1) / kLsHalf), p.rows_pad, reinterpret_cast<const __nv_bfloat16 *>(a.x),
       reinterpret_cast<const __nv_bfloat16 *>(a.w), a.d, a.pair_row, a.pair_target, a.n_pairs, a.out);
   return check_launch("label_pair_logprob");
