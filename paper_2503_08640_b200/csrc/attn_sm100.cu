@@ -49,11 +49,6 @@ constexpr int kBN = 128;  // keys per tile
 #ifndef DBSA_QSTAGE_BATCH
 #define DBSA_QSTAGE_BATCH 4
 #endif
-// experiment: the producer holds the K/V stream after the first K tile until
-// the first work's Q is staged
-#ifndef DBSA_QGATE
-#define DBSA_QGATE 0
-#endif
 #ifndef DBSA_RESCALE_LOG2
 #define DBSA_RESCALE_LOG2 8.f
 #endif
@@ -141,7 +136,6 @@ struct AttnParams {
   float *part_lse;
   const DbsaRowMap *row_map;
   int part_bf16;  // out_mode DBSA_OUT_MAPPED works: q_tok0 indexes this map
-  int l2_prefetch;  // producer prefetches each segment's later tiles into L2 (split-KV / latency launches)
   int dbg;  // profiling switches (DBSA_DEBUG_MODE): 1 = skip softmax math, 2 = skip MMAs, 4 = skip TMA loads,
             // 8 = skip epilogue stores, 16 = skip Q staging (two-tile kernel)
   unsigned long long *pair_count;  // optional: (row, key) pairs that entered the softmax (all heads)
@@ -623,7 +617,6 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
         }
         ++vj;
       };
-      bool gated = !(DBSA_QGATE);
       for (int wi = wr.begin; wi < wr.end; wi += wr.step) {
         const DbsaAttnWork w = p.works[wi];
         for (int si = w.seg_begin; si < w.seg_end; ++si) {
@@ -631,30 +624,9 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
           const int off = sg.row0 & 63;  // tiles start on 64-row page boundaries
           const int nt = (off + sg.n_tok + kBN - 1) / kBN;
           const CUtensorMap *tk = sg.src ? &tm_k1 : &tm_k0;
-          auto prefetch_seg = [&]() {
-            // split-KV (latency) schedules: the segment's later tiles go to L2 now,
-            // so the ring refills from L2 instead of waiting a DRAM round trip
-            if (!p.l2_prefetch || (p.dbg & 4)) return;
-            const CUtensorMap *tv = sg.src ? &tm_v1 : &tm_v0;
-            for (int tt = C::KST; tt < nt; ++tt) {
-              const int row = sg.row0 - off + tt * kBN;
-#pragma unroll
-              for (int a = 0; a < C::NATOM; ++a) tma_prefetch_l2_4d(tk, a * C::KATOM, row, w.kv_head, sg.layer);
-#pragma unroll
-              for (int a = 0; a < 2; ++a) tma_prefetch_l2_4d(tv, row + a * 64, 0, w.kv_head, sg.layer);
-            }
-          };
-          if (gated) prefetch_seg();
           for (int tt = 0; tt < nt; ++tt) {
             const int row = sg.row0 - off + tt * kBN;
             const int st = kj % C::KST;
-            if (!gated && kj == 1) {
-              // first work: let the softmax warps' Q loads through before the
-              // K/V stream fills the memory system
-              for (int m = 0; m < NUM_M; ++m) mbar_wait(&q_full[m], 0);
-              gated = true;
-              prefetch_seg();
-            }
             if (kj >= C::KST) mbar_wait(&k_empty[st], ((kj / C::KST) & 1) ^ 1);
             if (p.dbg & 4) {
               mbar_arrive(&k_full[st]);
@@ -1577,12 +1549,7 @@ extern "C" int dbsa_attention(const DbsaAttnArgs *args, void *stream) {
       const char *e = getenv("DBSA_DEBUG_MODE");
       return e ? atoi(e) : 0;
     }();
-    static const int l2pf = [] {
-      const char *e = getenv("DBSA_L2PF");
-      return e ? atoi(e) : 0;
-    }();
     p.dbg = dbg;
-    p.l2_prefetch = l2pf;
   }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   // num_m 1 runs the single-M-tile kernel (Q in TMEM, double-buffered S) unless
