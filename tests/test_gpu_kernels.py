@@ -530,12 +530,16 @@ def _rope64_t(x, pos, theta):
     return torch.cat([lo * c - hi * s, lo * s + hi * c], dim=-1)
 
 
-def _stage2_at_scale(H, Hkv, hd, theta, n_groups, group_tok, budget, n_queries, q_tok, labels, check, seed=0):
-    """One layer of K3 (chunk-major, bf16 partials) + K3m at a north-star
-    shape against float64 attention over the ASSEMBLED context: selected
-    groups' keys rotated at their new positions 0..T'-1 (kvstore.assemble,
-    kvstore.py:188-221), queries at their own positions T'+i, the query/label
-    tree mask (model.py:381-392), softmax in float64 (kernels.py:43-100)."""
+def _stage2_at_scale(H, Hkv, hd, theta, n_groups, group_tok, budget, n_queries, q_tok, labels, check, seed=0,
+                     mode="chunk"):
+    """One layer of K3 + K3m at a north-star shape against float64 attention
+    over the ASSEMBLED context: selected groups' keys rotated at their new
+    positions 0..T'-1 (kvstore.assemble, kvstore.py:188-221), queries at their
+    own positions T'+i, the query/label tree mask (model.py:381-392), softmax
+    in float64 (kernels.py:43-100).  mode: "chunk" (chunk-major, bf16
+    partials), "chunk-last" (the last layer's schedule over the scored rows
+    only: mapped SELF works, compact output), "query" (split-KV as Runner.infer
+    runs it: cost-packed CTA ranges, SELF as its own split, bf16 partials)."""
     import paper_2503_08640_b200 as P
     from paper_2503_08640_b200 import engine
 
@@ -566,18 +570,22 @@ def _stage2_at_scale(H, Hkv, hd, theta, n_groups, group_tok, budget, n_queries, 
         labs = [rng.integers(3, 200, labels[1]).tolist() for _ in range(labels[0])]
         jobs.append(engine.label_job(tab, int(ln.sum()), q_ids, labs))
         picks.append(pick)
-    plan = engine.Stage2Plan(dm, jobs, schedule="chunk")
-    assert plan.sched.part_o.dtype == torch.bfloat16
+    plan = engine.Stage2Plan(dm, jobs, schedule="query" if mode == "query" else "chunk")
+    sched = plan.last if mode == "chunk-last" else plan.sched
+    assert sched is not None and sched.part_o.dtype == torch.bfloat16
+    if mode == "query":
+        assert sched.cta_works is not None
     nt = plan.new
     qw, kw = H * hd, Hkv * hd
     qkv = (torch.randn(nt.n_tok, qw + 2 * kw, generator=g, device=dev) * 0.5).to(torch.bfloat16)
     ops.kv_write(qkv[:, qw:], qkv[:, qw + kw:], qw + 2 * kw, nt.pos, dm.rope, nt.pages, nt.n_pages, nt.k_aux,
                  nt.v_aux, nt.aux_rows, 1, 0, Hkv, hd)
     out = torch.zeros(nt.n_tok, qw, dtype=torch.bfloat16, device=dev)
-    plan.sched.launch(dm, nt, 0, qkv, out, st.planes())
-    ops.lse_merge(plan.sched.part_o, plan.sched.part_lse, plan.sched.merges, plan.sched.n_merge,
-                  plan.sched.max_rows, H, Hkv, hd, out, qw)
+    sched.launch(dm, nt, 0, qkv, out, st.planes())
+    ops.lse_merge(sched.part_o, sched.part_lse, sched.merges, sched.n_merge, sched.max_rows, H, Hkv, hd, out, qw)
     torch.cuda.synchronize()
+    kept = engine.scored_local_rows(jobs)
+    koff = np.concatenate([[0], np.cumsum([len(x) for x in kept])])
     gs = H // Hkv
     scale = 1.0 / math.sqrt(hd)
     worst = 0.0
@@ -610,7 +618,12 @@ def _stage2_at_scale(H, Hkv, hd, theta, n_groups, group_tok, budget, n_queries, 
             s = torch.where(mask[None], s, -torch.inf)
             p_ = torch.softmax(s, dim=-1)
             want = p_ @ V[kv]  # [gs, n, hd]
-            got = out[t0:t0 + n].view(n, H, hd)[:, kv * gs:(kv + 1) * gs].transpose(0, 1).double()
+            if mode == "chunk-last":  # the kept rows, compact in job order
+                rows = out[koff[qi]:koff[qi + 1]].view(-1, H, hd)[:, kv * gs:(kv + 1) * gs].transpose(0, 1).double()
+                want = want[:, torch.as_tensor(kept[qi], device=dev)]
+                got = rows
+            else:
+                got = out[t0:t0 + n].view(n, H, hd)[:, kv * gs:(kv + 1) * gs].transpose(0, 1).double()
             worst = max(worst, float((got - want).abs().max()))
     return worst
 
@@ -621,6 +634,24 @@ def test_k3_at_c3_shape_vs_float64():
     key tiles per work stream and re-positioning deltas up to ~63k with rope
     rows up to 90k), 64 queries of 32 tokens + 4 labels x 4 tokens."""
     worst = _stage2_at_scale(32, 8, 128, 500000.0, 60, 1500, 18, 64, 32, (4, 4), check=[0, 17, 40, 63])
+    assert worst < 2e-2, worst
+
+
+def test_k3_last_layer_scored_rows_at_c3_shape_vs_float64():
+    """The last layer's schedule (Stage2Plan.last: scored rows only, SELF works
+    through the row map, compact merge output) at the C3 shape."""
+    worst = _stage2_at_scale(32, 8, 128, 500000.0, 60, 1500, 18, 64, 32, (4, 4), check=[0, 17, 40, 63],
+                             mode="chunk-last")
+    assert worst < 2e-2, worst
+
+
+@pytest.mark.parametrize("n_queries", [1, 3])
+def test_k3_split_packed_at_c3_shape_vs_float64(n_queries):
+    """Batch 1 (and 3) at the C3 shape through the split-KV schedule as
+    Runner.infer runs it: cost-packed CTA ranges (DbsaAttnArgs.cta_works), the
+    queries' own tokens as a split of their own, bf16 partials."""
+    worst = _stage2_at_scale(32, 8, 128, 500000.0, 60, 1500, 18, n_queries, 32, (4, 4),
+                             check=list(range(n_queries)), mode="query")
     assert worst < 2e-2, worst
 
 
