@@ -24,6 +24,7 @@ ap.add_argument("--order", default="query")
 ap.add_argument("--schedule", default=None, help="chunk | query (default: by batch size)")
 ap.add_argument("--chunk-m", type=int, default=2, help="M tiles per chunk-major work")
 ap.add_argument("--dense", action="store_true", help="one contiguous T' chunk per query")
+ap.add_argument("--dense-split", type=int, default=1, help="with --dense: the T' run as this many contiguous chunks")
 args = ap.parse_args()
 
 dev = torch.device("cuda", 0)
@@ -104,7 +105,9 @@ if args.stage in ("2", "both"):
     tabs, n_ctx = sess.chunks_for(ids)
     if args.dense:  # one contiguous run of T' pool rows per query (the dense comparator)
         Tp = int(n_ctx[0])
-        tabs = np.array([[[0, Tp, 0]]] * B, np.int64)
+        k = args.dense_split
+        cuts = [Tp * i // k for i in range(k + 1)]
+        tabs = np.array([[[cuts[i], cuts[i + 1] - cuts[i], 0] for i in range(k)]] * B, np.int64)
     jobs = [engine.label_job(tabs[i], int(n_ctx[i]), q[i], sess.label_ids) for i in range(B)]
     plan = engine.Stage2Plan(dm, jobs, args.target or None, args.order, schedule=args.schedule)
     if plan.schedule == "chunk" and args.chunk_m != 2:
