@@ -160,6 +160,25 @@ class Clocks:
                 "samples": len(sm)}
 
 
+def _local_device() -> int:
+    """This rank's GPU: LOCAL_RANK, or 0 for every rank with
+    DBSA_BENCH_SAME_GPU=1 (a functional check of the multi-rank flow on one
+    GPU, together with DBSA_BENCH_BACKEND=gloo; not a measurement)."""
+    if os.environ.get("DBSA_BENCH_SAME_GPU") == "1":
+        return 0
+    return int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def _init_dist(dev):
+    import torch.distributed as dist
+
+    backend = os.environ.get("DBSA_BENCH_BACKEND", "nccl")
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        dist.init_process_group(backend)
+
+
 class KernelTimer:
     """CUDA events around every launch of one kernel family, on its stream."""
 
@@ -217,13 +236,13 @@ def run_ours(args):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = _local_device()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator lines on stderr (one rank per GPU)
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-        dist.init_process_group("nccl", device_id=dev)
+        _init_dist(dev)
 
     cfg = P.ModelConfig(**CFG8B)
     dm = engine.DeviceModel.random(cfg, seed=0, device=dev)
@@ -582,11 +601,11 @@ def run_c5(args):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = _local_device()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        _init_dist(dev)
         comm = parallel.DistComm()
     else:
         comm = parallel.LocalComm(1)
