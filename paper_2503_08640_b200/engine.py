@@ -718,42 +718,22 @@ class AttnSchedule:
     key on this shard, always writing an fp32 partial + LSE at the canonical
     row block (NewTokens.part_base) -- the per-rank half of the C5 merge.
     include_self: whether this schedule covers the jobs' own tokens (SELF).
-    row_ranges (split mode): per job a contiguous local token range (lo, hi);
-    only those rows are computed (the last layer of a scored forward needs
-    the scored rows alone), the merge writes them COMPACTLY in job order, and
-    `compact` is False when a job's range has a single split (it would be
-    written in place instead): the caller then falls back to the full rows.
     """
 
     def __init__(self, dm, jobs, nt: NewTokens, chunk_tables=None, target_ctas=None, order="query",
-                 mode="split", include_self=True, pack=None, row_ranges=None):
+                 mode="split", include_self=True, pack=None):
         torch = _torch()
         c = dm.config
         gs, hkv, hd = c.group_size, c.n_kv_heads, c.head_dim
         tables = chunk_tables if chunk_tables is not None else [j.chunks for j in jobs]
         target = target_ctas or 4 * 148
-        self.num_m = nt.num_m
-        self.compact = row_ranges is not None
-        job_slabs, out_off = nt.slabs, None
-        if row_ranges is not None:
-            # slabs over each job's range, balanced as NewTokens balances whole jobs
-            self.num_m = m_tiles(max(hi - lo for lo, hi in row_ranges) * gs)
-            slab = (128 * self.num_m) // gs
-            job_slabs, out_off, acc = [], [], 0
-            for lo, hi in row_ranges:
-                n = hi - lo
-                k = -(-n // slab)
-                size = -(-n // k)
-                job_slabs.append([(lo + t0, min(size, n - t0)) for t0 in range(0, n, size)])
-                out_off.append(acc - lo)  # compact output row of local token lo
-                acc += n
         # pack: SELF becomes a split of its own and the works are packed onto the
         # CTAs by cost (pack_works), instead of SELF riding on the last chunk
         # split and round-robin placement (the one-wave tail of a latency launch)
         if pack is None:
             import os
 
-            pack = mode == "split" and self.num_m == 2 and os.environ.get("DBSA_PACK", "1") != "0"
+            pack = mode == "split" and nt.num_m == 2 and os.environ.get("DBSA_PACK", "1") != "0"
         self.pack = pack
         dev = dm.device
         # split-KV tables depend on the chunk LENGTHS (and page offsets), not on
@@ -764,8 +744,7 @@ class AttnSchedule:
             key = (tuple(tuple((int(r[1]), int(r[0]) % PAGE) for r in np.asarray(t, np.int64).reshape(-1, 3))
                          for t in tables),
                    tuple(int(x) for x in nt.n_new), tuple(int(j.prefix) for j in jobs), nt.num_m, include_self,
-                   pack, target, gs, hkv, hd, c.n_layers, str(dev), _split_bf16(),
-                   tuple(tuple(r) for r in row_ranges) if row_ranges is not None else None)
+                   pack, target, gs, hkv, hd, c.n_layers, str(dev), _split_bf16())
             templates = _split_templates()
             tpl = templates.get(key)
             if tpl is not None:
@@ -779,7 +758,7 @@ class AttnSchedule:
         kv_tok = 0
         for qi, j in enumerate(jobs):
             n = nt.n_new[qi]
-            slabs = job_slabs[qi]
+            slabs = nt.slabs[qi]
             ch = np.asarray(tables[qi], dtype=np.int64).reshape(-1, 3)
             kv_tok += int(ch[:, 1].sum()) if len(ch) else 0
             chunk_segs = []
@@ -821,8 +800,6 @@ class AttnSchedule:
                     segs.append((1, 0, int(nt.aux_row0[qi]), t0 + ntk, SEG_SELF, 0))
                     seg_src.append((qi, -1))
                 last = (last_sb, len(segs))
-                if n_split == 1:
-                    self.compact = False  # a single split writes its rows in place
                 for kv in range(hkv):
                     base = part_rows
                     mode_w = 1 if n_split > 1 else 0
@@ -830,8 +807,7 @@ class AttnSchedule:
                         sb, se = last if sp == n_split - 1 else split_ranges[sp]
                         works.append((q0 + t0, ntk, q0, kv, sb, se, j.prefix, mode_w, base + sp * rows))
                     if n_split > 1:
-                        merges.append((base, rows, n_split, (out_off[qi] + t0) if out_off is not None else q0 + t0,
-                                       kv))
+                        merges.append((base, rows, n_split, q0 + t0, kv))
                         part_rows += n_split * rows
         if order == "chunk":
             first_row = [segs[wk[4]][2] if wk[5] > wk[4] and segs[wk[4]][0] == 0 else 1 << 30 for wk in works]
@@ -860,8 +836,7 @@ class AttnSchedule:
             templates[key] = dict(
                 works=self.works, merges=self.merges, cta_works=self.cta_works, n_ctas=self.n_ctas, segs=seg_arr,
                 seg_job=src[:, 0], seg_chunk=src[:, 1], n_works=self.n_works, n_merge=self.n_merge,
-                max_rows=self.max_rows, part_rows=part_rows, kv_tokens=kv_tok, part_dtype=self._part_spec[2],
-                num_m=self.num_m, compact=self.compact)
+                max_rows=self.max_rows, part_rows=part_rows, kv_tokens=kv_tok, part_dtype=self._part_spec[2])
             while len(templates) > _SPLIT_TEMPLATES_MAX:
                 templates.popitem(last=False)
 
@@ -883,7 +858,6 @@ class AttnSchedule:
         segs["row0"][~full] = np.asarray(nt.aux_row0, np.int64)[job[~full]]
         min_shift = min(0, int(allch[:, 2].min())) if len(allch) else 0
         self.works, self.merges, self.cta_works, self.n_ctas = tpl["works"], tpl["merges"], tpl["cta_works"], tpl["n_ctas"]
-        self.num_m, self.compact = tpl["num_m"], tpl["compact"]
         self.n_works, self.n_segs, self.n_merge = tpl["n_works"], len(segs), tpl["n_merge"]
         self.segs = ops.to_device(_per_layer_segs(segs, c.n_layers), dm.device)
         self.max_rows, self.part_rows, self.kv_tokens = tpl["max_rows"], tpl["part_rows"], tpl["kv_tokens"]
@@ -921,7 +895,7 @@ class AttnSchedule:
             return
         ops.attention(q=qkv, q_tok_stride=qw + 2 * kw, tok_pos=nt.pos, tok_lo=nt.lo, rope=self.rope,
                       pool=pool, aux=nt.aux(), n_heads=c.n_heads, n_kv_heads=c.n_kv_heads, head_dim=c.head_dim,
-                      works_dev=self.works, n_works=self.n_works, segs_dev=self.segs_ptr(layer), num_m=self.num_m,
+                      works_dev=self.works, n_works=self.n_works, segs_dev=self.segs_ptr(layer), num_m=nt.num_m,
                       out=out, out_tok_stride=qw, part_o=self.part_o if part_o is None else part_o,
                       part_lse=self.part_lse if part_lse is None else part_lse, cta_works=self.cta_works,
                       n_ctas=self.n_ctas, after_kv_write=True)
@@ -1260,10 +1234,10 @@ def _last_layer_subset_enabled() -> bool:
 class Stage2Plan:
     """Single-device tables for a batch of QueryJobs: NewTokens + a K3
     schedule over the jobs' chunk tables (chunk-major for batches, split-KV
-    per query otherwise; see stage2_schedule_kind).  A plan of label jobs also
-    holds `last`: the last layer's schedule over the scored rows alone
-    (chunk_major_tables subsets, or AttnSchedule row ranges), whose merge
-    writes them compactly in LabelScorer.keep order; `last` is None otherwise."""
+    per query otherwise; see stage2_schedule_kind).  A chunk-major plan of
+    label jobs also holds `last`: the last layer's schedule over the scored
+    rows alone (chunk_major_tables subsets), whose merge writes them compactly
+    in LabelScorer.keep order; `last` is None otherwise."""
 
     def __init__(self, dm, jobs, target_ctas: int | None = None, order: str = "query", schedule: str | None = None):
         self.new = NewTokens(dm, jobs)
@@ -1275,13 +1249,6 @@ class Stage2Plan:
                 self.last = ChunkMajorSchedule(dm, jobs, self.new, subsets=scored_local_rows(jobs))
         else:
             self.sched = AttnSchedule(dm, jobs, self.new, target_ctas=target_ctas, order=order)
-            if (order == "query" and jobs and all(j.labels is not None for j in jobs)
-                    and _last_layer_subset_enabled()):
-                kept = scored_local_rows(jobs)
-                if all(len(x) and int(x[-1]) - int(x[0]) + 1 == len(x) for x in kept):  # contiguous ranges
-                    last = AttnSchedule(dm, jobs, self.new, target_ctas=target_ctas, order=order,
-                                        row_ranges=[(int(x[0]), int(x[-1]) + 1) for x in kept])
-                    self.last = last if last.compact else None
         for name in ("tok0", "n_tok", "num_m", "pos", "lo", "ids", "pages", "n_pages", "aux_rows"):
             setattr(self, name, getattr(self.new, name))
         for name in ("works", "n_works", "n_segs", "n_merge", "merges", "max_rows", "rope", "kv_tokens"):
@@ -1574,13 +1541,11 @@ class GraphedStage2:
         else:
             # replay() copies later batches' tables into these buffers: they must not be
             # the shared split-KV template tensors (AttnSchedule._from_template)
-            for sc in (plan.sched, plan.last):
-                if sc is None:
-                    continue
-                sc.works = sc.works.clone()
-                sc.merges = sc.merges.clone() if sc.merges is not None else None
-                sc.cta_works = sc.cta_works.clone() if sc.cta_works is not None else None
-            plan.works, plan.merges = plan.sched.works, plan.sched.merges
+            sc = plan.sched
+            sc.works = sc.works.clone()
+            sc.merges = sc.merges.clone() if sc.merges is not None else None
+            sc.cta_works = sc.cta_works.clone() if sc.cta_works is not None else None
+            plan.works, plan.merges = sc.works, sc.merges
         self._run()  # warm-up: workspace allocation, cuBLAS handles, kernel attributes
         torch.cuda.current_stream(dm.device).synchronize()
         self.graph = torch.cuda.CUDAGraph()
@@ -1610,14 +1575,11 @@ class GraphedStage2:
                 if t.last is not None:
                     t.last.copy_tables_from(n.last)
             else:
-                for ts, ns in ((t.sched, n.sched), (t.last, n.last)):
-                    if ts is None:
-                        continue
-                    pairs += [(ts.works, ns.works), (ts.segs, ns.segs)]
-                    if ts.cta_works is not None:
-                        pairs.append((ts.cta_works, ns.cta_works))
-                    if ts.merges is not None:
-                        pairs.append((ts.merges, ns.merges))
+                pairs += [(t.sched.works, n.sched.works), (t.sched.segs, n.sched.segs)]
+                if t.sched.cta_works is not None:
+                    pairs.append((t.sched.cta_works, n.sched.cta_works))
+                if t.sched.merges is not None:
+                    pairs.append((t.sched.merges, n.sched.merges))
             for dst, src in pairs:
                 dst.copy_(src, non_blocking=True)
         if n.sched.rope is not t.sched.rope:
@@ -1635,9 +1597,7 @@ def plan_key(plan, scorer):
     if isinstance(sc, ChunkMajorSchedule):
         tables = ("chunk", sc.row_map.numel(), sc.num_m, plan.last.row_map.numel() if plan.last is not None else -1)
     else:
-        la = plan.last
-        tables = ("query", sc.n_works, sc.n_segs, sc.n_ctas,
-                  (la.n_works, la.n_segs, la.n_ctas, la.num_m, la.n_merge, la.part_rows) if la is not None else None)
+        tables = ("query", sc.n_works, sc.n_segs, sc.n_ctas)
     return (plan.new.n_tok, tuple(plan.new.n_new), plan.new.n_pages, tables, sc.n_merge, sc.part_rows,
             int(scorer.rows.numel()), int(scorer.keep.numel()), scorer.n_out, plan.new.num_m)
 
