@@ -1460,7 +1460,7 @@ class GraphedShardedStage2:
             sc.pad_to(-(-h(sc.n_real_works) // 64) * 64, -(-h(sc.n_real_segs) // 16) * 16,
                       rows_cap=h(sc.row_map.numel() // ops.ROWMAP_DTYPE.itemsize), part_cap=h(sc.part_rows))
         self.runner = ShardedStage2(dm, caches, comm, None, plan=plan)
-        self.scorer = LabelScorer(dm, plan.new, plan.jobs, n_labels)
+        self.scorer = LabelScorer(dm, plan.new, plan.jobs, n_labels).private_copy()
         self._run()  # warm-up: workspaces, cuBLAS handles, NCCL communicator, kernel attributes
         torch.cuda.current_stream(dm.device).synchronize()
         self.graph = torch.cuda.CUDAGraph()
@@ -1522,7 +1522,7 @@ class GraphedStage2:
         template (e.g. the largest tables of a set of batches to replay)."""
         torch = _torch()
         self.dm, self.store, self.plan = dm, store, plan
-        self.scorer = LabelScorer(dm, plan, jobs, n_labels)
+        self.scorer = LabelScorer(dm, plan, jobs, n_labels).private_copy()
         self.key = plan_key(plan, self.scorer)
         if isinstance(plan.sched, ChunkMajorSchedule):
             # the chunk-major table sizes vary with how a batch's selections
@@ -1623,12 +1623,32 @@ def _final_logits(dm, h_rows):
     return torch.mm(x, dm.lm_head, out_dtype=torch.float32)
 
 
+_SCORER_TLS = __import__("threading").local()
+
+
+def _scorer_tables():
+    d = getattr(_SCORER_TLS, "cache", None)
+    if d is None:
+        d = _SCORER_TLS.cache = __import__("collections").OrderedDict()
+    return d
+
+
 class LabelScorer:
     """Row gather + lm_head + log-softmax gather for a batch of label jobs
     (model.py:441-443, pipeline.py:376-382)."""
 
     def __init__(self, dm, plan, jobs, n_labels):
-        torch = _torch()
+        # the tables depend on the jobs' shapes and labels only: a per-thread LRU
+        # reuses their device copies across batches (Runner.infer's host path)
+        key = (tuple(int(x) for x in plan.tok0[:len(jobs)]), tuple(int(j.prefix) for j in jobs),
+               tuple(tuple(tuple(int(t) for t in lab) for lab in j.labels) for j in jobs), int(n_labels), str(dm.device))
+        cache = _scorer_tables()
+        hit = cache.get(key)
+        if hit is not None:
+            cache.move_to_end(key)
+            (self.keep, self.rows_in_keep, self.rows, self.targets, self.owner, self.label_row0,
+             self.n_out, self.n_labels) = hit
+            return
         rows, targets, owner = [], [], []
         for qi, j in enumerate(jobs):
             base = int(plan.tok0[qi])
@@ -1658,6 +1678,20 @@ class LabelScorer:
         self.label_row0 = ops.h2d(np.concatenate([[0], np.cumsum(counts)]).astype(np.int32), dev)
         self.n_out = len(jobs) * n_labels
         self.n_labels = n_labels
+        cache[key] = (self.keep, self.rows_in_keep, self.rows, self.targets, self.owner, self.label_row0,
+                      self.n_out, self.n_labels)
+        while len(cache) > 64:
+            cache.popitem(last=False)
+
+    def private_copy(self):
+        """A copy whose tables are its own (a captured graph's scorer: replay()
+        writes later batches' tables into them, so they must not be the shared
+        cached ones)."""
+        c = object.__new__(LabelScorer)
+        for name in ("keep", "rows_in_keep", "rows", "targets", "owner", "label_row0"):
+            setattr(c, name, getattr(self, name).clone())
+        c.n_out, c.n_labels = self.n_out, self.n_labels
+        return c
 
     def __call__(self, dm, h, subset: bool = False):
         """h: all rows' final hidden states, or (subset) only the rows `keep`.
