@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define DBSA_ABI_VERSION 9
+#define DBSA_ABI_VERSION 10
 #define DBSA_PAGE_TOKENS 64
 
 /* Error codes -> reference exceptions (errors.py:4-29). */
@@ -150,6 +150,10 @@ typedef struct DbsaAttnArgs {
                                (e.g. the K/V page write that precedes each layer's attention); the launch is then
                                a programmatic dependent launch that stages Q while the predecessor runs and waits
                                for it only before its first K/V tile load.  0: plain stream order. */
+  const void *rope_f16;     /* optional (NULL = rotate with rope_table): fp16 (cos, sin) pairs, [rope_rows]
+                               [head_dim/2] (dbsa_rope_table_f16), used for the query rotation of the two-tile
+                               kernel's Q staging: half the bytes per row of the float32 table.  The rounding
+                               (2^-11 relative) is below the bf16 rounding of the rotated query (2^-8). */
 } DbsaAttnArgs;
 int dbsa_attention(const DbsaAttnArgs *args, void *stream);
 
@@ -253,6 +257,10 @@ int dbsa_kv_read(const DbsaKvReadArgs *args, void *stream);
  * formed in float64 exactly as model.rope_angles (model.py:205-209). */
 int dbsa_rope_table(float *table, int64_t rows, const double *inv_freq, int32_t half,
                     int64_t pos0, void *stream);
+/* The same table rounded once from float64 to fp16 (cos, sin) pairs, for
+ * DbsaAttnArgs.rope_f16. */
+int dbsa_rope_table_f16(void *table, int64_t rows, const double *inv_freq, int32_t half,
+                        int64_t pos0, void *stream);
 
 /* Component K4: per query, [0] + top-(budget-1) of units 1..n-1 under the
  * total order (score desc, id asc), then re-ordered by `ordering`

@@ -34,10 +34,11 @@ EXPORTED_SYMBOLS = (
     "dbsa_label_score",
     "dbsa_bm25_scores",
     "dbsa_abi_version",
+    "dbsa_rope_table_f16",
     "dbsa_last_error",
 )
 
-ABI_VERSION = 9
+ABI_VERSION = 10
 OUT_BF16, OUT_PARTIAL, OUT_MAPPED = 0, 1, 2
 PAGE_TOKENS = 64
 SEG_FULL = 0
@@ -72,6 +73,7 @@ class AttnArgs(ctypes.Structure):
         ("works", _vp), ("n_works", _i32), ("segs", _vp),
         ("out", _vp), ("out_tok_stride", _i64), ("part_o", _vp), ("part_lse", _vp),
         ("row_map", _vp), ("part_bf16", _i32), ("pair_count", _vp), ("cta_works", _vp), ("n_ctas", _i32), ("pdl_early_q", _i32),
+        ("rope_f16", _vp),
     ]
 
 
@@ -155,6 +157,7 @@ def load_library(path: Path | str | None = None) -> ctypes.CDLL:
         lib.dbsa_kv_write.argtypes = [ctypes.POINTER(KvWriteArgs), _vp]
         lib.dbsa_kv_read.argtypes = [ctypes.POINTER(KvReadArgs), _vp]
         lib.dbsa_rope_table.argtypes = [_vp, _i64, _vp, _i32, _i64, _vp]
+        lib.dbsa_rope_table_f16.argtypes = [_vp, _i64, _vp, _i32, _i64, _vp]
         lib.dbsa_topk_select.argtypes = [_vp, _i64, _i64, _i64, _i32, _vp, _vp]
         lib.dbsa_rmsnorm.argtypes = [_vp, _vp, _vp, _i64, _i64, _f32, _vp]
         lib.dbsa_add_rmsnorm.argtypes = [_vp, _vp, _vp, _vp, _i64, _i64, _f32, _vp]

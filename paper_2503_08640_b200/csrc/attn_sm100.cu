@@ -30,6 +30,7 @@
 // of tile m run, and vice versa.
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -46,6 +47,9 @@ constexpr int kBN = 128;  // keys per tile
 // lazy O rescale: only when a row's max grows by more than 2^DBSA_RESCALE_LOG2
 // (P <= 2^DBSA_RESCALE_LOG2 stays exact in bf16's exponent range)
 // Q staging: load iterations batched per round trip (1 = one at a time)
+#ifndef DBSA_EPI_COLS
+#define DBSA_EPI_COLS 128  // O columns per epilogue TMEM round trip
+#endif
 #ifndef DBSA_QSTAGE_BATCH
 #define DBSA_QSTAGE_BATCH 4
 #endif
@@ -124,6 +128,7 @@ struct AttnParams {
   const int32_t *tok_pos;
   const int32_t *tok_lo;
   const float2 *rope;
+  const __half2 *rope_h;  // optional fp16 copy of rope: the Q staging's rotation table
   int64_t rope_rows;
   int32_t n_heads, n_kv_heads, head_dim, gs;
   float scale_log2;
@@ -300,30 +305,21 @@ __device__ __forceinline__ RowRef row_ref(const AttnParams &p, const DbsaAttnWor
   return x;
 }
 
-// Epilogue of one row (thread = TMEM lane = row): the whole O row from TMEM
-// in one round trip (HDP / 32 loads, one wait), normalised by 1/l, then
-// either bf16 into out or an fp32 partial + natural-log LSE.  Warp-collective
-// (tcgen05.ld): every lane calls it, invalid rows store nothing.
-template <int HDP>
-__device__ __forceinline__ void epilogue_row(const AttnParams &p, uint32_t t_o, bool valid, int t, int head,
-                                             int out_mode, int64_t part_row, float l_sum, float m_used) {
-  float o[HDP];
-  if constexpr (HDP >= 32) {
-#pragma unroll
-    for (int c = 0; c < HDP; c += 32) tmem_ld32(t_o + c, *reinterpret_cast<float(*)[32]>(&o[c]));
-  } else {
-    tmem_ld16(t_o, *reinterpret_cast<float(*)[16]>(&o[0]));
-  }
-  tmem_wait_ld();
-  if (!valid || (p.dbg & 8)) return;
-  const bool empty = !(l_sum > 0.f);  // no visible key (e.g. a shard without chunks): O = 0, LSE = -inf
-  const float inv_l = empty ? 0.f : 1.f / l_sum;
+// Columns [c0, c0 + CW) of one epilogue row, normalised by 1/l: bf16 into
+// out, or a bf16 / fp32 partial.  32-byte stores (st.global.v8, whole
+// sectors) on full-width aligned rows, element stores otherwise.
+template <int HDP, int CW>
+__device__ __forceinline__ void epilogue_cols(const AttnParams &p, const float (&o)[CW], int c0, int t, int head,
+                                              int out_mode, int64_t part_row, float inv_l) {
   const int hd = p.head_dim;
-  if (out_mode == DBSA_OUT_BF16) {
-    __nv_bfloat16 *dst = p.out + (int64_t)t * p.out_tok_stride + (int64_t)head * hd;
-    if (HDP >= 16 && hd == HDP && (reinterpret_cast<uintptr_t>(dst) & 31) == 0) {  // 32-byte stores
+  const bool full = hd == HDP;
+  if (out_mode == DBSA_OUT_BF16 || p.part_bf16) {
+    __nv_bfloat16 *dst = out_mode == DBSA_OUT_BF16
+                             ? p.out + (int64_t)t * p.out_tok_stride + (int64_t)head * hd + c0
+                             : reinterpret_cast<__nv_bfloat16 *>(p.part_o) + part_row * (int64_t)hd + c0;
+    if (CW >= 16 && full && (reinterpret_cast<uintptr_t>(dst) & 31) == 0) {
 #pragma unroll
-      for (int c = 0; c < HDP; c += 16) {
+      for (int c = 0; c < CW; c += 16) {
         uint32_t w[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) w[i] = pack_bf16(o[c + 2 * i] * inv_l, o[c + 2 * i + 1] * inv_l);
@@ -334,104 +330,116 @@ __device__ __forceinline__ void epilogue_row(const AttnParams &p, uint32_t t_o, 
       return;
     }
 #pragma unroll
-    for (int c = 0; c < HDP; c += 8) {
-      if (c + 8 <= hd && (hd & 7) == 0) {
+    for (int c = 0; c < CW; c += 8) {
+      if (c0 + c + 8 <= hd && (hd & 7) == 0) {
         *reinterpret_cast<uint4 *>(dst + c) =
             make_uint4(pack_bf16(o[c] * inv_l, o[c + 1] * inv_l), pack_bf16(o[c + 2] * inv_l, o[c + 3] * inv_l),
                        pack_bf16(o[c + 4] * inv_l, o[c + 5] * inv_l), pack_bf16(o[c + 6] * inv_l, o[c + 7] * inv_l));
       } else {
 #pragma unroll
         for (int i = 0; i < 8; ++i)
-          if (c + i < hd) dst[c + i] = __float2bfloat16(o[c + i] * inv_l);
+          if (c0 + c + i < hd) dst[c + i] = __float2bfloat16(o[c + i] * inv_l);
       }
     }
-  } else if (p.part_bf16) {
-    __nv_bfloat16 *dst = reinterpret_cast<__nv_bfloat16 *>(p.part_o) + part_row * (int64_t)hd;
-    if (HDP >= 16 && hd == HDP) {  // 32-byte stores (st.global.v8, whole sectors): half the store count
+    return;
+  }
+  float *dst = reinterpret_cast<float *>(p.part_o) + part_row * (int64_t)hd + c0;
+  if (CW >= 8 && full && (reinterpret_cast<uintptr_t>(dst) & 31) == 0) {
 #pragma unroll
-      for (int c = 0; c < HDP; c += 16) {
-        uint32_t w[8];
+    for (int c = 0; c < CW; c += 8)
+      asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst + c), "f"(o[c] * inv_l),
+                   "f"(o[c + 1] * inv_l), "f"(o[c + 2] * inv_l), "f"(o[c + 3] * inv_l), "f"(o[c + 4] * inv_l),
+                   "f"(o[c + 5] * inv_l), "f"(o[c + 6] * inv_l), "f"(o[c + 7] * inv_l)
+                   : "memory");
+    return;
+  }
 #pragma unroll
-        for (int i = 0; i < 8; ++i) w[i] = pack_bf16(o[c + 2 * i] * inv_l, o[c + 2 * i + 1] * inv_l);
-        asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst + c), "r"(w[0]), "r"(w[1]),
-                     "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
-                     : "memory");
-      }
-      p.part_lse[part_row] = empty ? -INFINITY : (m_used + log2f(l_sum)) * 0.69314718055994531f;
-      return;
+  for (int c = 0; c < CW; c += 4) {
+    if (c0 + c + 4 <= hd && (hd & 3) == 0) {
+      *reinterpret_cast<float4 *>(dst + c) =
+          make_float4(o[c] * inv_l, o[c + 1] * inv_l, o[c + 2] * inv_l, o[c + 3] * inv_l);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (c0 + c + i < hd) dst[c + i] = o[c + i] * inv_l;
     }
-#pragma unroll
-    for (int c = 0; c < HDP; c += 8) {
-      if (c + 8 <= hd && (hd & 7) == 0) {
-        *reinterpret_cast<uint4 *>(dst + c) =
-            make_uint4(pack_bf16(o[c] * inv_l, o[c + 1] * inv_l), pack_bf16(o[c + 2] * inv_l, o[c + 3] * inv_l),
-                       pack_bf16(o[c + 4] * inv_l, o[c + 5] * inv_l), pack_bf16(o[c + 6] * inv_l, o[c + 7] * inv_l));
-      } else {
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-          if (c + i < hd) dst[c + i] = __float2bfloat16(o[c + i] * inv_l);
-      }
-    }
-    p.part_lse[part_row] = empty ? -INFINITY : (m_used + log2f(l_sum)) * 0.69314718055994531f;
-  } else {
-    float *dst = reinterpret_cast<float *>(p.part_o) + part_row * (int64_t)hd;
-    if (HDP >= 8 && hd == HDP && (reinterpret_cast<uintptr_t>(dst) & 31) == 0) {  // 32-byte stores
-#pragma unroll
-      for (int c = 0; c < HDP; c += 8)
-        asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst + c), "f"(o[c] * inv_l),
-                     "f"(o[c + 1] * inv_l), "f"(o[c + 2] * inv_l), "f"(o[c + 3] * inv_l), "f"(o[c + 4] * inv_l),
-                     "f"(o[c + 5] * inv_l), "f"(o[c + 6] * inv_l), "f"(o[c + 7] * inv_l)
-                     : "memory");
-      p.part_lse[part_row] = empty ? -INFINITY : (m_used + log2f(l_sum)) * 0.69314718055994531f;
-      return;
-    }
-#pragma unroll
-    for (int c = 0; c < HDP; c += 4) {
-      if (c + 4 <= hd && (hd & 3) == 0) {
-        *reinterpret_cast<float4 *>(dst + c) =
-            make_float4(o[c] * inv_l, o[c + 1] * inv_l, o[c + 2] * inv_l, o[c + 3] * inv_l);
-      } else {
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          if (c + i < hd) dst[c + i] = o[c + i] * inv_l;
-      }
-    }
-    // natural-log LSE of the scaled scores: (m + log2 l) * ln 2
-    p.part_lse[part_row] = empty ? -INFINITY : (m_used + log2f(l_sum)) * 0.69314718055994531f;
   }
 }
 
-// Stage the 128-row Q tile m of work w cooperatively: a row's 16-byte chunk
-// pairs (c, c + HDP/16) -- the two rotary halves -- go to HDP/16 consecutive
-// lanes, so one warp instruction reads whole 128-byte lines of q and of the
-// rope table for 32 / (HDP/16) rows instead of one 16-byte piece of 32
-// different rows (the thread-per-row form costs ~32 L1 wavefronts per
-// instruction).  restage: rope row tok_pos - shift (a plain work's next
-// segment); otherwise the row's own (row_ref) rope row.  Full-width heads only
-// (hd == HDP, 16-byte aligned rows); the caller falls back to load_q_row.
+// Epilogue of one row (thread = TMEM lane = row): the O row from TMEM in
+// chunks of DBSA_EPI_COLS columns (default the whole row: one round trip),
+// normalised by 1/l, then either bf16 into out or a partial + natural-log LSE.
+// Warp-collective (tcgen05.ld): every lane calls it, invalid rows store nothing.
 template <int HDP>
-__device__ __forceinline__ void stage_q_coop(const AttnParams &p, const DbsaAttnWork &w, int m, uint8_t *q_tile,
-                                             int q4, int lane, bool restage, int shift) {
-  constexpr int QSW = AttnCfg<HDP, 1>::QSW;
-  constexpr int NCH = HDP / 16;  // chunk pairs per row == lanes per row
-  constexpr int RPI = 32 / NCH;  // rows per warp instruction
-  constexpr int NIT = 32 / RPI;  // iterations for the warp's 32 rows
-  const int c = lane % NCH, rsub = lane / NCH, half = HDP / 2;
-  // phase A: every iteration's (token, head, rope row) first, so the row-map /
-  // tok_pos round trip is paid once, not once per iteration
-  int tok[NIT], head[NIT], rrow[NIT];
+__device__ __forceinline__ void epilogue_row(const AttnParams &p, uint32_t t_o, bool valid, int t, int head,
+                                             int out_mode, int64_t part_row, float l_sum, float m_used) {
+  constexpr int CW = HDP > DBSA_EPI_COLS ? DBSA_EPI_COLS : HDP;
+  const bool store = valid && !(p.dbg & 8);
+  const bool empty = !(l_sum > 0.f);  // no visible key (e.g. a shard without chunks): O = 0, LSE = -inf
+  const float inv_l = empty ? 0.f : 1.f / l_sum;
+#pragma unroll
+  for (int c0 = 0; c0 < HDP; c0 += CW) {
+    float o[CW];
+    if constexpr (CW >= 32) {
+#pragma unroll
+      for (int c = 0; c < CW; c += 32) tmem_ld32(t_o + c0 + c, *reinterpret_cast<float(*)[32]>(&o[c]));
+    } else {
+      tmem_ld16(t_o + c0, *reinterpret_cast<float(*)[16]>(&o[0]));
+    }
+    tmem_wait_ld();
+    if (store) epilogue_cols<HDP, CW>(p, o, c0, t, head, out_mode, part_row, inv_l);
+  }
+  // natural-log LSE of the scaled scores: (m + log2 l) * ln 2
+  if (store && out_mode != DBSA_OUT_BF16)
+    p.part_lse[part_row] = empty ? -INFINITY : (m_used + log2f(l_sum)) * 0.69314718055994531f;
+}
+
+// Row refs of the coop Q staging: lane (c, rsub) of warp q4 stages rows
+// q4 * 32 + it * RPI + rsub, it < NIT, of M tile m.
+template <int HDP>
+struct QRefs {
+  static constexpr int NCH = HDP / 16;  // chunk pairs per row == lanes per row
+  static constexpr int RPI = 32 / NCH;  // rows per warp instruction
+  static constexpr int NIT = 32 / RPI;  // iterations for the warp's 32 rows
+  int tok[NIT], rrow[NIT];
+  int head0;  // first query head of the work's kv head; row r is head head0 + r % gs
+};
+
+// Phase A of the coop staging: every iteration's (token, head, rope row), so
+// the row-map / tok_pos round trip is paid once, not once per iteration.  The
+// work boundary issues it before the epilogue so its latency hides there.
+template <int HDP>
+__device__ __forceinline__ void stage_refs_coop(const AttnParams &p, const DbsaAttnWork &w, int m, int q4, int lane,
+                                                bool restage, int shift, QRefs<HDP> &x) {
+  constexpr int NCH = QRefs<HDP>::NCH, RPI = QRefs<HDP>::RPI, NIT = QRefs<HDP>::NIT;
+  const int rsub = lane / NCH;
 #pragma unroll
   for (int it = 0; it < NIT; ++it) {
-    const RowRef x = row_ref(p, w, m * 128 + q4 * 32 + it * RPI + rsub);
-    tok[it] = x.valid ? x.t : -1;
-    head[it] = x.head;
-    rrow[it] = x.rope_row;
+    const RowRef rr = row_ref(p, w, m * 128 + q4 * 32 + it * RPI + rsub);
+    x.tok[it] = rr.valid ? rr.t : -1;
+    x.rrow[it] = rr.rope_row;
   }
+  x.head0 = w.kv_head * p.gs;
   if (restage) {
 #pragma unroll
     for (int it = 0; it < NIT; ++it)
-      if (tok[it] >= 0) rrow[it] = p.tok_pos[tok[it]] - shift;
+      if (x.tok[it] >= 0) x.rrow[it] = p.tok_pos[x.tok[it]] - shift;
   }
+}
+
+// Phase B: q chunk pairs + their (cos, sin), rotate, swizzled 16-byte stores
+// into the Q tile.  HALF: the fp16 rotation table (AttnParams.rope_h).
+template <int HDP, bool HALF>
+__device__ __forceinline__ void stage_load_coop(const AttnParams &p, uint8_t *q_tile, int m, int q4, int lane,
+                                                const QRefs<HDP> &x) {
+  constexpr int QSW = AttnCfg<HDP, 1>::QSW;
+  constexpr int NCH = QRefs<HDP>::NCH, RPI = QRefs<HDP>::RPI, NIT = QRefs<HDP>::NIT;
+  const int c = lane % NCH, rsub = lane / NCH, half = HDP / 2;
+  const int(&tok)[NIT] = x.tok;
+  const int(&rrow)[NIT] = x.rrow;
+  int head[NIT];
+#pragma unroll
+  for (int it = 0; it < NIT; ++it) head[it] = x.head0 + (m * 128 + q4 * 32 + it * RPI + rsub) % p.gs;
 #if DBSA_QSTAGE_BATCH > 1
   // phase B, batched: the loads of QB iterations are issued before any of
   // them is used, so QB round trips overlap (QB x 24 registers in flight)
@@ -440,7 +448,8 @@ __device__ __forceinline__ void stage_q_coop(const AttnParams &p, const DbsaAttn
 #pragma unroll
   for (int i0 = 0; i0 < NIT; i0 += QB) {
     uint4 lo4[QB], hi4[QB];
-    float4 cs4[QB][4];
+    float4 cs4[QB][4];  // float32 table: (cos, sin) of 8 pairs
+    uint4 rh4[QB][2];   // fp16 table
 #pragma unroll
     for (int k = 0; k < QB; ++k) {
       const int it = i0 + k;
@@ -450,8 +459,15 @@ __device__ __forceinline__ void stage_q_coop(const AttnParams &p, const DbsaAttn
       const float4 *rp = reinterpret_cast<const float4 *>(p.rope + (int64_t)rk * half + c * 8);
       lo4[k] = __ldg(reinterpret_cast<const uint4 *>(src));
       hi4[k] = __ldg(reinterpret_cast<const uint4 *>(src + half));
+      if constexpr (HALF) {
+        // fp16 (cos, sin) of the chunk's 8 pairs: 32 contiguous bytes
+        const uint4 *rh = reinterpret_cast<const uint4 *>(p.rope_h + (int64_t)rk * half + c * 8);
+        rh4[k][0] = __ldg(rh);
+        rh4[k][1] = __ldg(rh + 1);
+      } else {
 #pragma unroll
-      for (int v = 0; v < 4; ++v) cs4[k][v] = __ldg(rp + v);
+        for (int v = 0; v < 4; ++v) cs4[k][v] = __ldg(rp + v);
+      }
     }
 #pragma unroll
     for (int k = 0; k < QB; ++k) {
@@ -459,7 +475,19 @@ __device__ __forceinline__ void stage_q_coop(const AttnParams &p, const DbsaAttn
       const int row = q4 * 32 + it * RPI + rsub;
       const __nv_bfloat16 *lo = reinterpret_cast<const __nv_bfloat16 *>(&lo4[k]);
       const __nv_bfloat16 *hi = reinterpret_cast<const __nv_bfloat16 *>(&hi4[k]);
-      const float *cs = reinterpret_cast<const float *>(cs4[k]);
+      float cs[16];
+      if constexpr (HALF) {
+        const __half2 *h2 = reinterpret_cast<const __half2 *>(rh4[k]);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float2 f = __half22float2(h2[j]);
+          cs[2 * j] = f.x;
+          cs[2 * j + 1] = f.y;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) cs[j] = reinterpret_cast<const float *>(cs4[k])[j];
+      }
       const float keep = tok[it] >= 0 ? 1.f : 0.f;
       float a[8], b[8];
 #pragma unroll
@@ -491,8 +519,17 @@ __device__ __forceinline__ void stage_q_coop(const AttnParams &p, const DbsaAttn
       const uint4 lo4 = *reinterpret_cast<const uint4 *>(src);
       const uint4 hi4 = *reinterpret_cast<const uint4 *>(src + half);
       float4 cs4[4];
+      if constexpr (HALF) {
+        const __half2 *h2 = p.rope_h + (int64_t)rrow[it] * half + c * 8;
 #pragma unroll
-      for (int v = 0; v < 4; ++v) cs4[v] = rp[v];
+        for (int v = 0; v < 4; ++v) {
+          const float2 f0 = __half22float2(h2[2 * v]), f1 = __half22float2(h2[2 * v + 1]);
+          cs4[v] = make_float4(f0.x, f0.y, f1.x, f1.y);
+        }
+      } else {
+#pragma unroll
+        for (int v = 0; v < 4; ++v) cs4[v] = rp[v];
+      }
       const __nv_bfloat16 *lo = reinterpret_cast<const __nv_bfloat16 *>(&lo4);
       const __nv_bfloat16 *hi = reinterpret_cast<const __nv_bfloat16 *>(&hi4);
       const float *cs = reinterpret_cast<const float *>(cs4);
@@ -517,6 +554,22 @@ __device__ __forceinline__ void stage_q_coop(const AttnParams &p, const DbsaAttn
     }
   }
 #endif
+}
+
+// Stage the 128-row Q tile m of work w cooperatively: a row's 16-byte chunk
+// pairs (c, c + HDP/16) -- the two rotary halves -- go to HDP/16 consecutive
+// lanes, so one warp instruction reads whole 128-byte lines of q and of the
+// rope table for 32 / (HDP/16) rows instead of one 16-byte piece of 32
+// different rows (the thread-per-row form costs ~32 L1 wavefronts per
+// instruction).  restage: rope row tok_pos - shift (a plain work's next
+// segment); otherwise the row's own (row_ref) rope row.  Full-width heads only
+// (hd == HDP, 16-byte aligned rows); the caller falls back to load_q_row.
+template <int HDP, bool HALF>
+__device__ __forceinline__ void stage_q_coop(const AttnParams &p, const DbsaAttnWork &w, int m, uint8_t *q_tile,
+                                             int q4, int lane, bool restage, int shift) {
+  QRefs<HDP> x;
+  stage_refs_coop<HDP>(p, w, m, q4, lane, restage, shift, x);
+  stage_load_coop<HDP, HALF>(p, q_tile, m, q4, lane, x);
 }
 
 template <int HDP, int NUM_M>
@@ -787,34 +840,51 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
     const bool coop = HDP >= 16 && p.head_dim == HDP && (p.q_tok_stride & 7) == 0;
     auto stage_q = [&](const DbsaAttnWork &wq, bool restage, int shift) {
       if (p.dbg & 16) return;  // profiling: keep whatever Q the tile holds
-      if (coop) {
-        stage_q_coop<HDP>(p, wq, m, q_tile, q4, lane, restage, shift);
+      if (coop && p.rope_h) {
+        stage_q_coop<HDP, true>(p, wq, m, q_tile, q4, lane, restage, shift);
+      } else if (coop) {
+        stage_q_coop<HDP, false>(p, wq, m, q_tile, q4, lane, restage, shift);
       } else {
         const RowRef xq = row_ref(p, wq, r);
         load_q_row<HDP>(p, q_tile, trow, xq.valid, xq.t, xq.head, restage ? p.tok_pos[xq.t] - shift : xq.rope_row);
       }
     };
+    // This thread's row of the next work (its descriptor, row refs, tree-mask
+    // bound and first RoPE shift), loaded one work ahead: at a work boundary
+    // the loads are issued before the epilogue, so their latency hides there.
+    RowRef x_nx;
+    DbsaAttnWork w_nx;
+    int lo_nx = 0, rot_nx = 0;
+    auto load_row = [&](const DbsaAttnWork &wq) {
+      x_nx = row_ref(p, wq, r);
+      lo_nx = (p.tok_lo && x_nx.valid) ? p.tok_lo[x_nx.t] : 0;
+      rot_nx = wq.seg_end > wq.seg_begin ? p.segs[wq.seg_begin].shift : 0;
+    };
     if (wr.begin < wr.end) {  // stage Q of the first work
-      stage_q(p.works[wr.begin], false, 0);
+      w_nx = p.works[wr.begin];
+      load_row(w_nx);
+      stage_q(w_nx, false, 0);
       fence_proxy_async_smem();
       mbar_arrive(&q_full[m]);
       if (m == 0 && trow == 0) CSTAMP(2);
     }
     for (int wi = wr.begin; wi < wr.end; wi += wr.step, ++wk) {
-      const DbsaAttnWork w = p.works[wi];
-      const RowRef xr = row_ref(p, w, r);
+      const DbsaAttnWork w = w_nx;  // read at the previous boundary
+      const RowRef xr = x_nx;
       const bool valid = xr.valid;
       const int t = xr.t, head = xr.head;
       const int rl = t - w.self_tok0;
-      const int lo = (p.tok_lo && valid) ? p.tok_lo[t] : 0;
-      int cur_rot = w.seg_end > w.seg_begin ? p.segs[w.seg_begin].shift : 0;
+      const int lo = lo_nx;
+      int cur_rot = rot_nx;
       // Online softmax in the log2 domain; the scale is folded into the exp2
       // FFMA: p = 2^(x * scale_log2 - m_used).
+      if (trow == 0 && m == 0 && w.seg_begin != 0x7fffffff) WSTAMP(8, wk);
       const bool warp_dead = __all_sync(0xffffffffu, !valid);
       float m_used = -INFINITY, l_sum = 0.f;
       int j = 0;
       for (int si = w.seg_begin; si < w.seg_end; ++si) {
         const DbsaAttnSeg sg = p.segs[si];
+        if (trow == 0 && m == 0 && si == w.seg_begin && sg.n_tok != 0x7fffffff) WSTAMP(9, wk);
         const int off = sg.row0 & 63;
         const int nt = (off + sg.n_tok + kBN - 1) / kBN;
         const bool is_self = sg.kind == DBSA_SEG_SELF;
@@ -938,21 +1008,24 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
         }
       }
       jg += j;
-      // The last QK of this work has retired (its S was read): stage the next
-      // work's Q now, so its first QK overlaps this epilogue.  A work without
-      // key tiles read no S, so nothing yet proves the MMA warp consumed this
-      // work's q_full phase: wait for its o_full first, or the next arrival
-      // could complete a second q_full phase before the first was observed.
-      if (j == 0) mbar_wait(&o_full[m], wk & 1);
       if (trow == 0) WSTAMP(m * 4 + 0, wk);
+      // Work boundary.  The last QK(m) of this work has retired (its S was
+      // read), so the next work's Q(m) is staged now and its first QK overlaps
+      // this epilogue.  A work without key tiles read no S, so nothing yet
+      // proves the MMA warp consumed this work's q_full phase: wait for its
+      // o_full first, or the next arrival could complete a second q_full phase
+      // before the first was observed.  This thread's own row of the next work
+      // is loaded first: its latency hides under the staging and the epilogue.
+      if (j == 0) mbar_wait(&o_full[m], wk & 1);
       const int wn = wi + wr.step;
       if (wn < wr.end) {
-        stage_q(p.works[wn], false, 0);
+        w_nx = p.works[wn];
+        load_row(w_nx);
+        stage_q(w_nx, false, 0);
         fence_proxy_async_smem();
         mbar_arrive(&q_full[m]);
       }
       if (trow == 0) WSTAMP(m * 4 + 1, wk);
-
       // ---------------------------------------------------------- epilogue
       mbar_wait(&o_full[m], wk & 1);
       tc_fence_after();
@@ -1522,6 +1595,7 @@ extern "C" int dbsa_attention(const DbsaAttnArgs *args, void *stream) {
   p.tok_pos = a.tok_pos;
   p.tok_lo = a.tok_lo;
   p.rope = reinterpret_cast<const float2 *>(a.rope_table);
+  p.rope_h = reinterpret_cast<const __half2 *>(a.rope_f16);
   p.rope_rows = a.rope_rows;
   p.n_heads = a.n_heads;
   p.n_kv_heads = a.n_kv_heads;

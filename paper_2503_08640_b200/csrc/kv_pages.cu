@@ -7,6 +7,7 @@
 // rotated at the original positions (so stage 1 reads it as-is) and stage 2
 // moves the re-positioning to the query side (attn_sm100.cu).
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include "../../include/dbsa_b200.h"
@@ -183,6 +184,20 @@ __global__ void rope_table_kernel(float2 *table, int64_t rows, const double *inv
   }
 }
 
+// The same angles rounded once from float64 to fp16 (cos, sin): the query
+// rotation table of the two-tile attention kernel's Q staging.
+__global__ void rope_table_f16_kernel(__half2 *table, int64_t rows, const double *inv_freq, int half, int64_t pos0) {
+  const int64_t n = rows * half;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = idx / half;
+    const int i = (int)(idx % half);
+    const double ang = (double)(pos0 + p) * inv_freq[i];
+    double s, c;
+    sincos(ang, &s, &c);
+    table[idx] = __halves2half2(__double2half(c), __double2half(s));
+  }
+}
+
 }  // namespace dbsa
 
 extern "C" int dbsa_kv_write(const DbsaKvWriteArgs *args, void *stream) {
@@ -225,4 +240,15 @@ extern "C" int dbsa_rope_table(float *table, int64_t rows, const double *inv_fre
   rope_table_kernel<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(reinterpret_cast<float2 *>(table),
                                                                                   rows, inv_freq, half, pos0);
   return check_launch("rope_table");
+}
+
+extern "C" int dbsa_rope_table_f16(void *table, int64_t rows, const double *inv_freq, int32_t half, int64_t pos0,
+                                   void *stream) {
+  using namespace dbsa;
+  if (rows <= 0 || half <= 0) return set_error(DBSA_ERR_VALIDATION, "rope table: empty");
+  const int64_t n = rows * half;
+  const int blocks = (int)((n + 255) / 256 < 148 * 16 ? (n + 255) / 256 : 148 * 16);
+  rope_table_f16_kernel<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<__half2 *>(table), rows, inv_freq, half, pos0);
+  return check_launch("rope_table_f16");
 }

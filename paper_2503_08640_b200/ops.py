@@ -7,6 +7,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 
 import numpy as np
 
@@ -93,6 +94,12 @@ def rope_table(rows: int, head_dim: int, theta: float, device, pos0: int = 0):
                                                  nat.stream_handle()))
     _launched()
     table._keepalive = freq  # freq must outlive the async launch
+    if os.environ.get("DBSA_ROPE_F16", "1") != "0":
+        # fp16 copy for the attention kernels' query rotation (DbsaAttnArgs.rope_f16)
+        table.f16 = torch.empty((rows, half, 2), dtype=torch.float16, device=device)
+        nat.check(nat.load_library().dbsa_rope_table_f16(table.f16.data_ptr(), rows, freq.data_ptr(), half, pos0,
+                                                         nat.stream_handle()))
+        _launched()
     return table
 
 
@@ -141,7 +148,8 @@ def attention(*, q, q_tok_stride, tok_pos, tok_lo, rope, pool, aux, n_heads, n_k
         n_works=n_works, segs=_p(segs_dev), out=out.data_ptr(), out_tok_stride=out_tok_stride,
         part_o=nat.ptr(part_o), part_lse=nat.ptr(part_lse), row_map=nat.ptr(row_map),
         part_bf16=int(part_o is not None and part_o.element_size() == 2), pair_count=nat.ptr(pair_count),
-        cta_works=nat.ptr(cta_works), n_ctas=int(n_ctas), pdl_early_q=int(bool(after_kv_write)))
+        cta_works=nat.ptr(cta_works), n_ctas=int(n_ctas), pdl_early_q=int(bool(after_kv_write)),
+        rope_f16=nat.ptr(getattr(rope, "f16", None)))
     nat.check(nat.load_library().dbsa_attention(ctypes.byref(a), nat.stream_handle()))
     _launched()
 

@@ -84,6 +84,21 @@ class Pool:
         return self.v[layer, s:s + n].double().numpy()
 
 
+@pytest.mark.parametrize("hd,theta", [(128, 500000.0), (64, 10000.0)])
+def test_rope_tables_vs_float64(hd, theta):
+    """dbsa_rope_table (float32) and dbsa_rope_table_f16 against (cos, sin) of
+    pos * inv_freq in float64 (model.rope_angles, model.py:205-209): one
+    rounding each, at positions up to 2^19."""
+    rows = 1 << 19
+    t = ops.rope_table(rows, hd, theta, "cuda")
+    ang = np.arange(rows, dtype=np.float64)[:, None] * ops.inv_freq(hd, theta)[None, :]
+    want = np.stack([np.cos(ang), np.sin(ang)], axis=-1)
+    got32 = t.cpu().double().numpy()
+    got16 = t.f16.cpu().double().numpy()
+    assert np.abs(got32 - want).max() <= 2.0 ** -24
+    assert np.abs(got16 - want).max() <= 2.0 ** -12
+
+
 @pytest.mark.parametrize("hd,H,Hkv", [(128, 8, 2), (64, 4, 4), (16, 4, 2), (32, 2, 1), (8, 4, 2)])
 def test_kv_write_pages(hd, H, Hkv):
     pool = Pool(Hkv, hd, [70, 64, 5, 130], layers=2, seed=1)
@@ -101,11 +116,14 @@ def test_kv_write_pages(hd, H, Hkv):
             assert pool.kp[layer, :, r0:r0 + n, hd:].abs().sum().item() == 0
 
 
-def _stage1_case(hd, H, Hkv, lengths, j=2, layer=0, layers=1, num_m=None):
+def _stage1_case(hd, H, Hkv, lengths, j=2, layer=0, layers=1, num_m=None, rope_f16=True):
     """Encode every group against sink + prev-j + self (masks.py:80-99) in one launch."""
     dev = "cuda"
     gs = H // Hkv
     pool = Pool(Hkv, hd, lengths, layers=layers, seed=7)
+    assert hasattr(pool.rope, "f16")  # ops.rope_table builds the fp16 query-rotation table too
+    if not rope_f16:
+        del pool.rope.f16  # the float32 table for the Q staging as well
     T = sum(lengths)
     g = torch.Generator().manual_seed(3)
     q = torch.randn(T, H, hd, generator=g).to(torch.bfloat16)
@@ -163,6 +181,12 @@ def test_stage1_block_sparse_attention(hd, H, Hkv, num_m):
     """num_m 1: single-M-tile kernel (Q in TMEM); 2: two ping-ponged M tiles."""
     worst = _stage1_case(hd, H, Hkv, [150, 64, 97, 200, 33], num_m=num_m)
     assert worst < 2e-2, worst
+
+
+@pytest.mark.parametrize("hd,H,Hkv", [(128, 8, 2), (64, 8, 2)])
+def test_stage1_attention_float32_query_rotation(hd, H, Hkv):
+    """DbsaAttnArgs.rope_f16 = NULL: Q staging rotates with the float32 table."""
+    assert _stage1_case(hd, H, Hkv, [150, 64, 97, 200, 33], num_m=2, rope_f16=False) < 2e-2
 
 
 def test_stage1_attention_second_layer():

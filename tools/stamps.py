@@ -38,3 +38,4 @@ if hasattr(lib, "dbsa_debug_wstamps") and lib.dbsa_debug_wstamps(wb, 256 * 12) =
             b = m * 4
             print(f"work boundary m{m}: stage next Q {np.median(w[:, b+1]-w[:, b]):7.0f}  wait O {np.median(w[:, b+2]-w[:, b+1]):7.0f}"
                   f"  epilogue {np.median(w[:, b+3]-w[:, b+2]):7.0f}  work period {np.median(np.diff(w[:, b])):7.0f}  (works {len(w)})")
+        print(f"m0 epilogue done -> loop top work loaded {np.median(w[1:, 8]-w[:-1, 3]):7.0f}  -> first seg loaded {np.median(w[:, 9]-w[:, 8]):7.0f}")
