@@ -173,6 +173,15 @@ __device__ __forceinline__ void flush_pair_count(unsigned long long *dst, uint32
   if ((threadIdx.x & 31) == 0 && v) atomicAdd(dst, v);
 }
 
+// Bits i of a 32-bit word with lo <= i < hi (lo, hi clamped to [0, 32]).
+__device__ __forceinline__ uint32_t range_bits(int lo, int hi) {
+  lo = min(max(lo, 0), 32);
+  hi = min(max(hi, 0), 32);
+  const uint32_t below_hi = hi >= 32 ? 0xffffffffu : (1u << hi) - 1u;
+  const uint32_t below_lo = lo >= 32 ? 0xffffffffu : (1u << lo) - 1u;
+  return below_hi & ~below_lo;
+}
+
 // 2^x for a pair on the FMA/ALU pipes (FA4's MUFU offload): round to the
 // nearest integer with the 1.5*2^23 trick, a cubic for 2^f on f in [-0.5, 0.5]
 // (rel. error < 7e-4, below bf16's 2^-8 resolution of P), integer part added
@@ -924,16 +933,16 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
           tmem_wait_ld();
           if (trow == 0) STAMP(m * 5 + 2, jg + j);
           if (!__all_sync(0xffffffffu, full)) {
-            if (is_self) {
+            // visible columns as four 32-bit words, then one bit test per column
+            // (R2P + FSEL instead of two compares per column)
+            uint32_t keep[kBN / 32];
 #pragma unroll
-              for (int c = 0; c < kBN; ++c) {
-                const bool ok = (c >= c_lo) & (c < c_hi) & ((c < b_lo) | (c >= b_hi));
-                x[c] = ok ? x[c] : -INFINITY;
-              }
-            } else {  // a context chunk's first / last tile: one column range
-#pragma unroll
-              for (int c = 0; c < kBN; ++c) x[c] = (c >= c_lo) & (c < c_hi) ? x[c] : -INFINITY;
+            for (int wd = 0; wd < kBN / 32; ++wd) {
+              keep[wd] = range_bits(c_lo - 32 * wd, c_hi - 32 * wd);
+              if (is_self) keep[wd] &= ~range_bits(b_lo - 32 * wd, b_hi - 32 * wd);
             }
+#pragma unroll
+            for (int c = 0; c < kBN; ++c) x[c] = (keep[c >> 5] >> (c & 31)) & 1u ? x[c] : -INFINITY;
           }
           if (p.pair_count && valid) n_pairs += count_visible(x);
           float mx[8];
@@ -1388,11 +1397,12 @@ __global__ void __launch_bounds__(256, 1)
         for (int c = 0; c < kBN; c += 32) tmem_ld32(t_s + c, *reinterpret_cast<float(*)[32]>(&x[c]));
         tmem_wait_ld();
         if (!__all_sync(0xffffffffu, full)) {
+          uint32_t keep[kBN / 32];
 #pragma unroll
-          for (int c = 0; c < kBN; ++c) {
-            const bool ok = (c >= c_lo) & (c < c_hi) & ((c < b_lo) | (c >= b_hi));
-            x[c] = ok ? x[c] : -INFINITY;
-          }
+          for (int wd = 0; wd < kBN / 32; ++wd)
+            keep[wd] = range_bits(c_lo - 32 * wd, c_hi - 32 * wd) & ~range_bits(b_lo - 32 * wd, b_hi - 32 * wd);
+#pragma unroll
+          for (int c = 0; c < kBN; ++c) x[c] = (keep[c >> 5] >> (c & 31)) & 1u ? x[c] : -INFINITY;
         }
         if (p.pair_count && valid) n_pairs += count_visible(x);
         float mx[8];
