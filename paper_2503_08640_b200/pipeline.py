@@ -312,15 +312,19 @@ class Stage2Session:
         key = engine.plan_key(plan, scorer)
         graphs = self.__dict__.setdefault("_graphs", OrderedDict())
         seen = self.__dict__.setdefault("_seen", {})
+        stats = self.__dict__.setdefault("graph_stats", {"replays": 0, "eager": 0, "captures": 0})
         g = graphs.get(key)
         if g is not None and engine.fits_graph(g, plan):
             graphs.move_to_end(key)
+            stats["replays"] += 1
             return g
         seen[key] = seen.get(key, 0) + 1
         if g is None and seen[key] < 2:
             if len(seen) > 64 * self.MAX_GRAPHS:
                 seen.clear()
+            stats["eager"] += 1
             return None
+        stats["captures"] += 1
         if before_capture is not None:
             before_capture()
         graphs.pop(key, None)
@@ -381,19 +385,25 @@ class Stage2Session:
                 ev.record(side)
             return ev, ids_host, q_ids
 
+        prof = self.__dict__.get("stream_profile")  # list: per-batch host phase times (s), when set
+        clock = time.perf_counter
         it = iter(batches)
         first = next(it, None)
         nxt = select_async(first) if first is not None else None
         pending = None
         while nxt is not None:
+            t0 = clock()
             ev_sel, ids_host, q_ids = nxt
             ev_sel.synchronize()  # this batch's K4 only
+            t1 = clock()
             ids = ids_host.numpy().astype(np.int64)
             jobs, plan = self.plan(ids, q_ids)
             scorer = engine.LabelScorer(self.dm, plan, jobs, len(self.label_ids))
             g = self._graph_for(jobs, plan, scorer, before_capture=main.synchronize)
+            t2 = clock()
             b = next(it, None)
             nxt = select_async(b) if b is not None else None  # ahead of this batch's replay
+            t3 = clock()
             if g is None:
                 _, h = engine.run_jobs(self.dm, self.cache.store, jobs, plan=plan, keep=scorer.keep)
                 s_dev, best_dev = scorer(self.dm, h, subset=True)
@@ -405,8 +415,13 @@ class Stage2Session:
             b_host.copy_(best_dev, non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(main)
+            t4 = clock()
             if pending is not None:
                 pending[0].synchronize()
+            if prof is not None:
+                prof.append({"wait_select": t1 - t0, "plan": t2 - t1, "select_next": t3 - t2,
+                             "enqueue": t4 - t3, "wait_prev": clock() - t4})
+            if pending is not None:
                 yield pending[1:]
             pending = (ev, ids, s_host.numpy(), b_host.numpy())
         if pending is not None:
