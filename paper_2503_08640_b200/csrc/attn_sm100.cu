@@ -51,7 +51,7 @@ constexpr int kBN = 128;  // keys per tile
 #define DBSA_EPI_COLS 128  // O columns per epilogue TMEM round trip
 #endif
 #ifndef DBSA_QSTAGE_BATCH
-#define DBSA_QSTAGE_BATCH 4
+#define DBSA_QSTAGE_BATCH 8
 #endif
 #ifndef DBSA_RESCALE_LOG2
 #define DBSA_RESCALE_LOG2 8.f
