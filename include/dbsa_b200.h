@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define DBSA_ABI_VERSION 10
+#define DBSA_ABI_VERSION 11
 #define DBSA_PAGE_TOKENS 64
 
 /* Error codes -> reference exceptions (errors.py:4-29). */
@@ -154,6 +154,11 @@ typedef struct DbsaAttnArgs {
                                [head_dim/2] (dbsa_rope_table_f16), used for the query rotation of the two-tile
                                kernel's Q staging: half the bytes per row of the float32 table.  The rounding
                                (2^-11 relative) is below the bf16 rounding of the rotated query (2^-8). */
+  int64_t part_chunk_rows;  /* 0: partial O rows are [rows][head_dim].  > 0 (bf16 partials, head_dim % 16 == 0):
+                               16-column chunks, element (row, d) at ((d / 16) * part_chunk_rows + row) * 16 +
+                               d % 16 for rows < part_chunk_rows -- the epilogue's 32-byte store of one chunk
+                               from 32 consecutive rows (one per TMEM lane) is then 1 KB contiguous instead of
+                               32 scattered sectors.  The merge reading them passes the same value. */
 } DbsaAttnArgs;
 int dbsa_attention(const DbsaAttnArgs *args, void *stream);
 
@@ -186,6 +191,7 @@ typedef struct DbsaMergeArgs {
                               (normalised, bf16) into out and its natural-log LSE into
                               out_lse[t * n_heads + head]; a row with no visible key gets O = 0 and
                               LSE = -inf (the per-rank half of the C5 merge) */
+  int64_t part_chunk_rows; /* the partials' layout, as DbsaAttnArgs.part_chunk_rows (part_tok_layout 0 only) */
 } DbsaMergeArgs;
 int dbsa_lse_merge(const DbsaMergeArgs *args, void *stream);
 

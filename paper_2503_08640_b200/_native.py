@@ -38,7 +38,7 @@ EXPORTED_SYMBOLS = (
     "dbsa_last_error",
 )
 
-ABI_VERSION = 10
+ABI_VERSION = 11
 OUT_BF16, OUT_PARTIAL, OUT_MAPPED = 0, 1, 2
 PAGE_TOKENS = 64
 SEG_FULL = 0
@@ -73,7 +73,7 @@ class AttnArgs(ctypes.Structure):
         ("works", _vp), ("n_works", _i32), ("segs", _vp),
         ("out", _vp), ("out_tok_stride", _i64), ("part_o", _vp), ("part_lse", _vp),
         ("row_map", _vp), ("part_bf16", _i32), ("pair_count", _vp), ("cta_works", _vp), ("n_ctas", _i32), ("pdl_early_q", _i32),
-        ("rope_f16", _vp),
+        ("rope_f16", _vp), ("part_chunk_rows", _i64),
     ]
 
 
@@ -90,6 +90,7 @@ class MergeArgs(ctypes.Structure):
         ("part_o", _vp), ("part_lse", _vp), ("groups", _vp), ("n_groups", _i32), ("max_rows", _i32),
         ("n_heads", _i32), ("n_kv_heads", _i32), ("head_dim", _i32), ("out", _vp), ("out_tok_stride", _i64),
         ("split_stride", _i64), ("part_bf16", _i32), ("part_tok_layout", _i32), ("out_lse", _vp),
+        ("part_chunk_rows", _i64),
     ]
 
 

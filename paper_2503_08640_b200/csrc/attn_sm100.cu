@@ -145,6 +145,7 @@ struct AttnParams {
             // 8 = skip epilogue stores, 16 = skip Q staging (two-tile kernel)
   unsigned long long *pair_count;  // optional: (row, key) pairs that entered the softmax (all heads)
   const int32_t *cta_works;        // optional: CTA b runs works [cta_works[b], cta_works[b+1])
+  int64_t part_chunk_rows;         // > 0: bf16 partials in 16-column chunks (DbsaAttnArgs.part_chunk_rows)
   int pdl_early;                   // DbsaAttnArgs.pdl_early_q: only the producer waits for the predecessor
 };
 
@@ -322,6 +323,22 @@ __device__ __forceinline__ void epilogue_cols(const AttnParams &p, const float (
                                               int out_mode, int64_t part_row, float inv_l) {
   const int hd = p.head_dim;
   const bool full = hd == HDP;
+  if (out_mode != DBSA_OUT_BF16 && p.part_chunk_rows > 0) {
+    // 16-column chunk layout: this row's chunk k at ((c0/16 + k) * chunk_rows + part_row) * 16
+    __nv_bfloat16 *base = reinterpret_cast<__nv_bfloat16 *>(p.part_o) + part_row * 16;
+#pragma unroll
+    for (int c = 0; c < CW; c += 16) {
+      if (c0 + c >= hd) break;
+      uint32_t w[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) w[i] = pack_bf16(o[c + 2 * i] * inv_l, o[c + 2 * i + 1] * inv_l);
+      asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(
+                       base + (int64_t)((c0 + c) >> 4) * p.part_chunk_rows * 16),
+                   "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+                   : "memory");
+    }
+    return;
+  }
   if (out_mode == DBSA_OUT_BF16 || p.part_bf16) {
     __nv_bfloat16 *dst = out_mode == DBSA_OUT_BF16
                              ? p.out + (int64_t)t * p.out_tok_stride + (int64_t)head * hd + c0
@@ -1624,6 +1641,9 @@ extern "C" int dbsa_attention(const DbsaAttnArgs *args, void *stream) {
   p.pair_count = a.pair_count;
   p.cta_works = a.cta_works;
   p.pdl_early = a.pdl_early_q;
+  p.part_chunk_rows = a.part_chunk_rows;
+  if (a.part_chunk_rows > 0 && (!a.part_bf16 || a.head_dim % 16))
+    return set_error(DBSA_ERR_CONFIG, "part_chunk_rows needs bf16 partials and head_dim %% 16 == 0");
   if (a.cta_works && (a.num_m != 2 || a.n_ctas <= 0 || a.n_ctas > num_sms()))
     return set_error(DBSA_ERR_CONFIG, "cta_works needs num_m == 2 and 0 < n_ctas <= %d, got num_m %d n_ctas %d",
                      num_sms(), a.num_m, a.n_ctas);

@@ -48,6 +48,13 @@ __device__ __forceinline__ float load1(const void *base, int64_t off) {
 }
 
 // Partial row of split 0, row r of group g (DbsaMergeArgs.part_tok_layout).
+// Element offset of (partial row, dim d) -- row-major, or the 16-column chunk
+// layout of DbsaMergeArgs.part_chunk_rows (d a multiple of 4 keeps a float4 /
+// 4-element load inside one chunk).
+__device__ __forceinline__ int64_t part_off(const DbsaMergeArgs &a, int64_t row, int d) {
+  return a.part_chunk_rows > 0 ? ((int64_t)(d >> 4) * a.part_chunk_rows + row) * 16 + (d & 15)
+                               : row * a.head_dim + d;
+}
 __device__ __forceinline__ int64_t merge_row0(const DbsaMergeArgs &a, const DbsaMergeGroup &g, int r, int gs) {
   return a.part_tok_layout ? (int64_t)(g.q_tok0 + r / gs) * a.n_heads + g.kv_head * gs + r % gs
                            : g.part_row0 + r;
@@ -77,7 +84,7 @@ __global__ void lse_merge_kernel(DbsaMergeArgs a) {
     float v[kFast][4];
 #pragma unroll
     for (int s = 0; s < kFast; ++s)
-      if (s < g.n_splits) load4<BF16>(a.part_o, (row0 + (int64_t)s * sstride) * hd + dl, v[s]);
+      if (s < g.n_splits) load4<BF16>(a.part_o, part_off(a, row0 + (int64_t)s * sstride, dl), v[s]);
     const float l = lane < g.n_splits ? a.part_lse[row0 + (int64_t)lane * sstride] : -INFINITY;
     const float mx = warp_max(l);
     const float e = l == -INFINITY ? 0.f : __expf(l - mx);
@@ -137,7 +144,7 @@ __global__ void lse_merge_kernel(DbsaMergeArgs a) {
         for (; k + 8 <= cnt; k += 8) {
           float v[8][4];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) load4<BF16>(a.part_o, (row0 + (int64_t)(s0 + k + u) * sstride) * hd + dl, v[u]);
+          for (int u = 0; u < 8; ++u) load4<BF16>(a.part_o, part_off(a, row0 + (int64_t)(s0 + k + u) * sstride, dl), v[u]);
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
             const float wu = __shfl_sync(0xffffffffu, wl, k + u);
@@ -149,7 +156,7 @@ __global__ void lse_merge_kernel(DbsaMergeArgs a) {
         }
         for (; k < cnt; ++k) {
           float v[4];
-          load4<BF16>(a.part_o, (row0 + (int64_t)(s0 + k) * sstride) * hd + dl, v);
+          load4<BF16>(a.part_o, part_off(a, row0 + (int64_t)(s0 + k) * sstride, dl), v);
           const float wu = __shfl_sync(0xffffffffu, wl, k);
           if (wu != 0.f) {
 #pragma unroll
@@ -210,7 +217,11 @@ __global__ void lse_merge_bf16_h128_kernel(DbsaMergeArgs a) {
 #pragma unroll
   for (int o = 4; o > 0; o >>= 1) tot += __shfl_xor_sync(full, tot, o);
   const float inv = tot > 0.f ? 1.f / tot : 0.f;
-  const __nv_bfloat16 *base = reinterpret_cast<const __nv_bfloat16 *>(a.part_o) + row0 * 128 + ql * 16;
+  // this lane's 16 dims of split 0's row, and the distance between splits
+  const bool chunked = a.part_chunk_rows > 0;
+  const __nv_bfloat16 *base = reinterpret_cast<const __nv_bfloat16 *>(a.part_o) +
+                              (chunked ? ((int64_t)ql * a.part_chunk_rows + row0) * 16 : row0 * 128 + ql * 16);
+  const int64_t split_elems = chunked ? sstride * 16 : sstride * 128;
   const int src0 = threadIdx.x & 24;  // lane 0 of this quarter-warp
   float acc[16];
 #pragma unroll
@@ -226,7 +237,7 @@ __global__ void lse_merge_bf16_h128_kernel(DbsaMergeArgs a) {
         asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                      : "=r"(v[u][0]), "=r"(v[u][1]), "=r"(v[u][2]), "=r"(v[u][3]), "=r"(v[u][4]), "=r"(v[u][5]),
                        "=r"(v[u][6]), "=r"(v[u][7])
-                     : "l"(base + (int64_t)(c0 + u) * sstride * 128));
+                     : "l"(base + (int64_t)(c0 + u) * split_elems));
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const float wgt = __shfl_sync(full, wl, src0 + u);
@@ -250,6 +261,84 @@ __global__ void lse_merge_bf16_h128_kernel(DbsaMergeArgs a) {
     for (int i = 0; i < 8; ++i) w[i] = pack2_bf16(acc[2 * i], acc[2 * i + 1]);
     *reinterpret_cast<uint4 *>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
     *reinterpret_cast<uint4 *>(dst + 8) = make_uint4(w[4], w[5], w[6], w[7]);
+  }
+}
+
+// Chunk-layout form (DbsaMergeArgs.part_chunk_rows, bf16): a thread per row,
+// so one 32-byte load of column chunk c from 32 consecutive rows is 1 KB of
+// contiguous partials (the layout's point: K3's epilogue stores the same way).
+// The row's split weights exp(lse_s - max) / sum go to shared memory once;
+// then per chunk, 8 splits' loads are in flight before they are used.
+constexpr int kChunkMergeThreads = 64, kChunkMergeMaxSplits = 64;
+__global__ void __launch_bounds__(kChunkMergeThreads) lse_merge_chunked_kernel(DbsaMergeArgs a) {
+  __shared__ float wsm[kChunkMergeMaxSplits][kChunkMergeThreads];
+  pdl_wait();
+  const DbsaMergeGroup g = a.groups[blockIdx.y];
+  const int r = blockIdx.x * kChunkMergeThreads + threadIdx.x;
+  if (r >= g.rows) return;  // no block-wide sync below: a thread's weights are its own
+  const int gs = a.n_heads / a.n_kv_heads, hd = a.head_dim;
+  const int64_t sstride = a.split_stride > 0 ? a.split_stride : g.rows;
+  const int64_t row0 = merge_row0(a, g, r, gs);
+  const int n = g.n_splits;
+  // one pass of online (max, sum) over the row's split LSEs, then the weights
+  float mx = -INFINITY, tot = 0.f;
+  for (int s = 0; s < n; ++s) {
+    const float l = a.part_lse[row0 + (int64_t)s * sstride];
+    if (l == -INFINITY) continue;
+    if (l > mx) {
+      tot = tot * __expf(mx - l) + 1.f;
+      mx = l;
+    } else {
+      tot += __expf(l - mx);
+    }
+  }
+  const float inv = tot > 0.f ? 1.f / tot : 0.f;
+  for (int s = 0; s < n && s < kChunkMergeMaxSplits; ++s) {
+    const float l = a.part_lse[row0 + (int64_t)s * sstride];
+    wsm[s][threadIdx.x] = l == -INFINITY ? 0.f : __expf(l - mx) * inv;
+  }
+  auto weight = [&](int s) {  // splits past the shared table (rare) recompute theirs
+    if (s < kChunkMergeMaxSplits) return wsm[s][threadIdx.x];
+    const float l = a.part_lse[row0 + (int64_t)s * sstride];
+    return l == -INFINITY ? 0.f : __expf(l - mx) * inv;
+  };
+  const int t = g.q_tok0 + r / gs, head = g.kv_head * gs + r % gs;
+  if (a.out_lse) merge_store_lse(a, t, head, mx, tot);
+  const __nv_bfloat16 *base = reinterpret_cast<const __nv_bfloat16 *>(a.part_o) + row0 * 16;
+  const int64_t cstride = a.part_chunk_rows * 16, s_el = sstride * 16;
+  __nv_bfloat16 *dst = reinterpret_cast<__nv_bfloat16 *>(a.out) + (int64_t)t * a.out_tok_stride + (int64_t)head * hd;
+  for (int c = 0; c < hd / 16; ++c) {
+    float acc[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc[i] = 0.f;
+    const __nv_bfloat16 *bc = base + c * cstride;
+    for (int s0 = 0; s0 < n; s0 += 8) {
+      uint32_t v[8][8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (s0 + u < n)
+          asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                       : "=r"(v[u][0]), "=r"(v[u][1]), "=r"(v[u][2]), "=r"(v[u][3]), "=r"(v[u][4]), "=r"(v[u][5]),
+                         "=r"(v[u][6]), "=r"(v[u][7])
+                       : "l"(bc + (int64_t)(s0 + u) * s_el));
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const float wgt = s0 + u < n ? weight(s0 + u) : 0.f;
+        if (wgt != 0.f) {  // an empty split (LSE -inf) may hold garbage: 0 * NaN
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&v[u][i]));
+            acc[2 * i] += wgt * f.x;
+            acc[2 * i + 1] += wgt * f.y;
+          }
+        }
+      }
+    }
+    uint32_t w[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) w[i] = pack2_bf16(acc[2 * i], acc[2 * i + 1]);
+    *reinterpret_cast<uint4 *>(dst + c * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+    *reinterpret_cast<uint4 *>(dst + c * 16 + 8) = make_uint4(w[4], w[5], w[6], w[7]);
   }
 }
 
@@ -500,9 +589,17 @@ extern "C" int dbsa_lse_merge(const DbsaMergeArgs *args, void *stream) {
   if (!args) return set_error(DBSA_ERR_VALIDATION, "dbsa_lse_merge: null args");
   const DbsaMergeArgs &a = *args;
   if (a.n_groups <= 0 || a.max_rows <= 0) return DBSA_OK;
+  if (a.part_chunk_rows > 0 && (!a.part_bf16 || a.part_tok_layout || a.head_dim % 16))
+    return set_error(DBSA_ERR_CONFIG, "part_chunk_rows needs bf16 row-indexed partials and head_dim %% 16 == 0");
   dim3 grid((a.max_rows + 3) / 4, a.n_groups);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const bool small = (int64_t)a.n_groups * a.max_rows <= 16384;
+  // the chunk layout: a thread per row (the latency form for small merges reads it through part_off)
+  if (a.part_chunk_rows > 0 && !small) {
+    launch_k(lse_merge_chunked_kernel, dim3((a.max_rows + kChunkMergeThreads - 1) / kChunkMergeThreads, a.n_groups),
+             dim3(kChunkMergeThreads), 0, st, true, a);
+    return check_launch("lse_merge");
+  }
   if (a.part_bf16 && a.head_dim == 128 && !small) {
     launch_k(lse_merge_bf16_h128_kernel, dim3((a.max_rows + 15) / 16, a.n_groups), dim3(128), 0, st, true, a);
     return check_launch("lse_merge");

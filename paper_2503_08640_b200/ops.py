@@ -126,16 +126,31 @@ def kv_read(k_planes, v_planes, rows, layers, layer, tok_pos, rope, pages_dev, n
     _launched()
 
 
+PART_CHUNKED = os.environ.get("DBSA_PART_CHUNKED", "1") != "0"
+
+
+def chunk_rows_of(part_o, head_dim: int) -> int:
+    """DbsaAttnArgs / DbsaMergeArgs.part_chunk_rows of a partial buffer: bf16
+    [rows, head_dim] buffers use the 16-column chunk layout (rows = the
+    buffer's first dimension, so the K3 launch that writes it and the K3m that
+    reads it agree); anything else is row-major."""
+    if not PART_CHUNKED or part_o is None or part_o.dim() != 2 or part_o.element_size() != 2 or head_dim % 16:
+        return 0
+    return int(part_o.shape[0])
+
+
 def attention(*, q, q_tok_stride, tok_pos, tok_lo, rope, pool, aux, n_heads, n_kv_heads, head_dim,
               works_dev, n_works, segs_dev, num_m, out, out_tok_stride, part_o=None, part_lse=None,
-              row_map=None, pair_count=None, cta_works=None, n_ctas=0, after_kv_write=False):
+              row_map=None, pair_count=None, cta_works=None, n_ctas=0, after_kv_write=False,
+              part_chunk_rows=None):
     """Launch K1/K3.  `pool` / `aux` are (k_planes, v_planes, rows, layers); `row_map`
     (ROWMAP_DTYPE, device) backs DBSA_OUT_MAPPED works; `pair_count` (int64 [1],
     device) makes the kernel add the (row, key) pairs it unmasked, all heads;
     `cta_works` (int32 [n_ctas + 1], device) assigns CTA b the works
     [cta_works[b], cta_works[b+1]) (two-tile kernel only); after_kv_write: the
     launch directly follows the layer's K2w page write, so Q staging may
-    overlap it (DbsaAttnArgs.pdl_early_q)."""
+    overlap it (DbsaAttnArgs.pdl_early_q); part_chunk_rows: the partials'
+    layout (None = chunk_rows_of(part_o))."""
     kp, vp, prow, pl = pool
     ka, va, arow, al = aux if aux is not None else (None, None, 0, 0)
     a = nat.AttnArgs(
@@ -149,13 +164,14 @@ def attention(*, q, q_tok_stride, tok_pos, tok_lo, rope, pool, aux, n_heads, n_k
         part_o=nat.ptr(part_o), part_lse=nat.ptr(part_lse), row_map=nat.ptr(row_map),
         part_bf16=int(part_o is not None and part_o.element_size() == 2), pair_count=nat.ptr(pair_count),
         cta_works=nat.ptr(cta_works), n_ctas=int(n_ctas), pdl_early_q=int(bool(after_kv_write)),
-        rope_f16=nat.ptr(getattr(rope, "f16", None)))
+        rope_f16=nat.ptr(getattr(rope, "f16", None)),
+        part_chunk_rows=chunk_rows_of(part_o, head_dim) if part_chunk_rows is None else part_chunk_rows)
     nat.check(nat.load_library().dbsa_attention(ctypes.byref(a), nat.stream_handle()))
     _launched()
 
 
 def lse_merge(part_o, part_lse, groups_dev, n_groups, max_rows, n_heads, n_kv_heads, head_dim, out,
-              out_tok_stride, split_stride=0, out_lse=None, tok_layout=False):
+              out_tok_stride, split_stride=0, out_lse=None, tok_layout=False, part_chunk_rows=None):
     """K3m.  out_lse (fp32 [tokens, n_heads], device): write the merged partial
     (bf16 O into `out`, its LSE into out_lse) instead of the final output;
     tok_layout: the partials are token-major [split][tokens][n_heads][hd] (a
@@ -164,7 +180,9 @@ def lse_merge(part_o, part_lse, groups_dev, n_groups, max_rows, n_heads, n_kv_he
                       n_groups=n_groups, max_rows=max_rows, n_heads=n_heads, n_kv_heads=n_kv_heads,
                       head_dim=head_dim, out=out.data_ptr(), out_tok_stride=out_tok_stride,
                       split_stride=split_stride, part_bf16=int(part_o.element_size() == 2),
-                      part_tok_layout=int(bool(tok_layout)), out_lse=nat.ptr(out_lse))
+                      part_tok_layout=int(bool(tok_layout)), out_lse=nat.ptr(out_lse),
+                      part_chunk_rows=(0 if tok_layout else chunk_rows_of(part_o, head_dim))
+                      if part_chunk_rows is None else part_chunk_rows)
     nat.check(nat.load_library().dbsa_lse_merge(ctypes.byref(a), nat.stream_handle()))
     _launched()
 

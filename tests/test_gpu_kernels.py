@@ -449,20 +449,21 @@ def test_stage2_batch_schedules_vs_float64(schedule, hd, H, Hkv):
     assert worst < 2e-2, worst
 
 
-@pytest.mark.parametrize("n_splits", [1, 7, 19, 40])
-@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+@pytest.mark.parametrize("n_splits", [1, 7, 19, 40, 70])
+@pytest.mark.parametrize("dtype", ["bf16", "bf16-chunked", "fp32"])
 def test_lse_merge_large_vs_torch(n_splits, dtype):
     """K3m on a merge large enough for the throughput kernels (the chunk-major
     batch shape: many groups of 176 rows, bf16 or fp32 partials, some splits
     empty): the single softmax over the concatenated key set (kernels.py:52-56)
-    recomputed in float64 from the same partials."""
+    recomputed in float64 from the same partials.  bf16-chunked: the partials
+    in the 16-column chunk layout (DbsaMergeArgs.part_chunk_rows) K3 writes."""
     dev = torch.device("cuda", 0)
     H, Hkv, hd = 32, 8, 128
     gs = H // Hkv
     n_q, n_tok = 24, 44
     rows = n_tok * gs
     g = torch.Generator(device=dev).manual_seed(n_splits)
-    part_dtype = torch.bfloat16 if dtype == "bf16" else torch.float32
+    part_dtype = torch.float32 if dtype == "fp32" else torch.bfloat16
     n_groups = n_q * Hkv
     part_o = torch.randn(n_groups * n_splits * rows, hd, generator=g, device=dev).to(part_dtype)
     part_lse = torch.randn(n_groups * n_splits * rows, generator=g, device=dev) * 3
@@ -473,7 +474,14 @@ def test_lse_merge_large_vs_torch(n_splits, dtype):
             i = q * Hkv + kv
             groups[i] = (i * n_splits * rows, rows, n_splits, q * n_tok, kv)
     out = torch.zeros(n_q * n_tok, H * hd, dtype=torch.bfloat16, device=dev)
-    ops.lse_merge(part_o, part_lse, ops.to_device(groups, dev), n_groups, rows, H, Hkv, hd, out, H * hd)
+    if dtype == "bf16-chunked":
+        R = part_o.shape[0]
+        chunked = part_o.view(R, hd // 16, 16).transpose(0, 1).contiguous().view(R, hd)  # [hd/16][R][16] in memory
+        ops.lse_merge(chunked, part_lse, ops.to_device(groups, dev), n_groups, rows, H, Hkv, hd, out, H * hd,
+                      part_chunk_rows=R)
+    else:
+        ops.lse_merge(part_o, part_lse, ops.to_device(groups, dev), n_groups, rows, H, Hkv, hd, out, H * hd,
+                      part_chunk_rows=0)
     torch.cuda.synchronize()
     po = part_o.double().view(n_groups, n_splits, rows, hd)
     pl = part_lse.double().view(n_groups, n_splits, rows)
@@ -515,7 +523,7 @@ def test_lse_merge_two_level_equals_one_level(n_local):
                 i = q * Hkv + kv
                 grp[i] = (i * ns * rows, rows, ns, q * n_tok, kv)
         ops.lse_merge(po, pl, ops.to_device(grp, dev), n_groups, rows, H, Hkv, hd, canon_o[r], H * hd,
-                      out_lse=canon_lse[r])
+                      out_lse=canon_lse[r], part_chunk_rows=0)
         parts.append((po[: n_groups * ns * rows].double().view(n_groups, ns, rows, hd),
                       pl[: n_groups * ns * rows].double().view(n_groups, ns, rows)))
     fin = np.zeros(n_groups, dtype=ops.MERGE_DTYPE)
