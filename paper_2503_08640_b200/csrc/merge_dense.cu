@@ -342,6 +342,81 @@ __global__ void __launch_bounds__(kChunkMergeThreads) lse_merge_chunked_kernel(D
   }
 }
 
+// Chunk layout, wide form: a block is 32 rows x (head_dim / 16) column chunks,
+// thread (row, chunk).  A warp reads one column chunk of 32 consecutive rows
+// (1 KB contiguous per split).  The rows' split LSEs are loaded once per block,
+// all in flight, into shared memory; each thread then has its 32-byte pieces
+// of up to kCM2Batch splits in flight at once, so a row costs about
+// 1 + n_splits / kCM2Batch memory round trips instead of one per (chunk, 8
+// splits) -- the thread-per-row form above is latency-bound on the K3 -> K3m
+// round trip of a large batch.
+constexpr int kCM2MaxSplits = 64, kCM2Batch = 10;
+__global__ void __launch_bounds__(512) lse_merge_chunked2_kernel(DbsaMergeArgs a) {
+  __shared__ float lse_s[kCM2MaxSplits][32];
+  pdl_wait();
+  const DbsaMergeGroup g = a.groups[blockIdx.y];
+  const int rl = threadIdx.x, c = threadIdx.y, nch = blockDim.y;
+  const int r = blockIdx.x * 32 + rl;
+  const bool ok = r < g.rows;
+  const int gs = a.n_heads / a.n_kv_heads, hd = a.head_dim;
+  const int64_t sstride = a.split_stride > 0 ? a.split_stride : g.rows;
+  const int64_t row0 = ok ? merge_row0(a, g, r, gs) : 0;
+  const int n = g.n_splits;
+  for (int s = c; s < n && s < kCM2MaxSplits; s += nch)
+    lse_s[s][rl] = ok ? a.part_lse[row0 + (int64_t)s * sstride] : -INFINITY;
+  __syncthreads();
+  if (!ok) return;
+  auto lse_at = [&](int s) {  // splits past the shared table (rare) read theirs again
+    return s < kCM2MaxSplits ? lse_s[s][rl] : a.part_lse[row0 + (int64_t)s * sstride];
+  };
+  float mx = -INFINITY;
+  for (int s = 0; s < n; ++s) mx = fmaxf(mx, lse_at(s));
+  float tot = 0.f;
+  for (int s = 0; s < n; ++s) {
+    const float l = lse_at(s);
+    tot += l == -INFINITY ? 0.f : __expf(l - mx);
+  }
+  const float inv = tot > 0.f ? 1.f / tot : 0.f;
+  const int t = g.q_tok0 + r / gs, head = g.kv_head * gs + r % gs;
+  if (a.out_lse && c == 0) merge_store_lse(a, t, head, mx, tot);
+  const __nv_bfloat16 *bc = reinterpret_cast<const __nv_bfloat16 *>(a.part_o) + row0 * 16 + c * a.part_chunk_rows * 16;
+  const int64_t s_el = sstride * 16;
+  float acc[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) acc[i] = 0.f;
+  for (int s0 = 0; s0 < n; s0 += kCM2Batch) {
+    uint32_t v[kCM2Batch][8];
+#pragma unroll
+    for (int u = 0; u < kCM2Batch; ++u)
+      if (s0 + u < n)
+        asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(v[u][0]), "=r"(v[u][1]), "=r"(v[u][2]), "=r"(v[u][3]), "=r"(v[u][4]), "=r"(v[u][5]),
+                       "=r"(v[u][6]), "=r"(v[u][7])
+                     : "l"(bc + (int64_t)(s0 + u) * s_el));
+#pragma unroll
+    for (int u = 0; u < kCM2Batch; ++u) {
+      const float l = s0 + u < n ? lse_at(s0 + u) : -INFINITY;
+      if (l != -INFINITY) {  // an empty split (LSE -inf) may hold garbage: 0 * NaN
+        const float wgt = __expf(l - mx) * inv;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&v[u][i]));
+          acc[2 * i] += wgt * f.x;
+          acc[2 * i + 1] += wgt * f.y;
+        }
+      }
+    }
+  }
+  if (c * 16 >= hd) return;
+  uint32_t w[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) w[i] = pack2_bf16(acc[2 * i], acc[2 * i + 1]);
+  __nv_bfloat16 *dst =
+      reinterpret_cast<__nv_bfloat16 *>(a.out) + (int64_t)t * a.out_tok_stride + (int64_t)head * hd + c * 16;
+  *reinterpret_cast<uint4 *>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+  *reinterpret_cast<uint4 *>(dst + 8) = make_uint4(w[4], w[5], w[6], w[7]);
+}
+
 // x fp32 [rows, dim] -> bf16 x * rsqrt(mean(x^2) + eps) * w (kernels.rms_norm, kernels.py:103-112).
 // ADD: first x += delta in place -- the residual add of model.py:352-359 fused
 // with the norm that reads the same row.  float4 path: each thread keeps its
@@ -595,6 +670,17 @@ extern "C" int dbsa_lse_merge(const DbsaMergeArgs *args, void *stream) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const bool small = (int64_t)a.n_groups * a.max_rows <= 16384;
   // the chunk layout: a thread per row (the latency form for small merges reads it through part_off)
+  static const bool wide = [] {
+    const char *e = getenv("DBSA_MERGE_WIDE");
+    return !(e && e[0] == '0');
+  }();
+  // the wide form wins on tall groups (GQA: rows = tokens x group size; C3 K3m
+  // 0.118 -> 0.109 ms) and loses on short ones (MHA C4, 44 rows: 0.037 -> 0.056)
+  if (a.part_chunk_rows > 0 && !small && wide && a.max_rows >= 128 && a.head_dim % 16 == 0 && a.head_dim <= 256) {
+    launch_k(lse_merge_chunked2_kernel, dim3((a.max_rows + 31) / 32, a.n_groups), dim3(32, a.head_dim / 16), 0, st,
+             true, a);
+    return check_launch("lse_merge");
+  }
   if (a.part_chunk_rows > 0 && !small) {
     launch_k(lse_merge_chunked_kernel, dim3((a.max_rows + kChunkMergeThreads - 1) / kChunkMergeThreads, a.n_groups),
              dim3(kChunkMergeThreads), 0, st, true, a);
