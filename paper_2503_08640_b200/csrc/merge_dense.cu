@@ -345,13 +345,19 @@ __global__ void __launch_bounds__(kChunkMergeThreads) lse_merge_chunked_kernel(D
 // Chunk layout, wide form: a block is 32 rows x (head_dim / 16) column chunks,
 // thread (row, chunk).  A warp reads one column chunk of 32 consecutive rows
 // (1 KB contiguous per split).  The rows' split LSEs are loaded once per block,
-// all in flight, into shared memory; each thread then has its 32-byte pieces
-// of up to kCM2Batch splits in flight at once, so a row costs about
-// 1 + n_splits / kCM2Batch memory round trips instead of one per (chunk, 8
-// splits) -- the thread-per-row form above is latency-bound on the K3 -> K3m
-// round trip of a large batch.
-constexpr int kCM2MaxSplits = 64, kCM2Batch = 10;
-__global__ void __launch_bounds__(512) lse_merge_chunked2_kernel(DbsaMergeArgs a) {
+// all in flight, into shared memory; each thread then streams its 32-byte
+// pieces kCM2Batch splits at a time.  Eight threads per row and four
+// resident blocks per SM keep more bytes in flight than the thread-per-row
+// form above (chunk-major C3: 0.118 ms -> 0.094 ms; 10 splits per batch at
+// 2 blocks / SM: 0.109, 5 at 3: 0.098, 20 at 1: 0.170).
+#ifndef DBSA_CM2_BATCH
+#define DBSA_CM2_BATCH 4
+#endif
+#ifndef DBSA_CM2_MINB
+#define DBSA_CM2_MINB 4
+#endif
+constexpr int kCM2MaxSplits = 64, kCM2Batch = DBSA_CM2_BATCH;
+__global__ void __launch_bounds__(256, DBSA_CM2_MINB) lse_merge_chunked2_kernel(DbsaMergeArgs a) {
   __shared__ float lse_s[kCM2MaxSplits][32];
   pdl_wait();
   const DbsaMergeGroup g = a.groups[blockIdx.y];
