@@ -356,6 +356,9 @@ __global__ void __launch_bounds__(kChunkMergeThreads) lse_merge_chunked_kernel(D
 #ifndef DBSA_CM2_MINB
 #define DBSA_CM2_MINB 4
 #endif
+#ifndef DBSA_CM2_MIN_ROWS
+#define DBSA_CM2_MIN_ROWS 128
+#endif
 constexpr int kCM2MaxSplits = 64, kCM2Batch = DBSA_CM2_BATCH;
 __global__ void __launch_bounds__(256, DBSA_CM2_MINB) lse_merge_chunked2_kernel(DbsaMergeArgs a) {
   __shared__ float lse_s[kCM2MaxSplits][32];
@@ -682,7 +685,7 @@ extern "C" int dbsa_lse_merge(const DbsaMergeArgs *args, void *stream) {
   }();
   // the wide form wins on tall groups (GQA: rows = tokens x group size; C3 K3m
   // 0.118 -> 0.109 ms) and loses on short ones (MHA C4, 44 rows: 0.037 -> 0.056)
-  if (a.part_chunk_rows > 0 && !small && wide && a.max_rows >= 128 && a.head_dim % 16 == 0 && a.head_dim <= 256) {
+  if (a.part_chunk_rows > 0 && !small && wide && a.max_rows >= DBSA_CM2_MIN_ROWS && a.head_dim % 16 == 0 && a.head_dim <= 256) {
     launch_k(lse_merge_chunked2_kernel, dim3((a.max_rows + 31) / 32, a.n_groups), dim3(32, a.head_dim / 16), 0, st,
              true, a);
     return check_launch("lse_merge");
