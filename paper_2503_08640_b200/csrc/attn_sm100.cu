@@ -457,7 +457,7 @@ __device__ __forceinline__ void stage_refs_coop(const AttnParams &p, const DbsaA
 // into the Q tile.  HALF: the fp16 rotation table (AttnParams.rope_h).
 template <int HDP, bool HALF>
 __device__ __forceinline__ void stage_load_coop(const AttnParams &p, uint8_t *q_tile, int m, int q4, int lane,
-                                                const QRefs<HDP> &x) {
+                                                const QRefs<HDP> &x, int sw = -1) {
   constexpr int QSW = AttnCfg<HDP, 1>::QSW;
   constexpr int NCH = QRefs<HDP>::NCH, RPI = QRefs<HDP>::RPI, NIT = QRefs<HDP>::NIT;
   const int c = lane % NCH, rsub = lane / NCH, half = HDP / 2;
@@ -495,6 +495,12 @@ __device__ __forceinline__ void stage_load_coop(const AttnParams &p, uint8_t *q_
         for (int v = 0; v < 4; ++v) cs4[k][v] = __ldg(rp + v);
       }
     }
+#ifdef DBSA_STAMPS
+    if (sw >= 0 && m == 0 && q4 == 0 && lane == 0 && i0 == 0) {  // the first batch's loads are back
+      asm volatile("" ::"r"(lo4[0].x), "r"(hi4[0].x), "r"(rh4[0][0].x), "r"(rh4[0][1].x));
+      WSTAMP(11, sw);
+    }
+#endif
 #pragma unroll
     for (int k = 0; k < QB; ++k) {
       const int it = i0 + k;
@@ -514,14 +520,21 @@ __device__ __forceinline__ void stage_load_coop(const AttnParams &p, uint8_t *q_
 #pragma unroll
         for (int j = 0; j < 16; ++j) cs[j] = reinterpret_cast<const float *>(cs4[k])[j];
       }
-      const float keep = tok[it] >= 0 ? 1.f : 0.f;
+      // rotate two pairs per FFMA2 / FMUL2.  A row past the work's rows keeps
+      // the (finite) q of the safe row it read: its scores feed only its own
+      // softmax row, whose O is never stored
       float a[8], b[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const float cc = cs[2 * j] * keep, sn = cs[2 * j + 1] * keep;
-        const float xl = __bfloat162float(lo[j]), yh = __bfloat162float(hi[j]);
-        a[j] = xl * cc - yh * sn;
-        b[j] = xl * sn + yh * cc;
+      for (int j = 0; j < 8; j += 2) {
+        const float2 xl = make_float2(__bfloat162float(lo[j]), __bfloat162float(lo[j + 1]));
+        const float2 yh = make_float2(__bfloat162float(hi[j]), __bfloat162float(hi[j + 1]));
+        const float2 cc = make_float2(cs[2 * j], cs[2 * j + 2]), sn = make_float2(cs[2 * j + 1], cs[2 * j + 3]);
+        const float2 av = ffma2(xl, cc, fmul2(yh, make_float2(-sn.x, -sn.y)));
+        const float2 bv = ffma2(xl, sn, fmul2(yh, cc));
+        a[j] = av.x;
+        a[j + 1] = av.y;
+        b[j] = bv.x;
+        b[j + 1] = bv.y;
       }
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
@@ -592,10 +605,16 @@ __device__ __forceinline__ void stage_load_coop(const AttnParams &p, uint8_t *q_
 // (hd == HDP, 16-byte aligned rows); the caller falls back to load_q_row.
 template <int HDP, bool HALF>
 __device__ __forceinline__ void stage_q_coop(const AttnParams &p, const DbsaAttnWork &w, int m, uint8_t *q_tile,
-                                             int q4, int lane, bool restage, int shift) {
+                                             int q4, int lane, bool restage, int shift, int sw = -1) {
   QRefs<HDP> x;
   stage_refs_coop<HDP>(p, w, m, q4, lane, restage, shift, x);
-  stage_load_coop<HDP, HALF>(p, q_tile, m, q4, lane, x);
+#ifdef DBSA_STAMPS
+  if (sw >= 0 && m == 0 && q4 == 0 && lane == 0) {  // the row refs are back
+    asm volatile("" ::"r"(x.tok[0]), "r"(x.rrow[0]));
+    WSTAMP(10, sw);
+  }
+#endif
+  stage_load_coop<HDP, HALF>(p, q_tile, m, q4, lane, x, sw);
 }
 
 template <int HDP, int NUM_M>
@@ -864,10 +883,10 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
     uint32_t n_pairs = 0;  // pair counter (p.pair_count)
 
     const bool coop = HDP >= 16 && p.head_dim == HDP && (p.q_tok_stride & 7) == 0;
-    auto stage_q = [&](const DbsaAttnWork &wq, bool restage, int shift) {
+    auto stage_q = [&](const DbsaAttnWork &wq, bool restage, int shift, int sw = -1) {
       if (p.dbg & 16) return;  // profiling: keep whatever Q the tile holds
       if (coop && p.rope_h) {
-        stage_q_coop<HDP, true>(p, wq, m, q_tile, q4, lane, restage, shift);
+        stage_q_coop<HDP, true>(p, wq, m, q_tile, q4, lane, restage, shift, sw);
       } else if (coop) {
         stage_q_coop<HDP, false>(p, wq, m, q_tile, q4, lane, restage, shift);
       } else {
@@ -1047,7 +1066,7 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
       if (wn < wr.end) {
         w_nx = p.works[wn];
         load_row(w_nx);
-        stage_q(w_nx, false, 0);
+        stage_q(w_nx, false, 0, wk);
         fence_proxy_async_smem();
         mbar_arrive(&q_full[m]);
       }

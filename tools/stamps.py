@@ -39,3 +39,6 @@ if hasattr(lib, "dbsa_debug_wstamps") and lib.dbsa_debug_wstamps(wb, 256 * 12) =
             print(f"work boundary m{m}: stage next Q {np.median(w[:, b+1]-w[:, b]):7.0f}  wait O {np.median(w[:, b+2]-w[:, b+1]):7.0f}"
                   f"  epilogue {np.median(w[:, b+3]-w[:, b+2]):7.0f}  work period {np.median(np.diff(w[:, b])):7.0f}  (works {len(w)})")
         print(f"m0 epilogue done -> loop top work loaded {np.median(w[1:, 8]-w[:-1, 3]):7.0f}  -> first seg loaded {np.median(w[:, 9]-w[:, 8]):7.0f}")
+        if (w[:, 10] > 0).all() and (w[:, 11] > 0).all():
+            print(f"m0 staging: last tile -> row refs back {np.median(w[:, 10]-w[:, 0]):7.0f}  -> first q/rope loads back "
+                  f"{np.median(w[:, 11]-w[:, 10]):7.0f}  -> Q tile stored {np.median(w[:, 1]-w[:, 11]):7.0f}")
