@@ -50,6 +50,10 @@ constexpr int kBN = 128;  // keys per tile
 #ifndef DBSA_EPI_COLS
 #define DBSA_EPI_COLS 128  // O columns per epilogue TMEM round trip
 #endif
+// one exp2 pair in four on the FMA pipe (polynomial) instead of MUFU (1)
+#ifndef DBSA_POLY_EXP
+#define DBSA_POLY_EXP 1
+#endif
 #ifndef DBSA_QSTAGE_BATCH
 #define DBSA_QSTAGE_BATCH 8
 #endif
@@ -326,12 +330,16 @@ __device__ __forceinline__ void epilogue_cols(const AttnParams &p, const float (
   if (out_mode != DBSA_OUT_BF16 && p.part_chunk_rows > 0) {
     // 16-column chunk layout: this row's chunk k at ((c0/16 + k) * chunk_rows + part_row) * 16
     __nv_bfloat16 *base = reinterpret_cast<__nv_bfloat16 *>(p.part_o) + part_row * 16;
+    const float2 il = make_float2(inv_l, inv_l);
 #pragma unroll
     for (int c = 0; c < CW; c += 16) {
       if (c0 + c >= hd) break;
       uint32_t w[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) w[i] = pack_bf16(o[c + 2 * i] * inv_l, o[c + 2 * i + 1] * inv_l);
+      for (int i = 0; i < 8; ++i) {
+        const float2 v = fmul2(make_float2(o[c + 2 * i], o[c + 2 * i + 1]), il);
+        w[i] = pack_bf16(v.x, v.y);
+      }
       asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(
                        base + (int64_t)((c0 + c) >> 4) * p.part_chunk_rows * 16),
                    "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
@@ -344,11 +352,15 @@ __device__ __forceinline__ void epilogue_cols(const AttnParams &p, const float (
                              ? p.out + (int64_t)t * p.out_tok_stride + (int64_t)head * hd + c0
                              : reinterpret_cast<__nv_bfloat16 *>(p.part_o) + part_row * (int64_t)hd + c0;
     if (CW >= 16 && full && (reinterpret_cast<uintptr_t>(dst) & 31) == 0) {
+      const float2 il = make_float2(inv_l, inv_l);
 #pragma unroll
       for (int c = 0; c < CW; c += 16) {
         uint32_t w[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) w[i] = pack_bf16(o[c + 2 * i] * inv_l, o[c + 2 * i + 1] * inv_l);
+        for (int i = 0; i < 8; ++i) {
+          const float2 v = fmul2(make_float2(o[c + 2 * i], o[c + 2 * i + 1]), il);
+          w[i] = pack_bf16(v.x, v.y);
+        }
         asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst + c), "r"(w[0]), "r"(w[1]),
                      "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
                      : "memory");
@@ -1027,7 +1039,8 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
 #pragma unroll
             for (int c = 0; c < 64; c += 2) {
               const float2 a = ffma2(make_float2(x[h * 64 + c], x[h * 64 + c + 1]), sl2v, nmv);
-              const float2 e = ((c >> 1) & 3) == 3 ? exp2_fma2(a) : make_float2(fast_exp2(a.x), fast_exp2(a.y));
+              const float2 e = DBSA_POLY_EXP && ((c >> 1) & 3) == 3 ? exp2_fma2(a)
+                                                                      : make_float2(fast_exp2(a.x), fast_exp2(a.y));
               ps[(c >> 1) & 1] = fadd2(ps[(c >> 1) & 1], e);
               pk[c >> 1] = pack_bf16(e.x, e.y);
             }
