@@ -135,6 +135,7 @@ struct AttnParams {
   const __half2 *rope_h;  // optional fp16 copy of rope: the Q staging's rotation table
   int64_t rope_rows;
   int32_t n_heads, n_kv_heads, head_dim, gs;
+  uint32_t gs_magic;  // ceil(2^32 / gs) for gs > 1 (0 for gs == 1): row / gs by one IMAD.HI (rows < 2^16)
   float scale_log2;
   const DbsaAttnWork *works;
   int32_t n_works;
@@ -301,10 +302,16 @@ struct RowRef {
   int t, head, rope_row;
   int64_t part_row;
 };
+// r / gs and r % gs for a row index r < 2^16 (exact: the magic's error term
+// r * (magic * gs - 2^32) / 2^32 stays below 1 / gs)
+__device__ __forceinline__ int gs_div(const AttnParams &p, int r) {
+  return p.gs_magic ? (int)__umulhi((uint32_t)r, p.gs_magic) : r;
+}
 __device__ __forceinline__ RowRef row_ref(const AttnParams &p, const DbsaAttnWork &w, int r) {
   RowRef x;
   x.valid = r < w.n_tok * p.gs;
-  const int i = x.valid ? r / p.gs : 0, hl = x.valid ? r % p.gs : 0;
+  const int q = gs_div(p, r);
+  const int i = x.valid ? q : 0, hl = x.valid ? r - q * p.gs : 0;
   x.head = w.kv_head * p.gs + hl;
   if (w.out_mode == DBSA_OUT_MAPPED) {
     const DbsaRowMap e = p.row_map[w.q_tok0 + i];
@@ -477,7 +484,10 @@ __device__ __forceinline__ void stage_load_coop(const AttnParams &p, uint8_t *q_
   const int(&rrow)[NIT] = x.rrow;
   int head[NIT];
 #pragma unroll
-  for (int it = 0; it < NIT; ++it) head[it] = x.head0 + (m * 128 + q4 * 32 + it * RPI + rsub) % p.gs;
+  for (int it = 0; it < NIT; ++it) {
+    const int rr = m * 128 + q4 * 32 + it * RPI + rsub;
+    head[it] = x.head0 + rr - gs_div(p, rr) * p.gs;
+  }
 #if DBSA_QSTAGE_BATCH > 1
   // phase B, batched: the loads of QB iterations are issued before any of
   // them is used, so QB round trips overlap (QB x 24 registers in flight)
@@ -1660,6 +1670,7 @@ extern "C" int dbsa_attention(const DbsaAttnArgs *args, void *stream) {
   p.n_kv_heads = a.n_kv_heads;
   p.head_dim = a.head_dim;
   p.gs = a.n_heads / a.n_kv_heads;
+  p.gs_magic = p.gs > 1 ? (uint32_t)((0x100000000ull + (uint64_t)p.gs - 1) / (uint64_t)p.gs) : 0u;
   p.scale_log2 = a.scale * 1.4426950408889634f;
   p.works = a.works;
   p.n_works = a.n_works;

@@ -494,12 +494,15 @@ def test_lse_merge_large_vs_torch(n_splits, dtype):
 
 
 @pytest.mark.parametrize("n_local", [1, 24])
-def test_lse_merge_two_level_equals_one_level(n_local):
+@pytest.mark.parametrize("chunked", [False, True])
+def test_lse_merge_two_level_equals_one_level(n_local, chunked):
     """The C5 merge (engine.ShardedStage2): each of 3 "ranks" merges its own
     splits into a bf16 (O, LSE) per (token, head) (out_lse mode; a rank with
     no split for a row yields O = 0, LSE = -inf), and the token-layout merge
     of the 3 results equals the single softmax over all splits
-    (kernels.py:52-56) within the bf16 tolerance."""
+    (kernels.py:52-56) within the bf16 tolerance.  chunked: the per-rank
+    partials in K3's 16-column chunk layout (the chunk-major schedule's), which
+    at 12 queries takes the wide K3m form in out_lse mode."""
     dev = torch.device("cuda", 0)
     H, Hkv, hd = 32, 8, 128
     gs = H // Hkv
@@ -522,8 +525,14 @@ def test_lse_merge_two_level_equals_one_level(n_local):
             for kv in range(Hkv):
                 i = q * Hkv + kv
                 grp[i] = (i * ns * rows, rows, ns, q * n_tok, kv)
-        ops.lse_merge(po, pl, ops.to_device(grp, dev), n_groups, rows, H, Hkv, hd, canon_o[r], H * hd,
-                      out_lse=canon_lse[r], part_chunk_rows=0)
+        if chunked:
+            R = po.shape[0]
+            po_c = po.view(R, hd // 16, 16).transpose(0, 1).contiguous().view(R, hd)
+            ops.lse_merge(po_c, pl, ops.to_device(grp, dev), n_groups, rows, H, Hkv, hd, canon_o[r], H * hd,
+                          out_lse=canon_lse[r], part_chunk_rows=R)
+        else:
+            ops.lse_merge(po, pl, ops.to_device(grp, dev), n_groups, rows, H, Hkv, hd, canon_o[r], H * hd,
+                          out_lse=canon_lse[r], part_chunk_rows=0)
         parts.append((po[: n_groups * ns * rows].double().view(n_groups, ns, rows, hd),
                       pl[: n_groups * ns * rows].double().view(n_groups, ns, rows)))
     fin = np.zeros(n_groups, dtype=ops.MERGE_DTYPE)
