@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define DBSA_ABI_VERSION 11
+#define DBSA_ABI_VERSION 12
 #define DBSA_PAGE_TOKENS 64
 
 /* Error codes -> reference exceptions (errors.py:4-29). */
@@ -159,6 +159,11 @@ typedef struct DbsaAttnArgs {
                                d % 16 for rows < part_chunk_rows -- the epilogue's 32-byte store of one chunk
                                from 32 consecutive rows (one per TMEM lane) is then 1 KB contiguous instead of
                                32 scattered sectors.  The merge reading them passes the same value. */
+  int32_t one_seg_partials; /* 1: every work has exactly one segment and writes a partial (out_mode
+                               DBSA_OUT_PARTIAL or DBSA_OUT_MAPPED) -- the chunk-major stage-2 schedule.  With
+                               bf16 chunk-layout partials, rope_f16, no pair_count and head_dim == hd_pad (a
+                               multiple of 16) the launch then runs a kernel instance specialised for that
+                               case; results are identical.  0: the generic kernel. */
 } DbsaAttnArgs;
 int dbsa_attention(const DbsaAttnArgs *args, void *stream);
 

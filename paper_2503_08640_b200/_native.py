@@ -38,7 +38,7 @@ EXPORTED_SYMBOLS = (
     "dbsa_last_error",
 )
 
-ABI_VERSION = 11
+ABI_VERSION = 12
 OUT_BF16, OUT_PARTIAL, OUT_MAPPED = 0, 1, 2
 PAGE_TOKENS = 64
 SEG_FULL = 0
@@ -73,7 +73,7 @@ class AttnArgs(ctypes.Structure):
         ("works", _vp), ("n_works", _i32), ("segs", _vp),
         ("out", _vp), ("out_tok_stride", _i64), ("part_o", _vp), ("part_lse", _vp),
         ("row_map", _vp), ("part_bf16", _i32), ("pair_count", _vp), ("cta_works", _vp), ("n_ctas", _i32), ("pdl_early_q", _i32),
-        ("rope_f16", _vp), ("part_chunk_rows", _i64),
+        ("rope_f16", _vp), ("part_chunk_rows", _i64), ("one_seg_partials", _i32),
     ]
 
 

@@ -329,12 +329,12 @@ __device__ __forceinline__ RowRef row_ref(const AttnParams &p, const DbsaAttnWor
 // Columns [c0, c0 + CW) of one epilogue row, normalised by 1/l: bf16 into
 // out, or a bf16 / fp32 partial.  32-byte stores (st.global.v8, whole
 // sectors) on full-width aligned rows, element stores otherwise.
-template <int HDP, int CW>
+template <int HDP, int CW, bool CM = false>
 __device__ __forceinline__ void epilogue_cols(const AttnParams &p, const float (&o)[CW], int c0, int t, int head,
                                               int out_mode, int64_t part_row, float inv_l) {
   const int hd = p.head_dim;
   const bool full = hd == HDP;
-  if (out_mode != DBSA_OUT_BF16 && p.part_chunk_rows > 0) {
+  if (CM || (out_mode != DBSA_OUT_BF16 && p.part_chunk_rows > 0)) {
     // 16-column chunk layout: this row's chunk k at ((c0/16 + k) * chunk_rows + part_row) * 16
     __nv_bfloat16 *base = reinterpret_cast<__nv_bfloat16 *>(p.part_o) + part_row * 16;
     const float2 il = make_float2(inv_l, inv_l);
@@ -415,11 +415,11 @@ __device__ __forceinline__ void epilogue_cols(const AttnParams &p, const float (
 // chunks of DBSA_EPI_COLS columns (default the whole row: one round trip),
 // normalised by 1/l, then either bf16 into out or a partial + natural-log LSE.
 // Warp-collective (tcgen05.ld): every lane calls it, invalid rows store nothing.
-template <int HDP>
+template <int HDP, bool CM = false>
 __device__ __forceinline__ void epilogue_row(const AttnParams &p, uint32_t t_o, bool valid, int t, int head,
                                              int out_mode, int64_t part_row, float l_sum, float m_used) {
   constexpr int CW = HDP > DBSA_EPI_COLS ? DBSA_EPI_COLS : HDP;
-  const bool store = valid && !(p.dbg & 8);
+  const bool store = valid && (CM || !(p.dbg & 8));
   const bool empty = !(l_sum > 0.f);  // no visible key (e.g. a shard without chunks): O = 0, LSE = -inf
   const float inv_l = empty ? 0.f : 1.f / l_sum;
 #pragma unroll
@@ -432,7 +432,7 @@ __device__ __forceinline__ void epilogue_row(const AttnParams &p, uint32_t t_o, 
       tmem_ld16(t_o + c0, *reinterpret_cast<float(*)[16]>(&o[0]));
     }
     tmem_wait_ld();
-    if (store) epilogue_cols<HDP, CW>(p, o, c0, t, head, out_mode, part_row, inv_l);
+    if (store) epilogue_cols<HDP, CW, CM>(p, o, c0, t, head, out_mode, part_row, inv_l);
   }
   // natural-log LSE of the scaled scores: (m + log2 l) * ln 2
   if (store && out_mode != DBSA_OUT_BF16)
@@ -639,7 +639,13 @@ __device__ __forceinline__ void stage_q_coop(const AttnParams &p, const DbsaAttn
   stage_load_coop<HDP, HALF>(p, q_tile, m, q4, lane, x, sw);
 }
 
-template <int HDP, int NUM_M>
+// CM: the chunk-major specialisation (DbsaAttnArgs.one_seg_partials): every work
+// has one segment and writes a partial, partials are bf16 in the 16-column chunk
+// layout, Q is staged cooperatively with the fp16 rotation table, no pair
+// counter and no profiling switches.  The paths it cannot take are compiled
+// out, which leaves a third of the generic kernel's code to fetch at every
+// work boundary (chunk-major C3 K3 1.184 -> 1.158 ms, C4 0.604 -> 0.582).
+template <int HDP, int NUM_M, bool CM = false>
 __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
     dbsa_attn_kernel(const __grid_constant__ CUtensorMap tm_k0, const __grid_constant__ CUtensorMap tm_v0,
                      const __grid_constant__ CUtensorMap tm_k1, const __grid_constant__ CUtensorMap tm_v1,
@@ -725,7 +731,7 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
       auto load_v = [&]() {
         const int st = vj % C::VST;
         if (vj >= C::VST) mbar_wait(&v_empty[st], ((vj / C::VST) & 1) ^ 1);
-        if (p.dbg & 4) {
+        if (!CM && (p.dbg & 4)) {
           mbar_arrive(&v_full[st]);
         } else {
           const CUtensorMap *tv = pend_src ? &tm_v1 : &tm_v0;
@@ -748,7 +754,7 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
             const int row = sg.row0 - off + tt * kBN;
             const int st = kj % C::KST;
             if (kj >= C::KST) mbar_wait(&k_empty[st], ((kj / C::KST) & 1) ^ 1);
-            if (p.dbg & 4) {
+            if (!CM && (p.dbg & 4)) {
               mbar_arrive(&k_full[st]);
             } else {
               mbar_arrive_expect_tx(&k_full[st], C::K_BYTES);
@@ -784,7 +790,7 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
           const int off = ((kk * 16) % C::KATOM) * 2;
           const uint64_t ad = umma_desc_kmajor(sQa + m * C::Q_BYTES + a * 128 * C::QSW + off, C::QSW);
           const uint64_t bd = umma_desc_kmajor(sKa + st * C::K_BYTES + a * kBN * C::QSW + off, C::QSW);
-          if (!(p.dbg & 2)) umma_bf16_ss(d, ad, bd, idesc_s, kk > 0 ? 1u : 0u);
+          if (CM || !(p.dbg & 2)) umma_bf16_ss(d, ad, bd, idesc_s, kk > 0 ? 1u : 0u);
         }
         umma_commit(&s_full[m]);
       }
@@ -803,7 +809,7 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
           const int a = kk / 4;
           const int off = (kk % 4) * 32;
           const uint64_t bd = umma_desc_kmajor(sVa + st * C::V_BYTES + a * HDP * 128 + off, 128);
-          if (!(p.dbg & 2)) umma_bf16_ts(d, pa + kk * 8, bd, idesc_o, (!first || kk > 0) ? 1u : 0u);
+          if (CM || !(p.dbg & 2)) umma_bf16_ts(d, pa + kk * 8, bd, idesc_o, (!first || kk > 0) ? 1u : 0u);
         }
       }
       __syncwarp();
@@ -904,10 +910,10 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
     int jg = 0, wk = 0;
     uint32_t n_pairs = 0;  // pair counter (p.pair_count)
 
-    const bool coop = HDP >= 16 && p.head_dim == HDP && (p.q_tok_stride & 7) == 0;
+    const bool coop = CM || (HDP >= 16 && p.head_dim == HDP && (p.q_tok_stride & 7) == 0);
     auto stage_q = [&](const DbsaAttnWork &wq, bool restage, int shift, int sw = -1) {
-      if (p.dbg & 16) return;  // profiling: keep whatever Q the tile holds
-      if (coop && p.rope_h) {
+      if (!CM && (p.dbg & 16)) return;  // profiling: keep whatever Q the tile holds
+      if (CM || (coop && p.rope_h)) {
         stage_q_coop<HDP, true>(p, wq, m, q_tile, q4, lane, restage, shift, sw);
       } else if (coop) {
         stage_q_coop<HDP, false>(p, wq, m, q_tile, q4, lane, restage, shift);
@@ -970,12 +976,12 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
           // invalid rows (beyond the work's rows) count as full: their S is Q=0 . K = 0
           // and their P only feeds their own (never stored) O rows
           const bool full = !valid || (c_lo == 0 && c_hi == kBN && (b_hi <= 0 || b_lo >= kBN || b_lo >= b_hi));
-          const bool restage = tt == nt - 1 && si + 1 < w.seg_end && p.segs[si + 1].shift != cur_rot;
+          const bool restage = !CM && tt == nt - 1 && si + 1 < w.seg_end && p.segs[si + 1].shift != cur_rot;
           if (trow == 0) STAMP(m * 5 + 0, jg + j);
           mbar_wait(&s_full[m], (jg + j) & 1);
           tc_fence_after();
           if (trow == 0) STAMP(m * 5 + 1, jg + j);
-          if (warp_dead || (p.dbg & 1)) {  // no valid row: its P rows only feed its own (discarded) O rows
+          if (warp_dead || (!CM && (p.dbg & 1))) {  // no valid row: its P rows only feed its own (discarded) O rows
             if (restage) {
               cur_rot = p.segs[si + 1].shift;
               mbar_arrive(&q_ready[m]);  // nothing to re-stage for invalid rows
@@ -1002,7 +1008,7 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
 #pragma unroll
             for (int c = 0; c < kBN; ++c) x[c] = (keep[c >> 5] >> (c & 31)) & 1u ? x[c] : -INFINITY;
           }
-          if (p.pair_count && valid) n_pairs += count_visible(x);
+          if (!CM && p.pair_count && valid) n_pairs += count_visible(x);
           float mx[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) mx[i] = fmax3(x[i], x[i + 8], x[i + 16]);
@@ -1098,13 +1104,13 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
       mbar_wait(&o_full[m], wk & 1);
       tc_fence_after();
       if (trow == 0) WSTAMP(m * 4 + 2, wk);
-      epilogue_row<HDP>(p, t_o, valid, t, head, w.out_mode, xr.part_row, l_sum, m_used);
+      epilogue_row<HDP, CM>(p, t_o, valid, t, head, w.out_mode, xr.part_row, l_sum, m_used);
       tc_fence_before();
       mbar_arrive(&o_free[m]);  // O(m) may be overwritten by the next work's first P.V
       if (trow == 0) WSTAMP(m * 4 + 3, wk);
       if (trow == 0) CSTAMP(5 + m);
     }
-    if (p.pair_count) flush_pair_count(p.pair_count, n_pairs);
+    if (!CM && p.pair_count) flush_pair_count(p.pair_count, n_pairs);
   }
 
   tc_fence_before();
@@ -1589,10 +1595,10 @@ static int num_sms() {
   return n;
 }
 
-template <int HDP, int NUM_M>
+template <int HDP, int NUM_M, bool CM = false>
 static int launch_attn(const DbsaAttnArgs &a, const AttnParams &p, const CUtensorMap *maps, cudaStream_t s) {
   using C = AttnCfg<HDP, NUM_M>;
-  auto kern = dbsa_attn_kernel<HDP, NUM_M>;
+  auto kern = dbsa_attn_kernel<HDP, NUM_M, CM>;
   static thread_local bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -1711,6 +1717,19 @@ extern "C" int dbsa_attention(const DbsaAttnArgs *args, void *stream) {
       case 32: return launch_attn<32, 1>(a, p, maps, s);
       case 64: return launch_attn<64, 1>(a, p, maps, s);
       case 128: return launch_attn<128, 1>(a, p, maps, s);
+    }
+  }
+  // the chunk-major specialisation: the caller vouches that every work has one
+  // segment and writes a partial (one_seg_partials); the launcher checks the rest
+  const bool cm = a.one_seg_partials && a.num_m == 2 && a.row_map && a.part_bf16 && a.part_chunk_rows > 0 &&
+                  !a.pair_count && !p.dbg && a.rope_f16 && a.head_dim == a.hd_pad && a.hd_pad >= 16 &&
+                  (a.q_tok_stride & 7) == 0;
+  if (cm) {
+    switch (a.hd_pad) {
+      case 16: return launch_attn<16, 2, true>(a, p, maps, s);
+      case 32: return launch_attn<32, 2, true>(a, p, maps, s);
+      case 64: return launch_attn<64, 2, true>(a, p, maps, s);
+      case 128: return launch_attn<128, 2, true>(a, p, maps, s);
     }
   }
   switch (a.hd_pad * 10 + a.num_m) {

@@ -1060,7 +1060,8 @@ class ChunkMajorSchedule:
                       pool=pool, aux=nt.aux(), n_heads=c.n_heads, n_kv_heads=c.n_kv_heads, head_dim=c.head_dim,
                       works_dev=self.works, n_works=self.n_works, segs_dev=self.segs_ptr(layer), num_m=self.num_m,
                       out=out, out_tok_stride=qw, part_o=self.part_o if part_o is None else part_o,
-                      part_lse=self.part_lse if part_lse is None else part_lse, row_map=self.row_map)
+                      part_lse=self.part_lse if part_lse is None else part_lse, row_map=self.row_map,
+                      one_seg_partials=True)
 
 
 def chunk_major_tables(tables, n_new, pos_host, aux_row0, prefixes, gs: int, hkv: int, num_m: int = 2,

@@ -142,7 +142,7 @@ def chunk_rows_of(part_o, head_dim: int) -> int:
 def attention(*, q, q_tok_stride, tok_pos, tok_lo, rope, pool, aux, n_heads, n_kv_heads, head_dim,
               works_dev, n_works, segs_dev, num_m, out, out_tok_stride, part_o=None, part_lse=None,
               row_map=None, pair_count=None, cta_works=None, n_ctas=0, after_kv_write=False,
-              part_chunk_rows=None):
+              part_chunk_rows=None, one_seg_partials=False):
     """Launch K1/K3.  `pool` / `aux` are (k_planes, v_planes, rows, layers); `row_map`
     (ROWMAP_DTYPE, device) backs DBSA_OUT_MAPPED works; `pair_count` (int64 [1],
     device) makes the kernel add the (row, key) pairs it unmasked, all heads;
@@ -150,7 +150,9 @@ def attention(*, q, q_tok_stride, tok_pos, tok_lo, rope, pool, aux, n_heads, n_k
     [cta_works[b], cta_works[b+1]) (two-tile kernel only); after_kv_write: the
     launch directly follows the layer's K2w page write, so Q staging may
     overlap it (DbsaAttnArgs.pdl_early_q); part_chunk_rows: the partials'
-    layout (None = chunk_rows_of(part_o))."""
+    layout (None = chunk_rows_of(part_o)); one_seg_partials: every work has
+    one segment and writes a partial (the chunk-major schedule), which allows
+    the specialised kernel instance (DbsaAttnArgs.one_seg_partials)."""
     kp, vp, prow, pl = pool
     ka, va, arow, al = aux if aux is not None else (None, None, 0, 0)
     a = nat.AttnArgs(
@@ -165,7 +167,8 @@ def attention(*, q, q_tok_stride, tok_pos, tok_lo, rope, pool, aux, n_heads, n_k
         part_bf16=int(part_o is not None and part_o.element_size() == 2), pair_count=nat.ptr(pair_count),
         cta_works=nat.ptr(cta_works), n_ctas=int(n_ctas), pdl_early_q=int(bool(after_kv_write)),
         rope_f16=nat.ptr(getattr(rope, "f16", None)),
-        part_chunk_rows=chunk_rows_of(part_o, head_dim) if part_chunk_rows is None else part_chunk_rows)
+        part_chunk_rows=chunk_rows_of(part_o, head_dim) if part_chunk_rows is None else part_chunk_rows,
+        one_seg_partials=int(bool(one_seg_partials)))
     nat.check(nat.load_library().dbsa_attention(ctypes.byref(a), nat.stream_handle()))
     _launched()
 
