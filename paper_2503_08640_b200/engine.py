@@ -709,6 +709,13 @@ def _split_bf16() -> bool:
     return os.environ.get("DBSA_SPLIT_BF16", "1") == "1"
 
 
+def _split_cm() -> bool:
+    # DBSA_SPLIT_CM=0: split-KV launches keep the generic kernel instance
+    import os
+
+    return os.environ.get("DBSA_SPLIT_CM", "1") != "0"
+
+
 class AttnSchedule:
     """K3 works + segments (+ K3m merge groups) of a batch against chunk tables.
 
@@ -820,6 +827,9 @@ class AttnSchedule:
             self.cta_works = ops.to_device(np.asarray(bounds_cta, dtype=np.int32), dm.device)
         self.kv_tokens = kv_tok
         self.n_works, self.n_segs, self.n_merge = len(works), len(segs), len(merges)
+        # every work one segment, writing a partial (e.g. batch-1 packed splits):
+        # the launch may use the specialised kernel instance (one_seg_partials)
+        self.one_seg = _split_cm() and bool(works) and all(w[5] - w[4] == 1 and w[7] != 0 for w in works)
         self.works = ops.to_device(_work_array(works), dev)
         seg_arr = _seg_array(segs)
         self.segs = ops.to_device(_per_layer_segs(seg_arr, c.n_layers), dev)
@@ -835,6 +845,7 @@ class AttnSchedule:
             templates = _split_templates()
             templates[key] = dict(
                 works=self.works, merges=self.merges, cta_works=self.cta_works, n_ctas=self.n_ctas, segs=seg_arr,
+                one_seg=self.one_seg,
                 seg_job=src[:, 0], seg_chunk=src[:, 1], n_works=self.n_works, n_merge=self.n_merge,
                 max_rows=self.max_rows, part_rows=part_rows, kv_tokens=kv_tok, part_dtype=self._part_spec[2])
             while len(templates) > _SPLIT_TEMPLATES_MAX:
@@ -858,6 +869,7 @@ class AttnSchedule:
         segs["row0"][~full] = np.asarray(nt.aux_row0, np.int64)[job[~full]]
         min_shift = min(0, int(allch[:, 2].min())) if len(allch) else 0
         self.works, self.merges, self.cta_works, self.n_ctas = tpl["works"], tpl["merges"], tpl["cta_works"], tpl["n_ctas"]
+        self.one_seg = tpl["one_seg"]
         self.n_works, self.n_segs, self.n_merge = tpl["n_works"], len(segs), tpl["n_merge"]
         self.segs = ops.to_device(_per_layer_segs(segs, c.n_layers), dm.device)
         self.max_rows, self.part_rows, self.kv_tokens = tpl["max_rows"], tpl["part_rows"], tpl["kv_tokens"]
@@ -898,7 +910,7 @@ class AttnSchedule:
                       works_dev=self.works, n_works=self.n_works, segs_dev=self.segs_ptr(layer), num_m=nt.num_m,
                       out=out, out_tok_stride=qw, part_o=self.part_o if part_o is None else part_o,
                       part_lse=self.part_lse if part_lse is None else part_lse, cta_works=self.cta_works,
-                      n_ctas=self.n_ctas, after_kv_write=True)
+                      n_ctas=self.n_ctas, after_kv_write=True, one_seg_partials=self.one_seg)
 
 
 # Cost model of pack_works, in key tiles: a CTA's first work pays the cold
@@ -1598,7 +1610,7 @@ def plan_key(plan, scorer):
     if isinstance(sc, ChunkMajorSchedule):
         tables = ("chunk", sc.row_map.numel(), sc.num_m, plan.last.row_map.numel() if plan.last is not None else -1)
     else:
-        tables = ("query", sc.n_works, sc.n_segs, sc.n_ctas)
+        tables = ("query", sc.n_works, sc.n_segs, sc.n_ctas, getattr(sc, "one_seg", False))
     return (plan.new.n_tok, tuple(plan.new.n_new), plan.new.n_pages, tables, sc.n_merge, sc.part_rows,
             int(scorer.rows.numel()), int(scorer.keep.numel()), scorer.n_out, plan.new.num_m)
 
