@@ -1721,7 +1721,7 @@ extern "C" int dbsa_attention(const DbsaAttnArgs *args, void *stream) {
   }
   // the chunk-major specialisation: the caller vouches that every work has one
   // segment and writes a partial (one_seg_partials); the launcher checks the rest
-  const bool cm = a.one_seg_partials && a.num_m == 2 && a.row_map && a.part_bf16 && a.part_chunk_rows > 0 &&
+  const bool cm = a.one_seg_partials && a.num_m == 2 && a.part_bf16 && a.part_chunk_rows > 0 &&
                   !a.pair_count && !p.dbg && a.rope_f16 && a.head_dim == a.hd_pad && a.hd_pad >= 16 &&
                   (a.q_tok_stride & 7) == 0;
   if (cm) {
