@@ -176,7 +176,7 @@ def _stage1_case(hd, H, Hkv, lengths, j=2, layer=0, layers=1, num_m=None, rope_f
 
 
 @pytest.mark.parametrize("num_m", [1, 2])
-@pytest.mark.parametrize("hd,H,Hkv", [(128, 8, 2), (128, 4, 4), (64, 8, 2), (16, 4, 2), (32, 6, 3), (8, 4, 2)])
+@pytest.mark.parametrize("hd,H,Hkv", [(128, 8, 2), (128, 4, 4), (64, 8, 2), (16, 4, 2), (32, 6, 3), (32, 6, 2), (8, 4, 2)])
 def test_stage1_block_sparse_attention(hd, H, Hkv, num_m):
     """num_m 1: single-M-tile kernel (Q in TMEM); 2: two ping-ponged M tiles."""
     worst = _stage1_case(hd, H, Hkv, [150, 64, 97, 200, 33], num_m=num_m)
@@ -354,7 +354,7 @@ class _DM:
 
 
 @pytest.mark.parametrize("schedule", ["chunk", "query", "chunk-padded"])
-@pytest.mark.parametrize("hd,H,Hkv", [(128, 8, 2), (64, 4, 4), (32, 8, 1), (128, 4, 4), (128, 16, 2)])
+@pytest.mark.parametrize("hd,H,Hkv", [(128, 8, 2), (64, 4, 4), (32, 8, 1), (128, 4, 4), (128, 16, 2), (64, 6, 2)])
 def test_stage2_batch_schedules_vs_float64(schedule, hd, H, Hkv):
     """(128, 4, 4): MHA at head_dim 128 (C4's layout, 256-token chunk works);
     (128, 16, 2): GQA-8 (the 70B shape's grouping, 32-token works)."""
