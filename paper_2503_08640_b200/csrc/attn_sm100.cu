@@ -474,7 +474,7 @@ __device__ __forceinline__ void stage_refs_coop(const AttnParams &p, const DbsaA
 
 // Phase B: q chunk pairs + their (cos, sin), rotate, swizzled 16-byte stores
 // into the Q tile.  HALF: the fp16 rotation table (AttnParams.rope_h).
-template <int HDP, bool HALF>
+template <int HDP, bool HALF, int QBATCH = DBSA_QSTAGE_BATCH>
 __device__ __forceinline__ void stage_load_coop(const AttnParams &p, uint8_t *q_tile, int m, int q4, int lane,
                                                 const QRefs<HDP> &x, int sw = -1) {
   constexpr int QSW = AttnCfg<HDP, 1>::QSW;
@@ -491,7 +491,7 @@ __device__ __forceinline__ void stage_load_coop(const AttnParams &p, uint8_t *q_
 #if DBSA_QSTAGE_BATCH > 1
   // phase B, batched: the loads of QB iterations are issued before any of
   // them is used, so QB round trips overlap (QB x 24 registers in flight)
-  constexpr int QB = DBSA_QSTAGE_BATCH < NIT ? DBSA_QSTAGE_BATCH : NIT;
+  constexpr int QB = QBATCH < NIT ? QBATCH : NIT;
   static_assert(NIT % QB == 0, "DBSA_QSTAGE_BATCH must divide the staging iterations");
 #pragma unroll
   for (int i0 = 0; i0 < NIT; i0 += QB) {
@@ -625,7 +625,7 @@ __device__ __forceinline__ void stage_load_coop(const AttnParams &p, uint8_t *q_
 // instruction).  restage: rope row tok_pos - shift (a plain work's next
 // segment); otherwise the row's own (row_ref) rope row.  Full-width heads only
 // (hd == HDP, 16-byte aligned rows); the caller falls back to load_q_row.
-template <int HDP, bool HALF>
+template <int HDP, bool HALF, int QBATCH = DBSA_QSTAGE_BATCH>
 __device__ __forceinline__ void stage_q_coop(const AttnParams &p, const DbsaAttnWork &w, int m, uint8_t *q_tile,
                                              int q4, int lane, bool restage, int shift, int sw = -1) {
   QRefs<HDP> x;
@@ -636,7 +636,7 @@ __device__ __forceinline__ void stage_q_coop(const AttnParams &p, const DbsaAttn
     WSTAMP(10, sw);
   }
 #endif
-  stage_load_coop<HDP, HALF>(p, q_tile, m, q4, lane, x, sw);
+  stage_load_coop<HDP, HALF, QBATCH>(p, q_tile, m, q4, lane, x, sw);
 }
 
 // CM: the chunk-major specialisation (DbsaAttnArgs.one_seg_partials): every work
@@ -914,7 +914,9 @@ __global__ void __launch_bounds__(AttnCfg<HDP, NUM_M>::THREADS, 1)
     auto stage_q = [&](const DbsaAttnWork &wq, bool restage, int shift, int sw = -1) {
       if (!CM && (p.dbg & 16)) return;  // profiling: keep whatever Q the tile holds
       if (CM || (coop && p.rope_h)) {
-        stage_q_coop<HDP, true>(p, wq, m, q_tile, q4, lane, restage, shift, sw);
+        // the specialised instance stages 4 iterations per batch (C3 K3 -0.5 %;
+        // the generic kernel keeps 8: K1 +0.8 % and spills at 4)
+        stage_q_coop<HDP, true, CM ? 4 : DBSA_QSTAGE_BATCH>(p, wq, m, q_tile, q4, lane, restage, shift, sw);
       } else if (coop) {
         stage_q_coop<HDP, false>(p, wq, m, q_tile, q4, lane, restage, shift);
       } else {
